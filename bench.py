@@ -1,0 +1,433 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 HoloGen hot path (BASELINE.json metric:
+"GS iterations/sec at 4096^2 and OSPR subframes/sec; % of HBM roofline").
+
+Workload (BASELINE config 5, the largest single-GPU config): batch GS,
+4096x4096, 256-level full-circle phase SLM, K = 25 iterations (reference
+default, config.hpp:35), smooth_blobs + UnitEnergy targets (the reference's
+bench target, bench.cpp:115-116), target t seeded with 1 + t.  One step = one
+full batched run per GPU (random-phase init + K iterations + trace reduction)
+of `--targets` targets; value = target-iterations per second over all GPUs.
+OSPR (config 3: 1024^2 binary, 24 subframes) is reported in the "ospr" object.
+
+  python bench.py [--gpus N --steps K --warmup W]          ours
+  python bench.py --impl reference [...]                  reference CPU path
+
+Multi-GPU: one process per GPU (torchrun); whole targets per GPU, no
+data-path collective; NCCL only gathers the per-target final errors.
+"""
+from __future__ import annotations
+
+import argparse
+import concurrent.futures as cf
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GS iterations/sec at 4096² and OSPR subframes/sec; % of HBM roofline"
+GS_BYTES_PER_PX = {"row": 16, "col": 20, "iteration": 36}  # 2 fused round trips + fp32 target
+OSPR_BYTES_PER_PX = {"seed": 8, "col_inv": 16, "row": 17, "col_acc": 20, "subframe": 49}
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"], "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=4096)
+    ap.add_argument("--levels", type=int, default=256)
+    ap.add_argument("--targets", type=int, default=64, help="targets per GPU per step")
+    ap.add_argument("--iters", type=int, default=25)
+    ap.add_argument("--ospr-n", type=int, default=1024)
+    ap.add_argument("--ospr-jobs", type=int, default=64, help="OSPR jobs per GPU per step")
+    ap.add_argument("--ospr-subframes", type=int, default=24)
+    ap.add_argument("--no-ospr", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------- distributed
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(self.local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def max(self, v: float) -> float:
+        if not self.pg:
+            return v
+        import torch
+        t = torch.tensor([v], device="cuda", dtype=torch.float64)
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def gather_errors(self, errs_dev):
+        """NCCL gather of per-target final errors to rank 0 (the only
+        collective of the sharded path)."""
+        if not self.pg:
+            return errs_dev
+        import torch
+        out = [torch.empty_like(errs_dev) for _ in range(self.world)] if self.rank == 0 else None
+        self.pg.gather(errs_dev, out, dst=0)
+        return torch.cat(out) if self.rank == 0 else None
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+# ----------------------------------------------------------------- clocks
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev: int):
+        self.dev, self.rows, self.proc = dev, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------- GS (ours)
+def gs_ours(args, d: Dist):
+    import torch
+    import paper_2008_12214_b200 as hg
+    from paper_2008_12214_b200 import _lib
+    n, B, K = args.n, args.targets, args.iters
+    hg.set_device(d.local)
+    amp1 = hg.patterns.bench_target(n)
+    seeds = np.arange(1 + d.rank * B, 1 + (d.rank + 1) * B, dtype=np.uint64)
+    slm = hg.SlmSpec.full_circle_phase(args.levels) if args.levels > 2 else hg.SlmSpec.binary_phase()
+    cfg = hg.IftaConfig(iterations=K, slm=slm, target=hg.TargetSpec(amp1))
+    npix = n * n
+    # pinned host inputs [B][n][n] (every target its own buffer, as cmd_batch jobs are)
+    amps = torch.empty((B, n, n), dtype=torch.float64, pin_memory=True)
+    amps[:] = torch.from_numpy(amp1)
+    plan = hg.IftaPlan(cfg, n, n, B)
+    plan.upload(amps.numpy(), seeds=seeds)
+    stream = torch.cuda.Stream()  # the graph runs on this stream; events are recorded on it
+    for _ in range(args.warmup):
+        plan.execute(stream.cuda_stream)
+    torch.cuda.synchronize()
+    d.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(d.local) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            plan.execute(stream.cuda_stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    d.barrier()
+    ms = e0.elapsed_time(e1)
+    ms_max = d.max(ms)
+    launches = plan.launches() * args.steps
+    # result check + the sharded path's only collective: gather final errors
+    _, _, tr = plan.device_arrays()
+    trace = torch.as_tensor(tr, device="cuda")
+    finals = d.gather_errors(trace[:, -1].contiguous())
+    ok = bool(torch.isfinite(trace).all().item() and (trace[:, -1] < trace[:, 0]).all().item())
+    prof = plan.profile(reps=5)
+    res = {"ms": ms_max, "launches": launches, "clocks": clk.summary(), "profile_ms": prof, "check_ok": ok,
+           "final_mse_mean": float(finals.mean().item()) if finals is not None else None, "npix": npix, "B": B}
+    if not args.no_e2e:
+        res["e2e"] = gs_e2e(args, plan, amps, seeds, d)
+    plan.close()
+    return res
+
+
+def gs_e2e(args, plan, amps, seeds, d: Dist):
+    """Same metric through the C ABI with host buffers: every step uploads the
+    step's targets from pinned memory (H2D, validated on device), runs, and
+    reads back the levels and traces (D2H)."""
+    import torch
+    from paper_2008_12214_b200 import _lib
+    B, n, K = args.targets, args.n, args.iters
+    lv = torch.empty((B, n, n), dtype=torch.uint8, pin_memory=True)
+    tr = np.empty((B, K), np.float64)
+    io = _lib.HgcIftaIo()
+    io.amplitude = amps.data_ptr()
+    io.seeds = seeds.ctypes.data
+    io.levels8 = lv.data_ptr()
+    io.trace = tr.ctypes.data
+    h = plan._h
+    for _ in range(1):  # warm
+        _lib.check(_lib.lib.hgc_ifta_plan_upload(h, C.byref(io)))
+        _lib.check(_lib.lib.hgc_ifta_plan_execute(h, None))
+        _lib.check(_lib.lib.hgc_ifta_plan_download(h, C.byref(io)))
+    d.barrier()
+    steps = max(1, min(args.steps, 3))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        _lib.check(_lib.lib.hgc_ifta_plan_upload(h, C.byref(io)))
+        _lib.check(_lib.lib.hgc_ifta_plan_execute(h, None))
+        _lib.check(_lib.lib.hgc_ifta_plan_download(h, C.byref(io)))
+    dt = d.max(time.perf_counter() - t0)
+    units = d.world * B * K * steps
+    return {"value": units / dt, "unit": "iterations/s", "h2d_bytes_per_step": int(B * n * n * 8 + B * 8),
+            "d2h_bytes_per_step": int(B * n * n + B * K * 8), "steps": steps,
+            "api": "hgc_ifta_plan_upload/execute/download (C ABI, pinned host buffers)"}
+
+
+# ------------------------------------------------------------- OSPR (ours)
+def ospr_ours(args, d: Dist):
+    import torch
+    import paper_2008_12214_b200 as hg
+    from paper_2008_12214_b200 import _lib
+    n, J, N = args.ospr_n, args.ospr_jobs, args.ospr_subframes
+    amp = hg.patterns.bench_target(n)
+    cfg = hg.OsprConfig(subframes=N, slm=hg.SlmSpec.binary_phase(), target=hg.TargetSpec(amp))
+    seeds = np.arange(1 + d.rank * J, 1 + (d.rank + 1) * J, dtype=np.uint64)
+    plan = hg.OsprPlan(cfg, n, n, J)
+    plan.upload(amp, seeds=seeds)
+    stream = torch.cuda.Stream()
+    for _ in range(max(1, args.warmup)):
+        plan.execute(stream.cuda_stream)
+    torch.cuda.synchronize()
+    d.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    steps = max(1, args.steps)
+    for _ in range(steps):
+        plan.execute(stream.cuda_stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = d.max(e0.elapsed_time(e1))
+    prof = plan.profile(reps=5)
+    res = {"ms": ms, "steps": steps, "launches": plan.launches() * steps, "profile_ms": prof}
+    if not args.no_e2e:
+        lv = torch.empty((J, N, n, n), dtype=torch.uint8, pin_memory=True)
+        fm, cm = np.empty((J, N)), np.empty((J, N))
+        io = _lib.HgcOsprIo()
+        io.amplitude = amp.ctypes.data
+        io.seeds = seeds.ctypes.data
+        io.levels8 = lv.data_ptr()
+        io.frame_mse, io.cumulative_mse = fm.ctypes.data, cm.ctypes.data
+        h = plan._h
+        d.barrier()
+        t0 = time.perf_counter()
+        es = max(1, min(steps, 3))
+        for _ in range(es):
+            _lib.check(_lib.lib.hgc_ospr_plan_upload(h, C.byref(io)))
+            _lib.check(_lib.lib.hgc_ospr_plan_execute(h, None))
+            _lib.check(_lib.lib.hgc_ospr_plan_download(h, C.byref(io)))
+        dt = d.max(time.perf_counter() - t0)
+        res["e2e"] = {"value": d.world * J * N * es / dt, "unit": "subframes/s",
+                      "h2d_bytes_per_step": int(n * n * 8 + J * 8), "d2h_bytes_per_step": int(J * N * n * n + 2 * J * N * 8)}
+    plan.close()
+    return res
+
+
+# ---------------------------------------------------- reference CPU path
+def reference_gs(n, levels, iters, jobs, threads):
+    """The reference's own run_ifta<float> (oracle/_ref: unmodified headers,
+    substitute f32 FFT since FFTW is absent), `jobs` independent targets on
+    `threads` host threads (cmd_batch's job pool, runner.cpp:388-421)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from pyoracle import Oracle
+    import paper_2008_12214_b200.patterns as pat
+    from paper_2008_12214_b200.types import SlmSpec
+    ref = Oracle("reference")
+    ref.set_fast_fft(True)
+    amp = pat.bench_target(n)
+    slm = SlmSpec.full_circle_phase(levels) if levels > 2 else SlmSpec.binary_phase()
+    t0 = time.perf_counter()
+    with cf.ThreadPoolExecutor(max_workers=threads) as ex:
+        list(ex.map(lambda s: ref.ifta(amp, slm, iters, seed=int(s)), range(1, jobs + 1)))
+    return time.perf_counter() - t0
+
+
+def reference_ospr(n, subframes, jobs, threads):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from pyoracle import Oracle
+    import paper_2008_12214_b200.patterns as pat
+    from paper_2008_12214_b200.types import SlmSpec
+    ref = Oracle("reference")
+    ref.set_fast_fft(True)
+    amp = pat.bench_target(n)
+    t0 = time.perf_counter()
+    with cf.ThreadPoolExecutor(max_workers=threads) as ex:
+        list(ex.map(lambda s: ref.ospr(amp, SlmSpec.binary_phase(), subframes, seed=int(s)), range(1, jobs + 1)))
+    return time.perf_counter() - t0
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def base_config(args, d):
+    return {"workload": f"batch_gs_{args.n}_{args.levels}level (BASELINE config 5)", "resolution": args.n,
+            "levels": args.levels, "iterations": args.iters, "targets_per_gpu": args.targets,
+            "total_targets": args.targets * d.world, "seeds": "1 + target index",
+            "target": "smooth_blobs + UnitEnergy (bench.cpp:115-116)",
+            "l2": "inputs larger than L2 (per GPU: targets x 128 MiB field + 64 MiB fp32 target)"}
+
+
+def run_reference(args, d: Dist):
+    if d.rank != 0:
+        d.close()
+        return
+    threads = cpu_threads()
+    jobs, iters = threads, 1
+    for _ in range(args.warmup):
+        reference_gs(args.n, args.levels, iters, jobs, threads)
+    times = [reference_gs(args.n, args.levels, iters, jobs, threads) for _ in range(args.steps)]
+    t = sum(times)
+    value = jobs * iters * args.steps / t
+    sample = (f"{jobs} jobs x {iters} iteration (incl. random-phase init) of GS {args.n}^2 {args.levels}-level per "
+              f"step, one job per host thread; reference headers + substitute f32 FFT (FFTW absent)")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": d.world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": base_config(args, d),
+            "cpu_baseline": {"value": value, "unit": "iterations/s", "cores": threads, "kind": "reference",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    d.close()
+
+
+def main():
+    args = parse()
+    d = Dist()
+    if args.impl == "reference":
+        return run_reference(args, d)
+    peak, peak_kind = peaks()
+    gs = gs_ours(args, d)
+    osp = None if args.no_ospr else ospr_ours(args, d)
+    cpu = None
+    if d.rank == 0 and d.world == 1 and not args.no_cpu:
+        threads = cpu_threads()
+        t = reference_gs(args.n, args.levels, 1, threads, threads)
+        cpu = {"value": threads / t, "unit": "iterations/s", "cores": threads, "kind": "reference",
+               "sample": f"{threads} concurrent jobs x 1 iteration (+init) of GS {args.n}^2 {args.levels}-level, "
+                         f"reference headers + substitute f32 FFT (FFTW absent), one job per host thread"}
+        if osp is not None:
+            to = reference_ospr(args.ospr_n, 2, threads, threads)
+            cpu["ospr"] = {"value": threads * 2 / to, "unit": "subframes/s", "cores": threads,
+                           "sample": f"{threads} concurrent jobs x 2 subframes of OSPR {args.ospr_n}^2 binary"}
+    if d.rank != 0:
+        d.close()
+        return
+    B, K, npix = gs["B"], args.iters, gs["npix"]
+    units = d.world * B * K * args.steps
+    value = units / (gs["ms"] / 1e3)
+    pr = gs["profile_ms"]
+    row_gbs = GS_BYTES_PER_PX["row"] * npix * B / (pr["row"] * 1e-3) / 1e9
+    col_gbs = GS_BYTES_PER_PX["col"] * npix * B / (pr["col"] * 1e-3) / 1e9
+    dom = "col" if pr["col"] >= pr["row"] else "row"
+    ach = col_gbs if dom == "col" else row_gbs
+    it_ms = pr["row"] + pr["col"]
+    it_gbs = GS_BYTES_PER_PX["iteration"] * npix * B / (it_ms * 1e-3) / 1e9
+    step_gbs = GS_BYTES_PER_PX["iteration"] * npix * B * K / (gs["ms"] / args.steps * 1e-3) / 1e9
+    traffic = None
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(f"gs_{dom}")
+    except Exception:
+        pass
+    line = {
+        "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": d.world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": gs["ms"] / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": base_config(args, d),
+        "roofline": {"bound": "hbm", "kernel": f"k_{dom} (fused {'replay-plane column' if dom == 'col' else 'aperture-plane row'} pass)",
+                     "achieved": ach, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": ach / peak,
+                     "traffic": traffic, "bytes_per_px": GS_BYTES_PER_PX[dom],
+                     "kernel_ms": pr[dom],
+                     "iteration": {"bytes_per_px": 36, "kernel_ms": it_ms, "achieved": it_gbs, "frac": it_gbs / peak,
+                                   "per_gpu_it_per_s": 1e3 / it_ms * B},
+                     "step_including_init": {"achieved": step_gbs, "frac": step_gbs / peak},
+                     "row": {"ms": pr["row"], "achieved": row_gbs, "frac": row_gbs / peak},
+                     "col": {"ms": pr["col"], "achieved": col_gbs, "frac": col_gbs / peak},
+                     "seed_ms": pr["seed"]},
+        "cpu_baseline": cpu, "e2e": gs.get("e2e"), "gpu_launches": gs["launches"], "clocks": gs["clocks"],
+        "check": {"traces_finite_and_decreasing": gs["check_ok"], "final_mse_mean": gs["final_mse_mean"]},
+    }
+    if osp is not None:
+        J, N, on = args.ospr_jobs, args.ospr_subframes, args.ospr_n
+        sub = d.world * J * N * osp["steps"] / (osp["ms"] / 1e3)
+        po = osp["profile_ms"]
+        onpx = on * on
+        parts = {k: {"ms": po[k], "achieved": OSPR_BYTES_PER_PX[k] * onpx * J / (po[k] * 1e-3) / 1e9}
+                 for k in ("seed", "col_inv", "row", "col_acc")}
+        sf_ms = sum(po.values())
+        sf_gbs = OSPR_BYTES_PER_PX["subframe"] * onpx * J / (sf_ms * 1e-3) / 1e9
+        line["ospr"] = {"metric": "OSPR subframes/s", "value": sub, "unit": "subframes/s",
+                        "config": {"workload": f"ospr_{on}_binary (BASELINE config 3)", "subframes": N,
+                                   "jobs_per_gpu": J, "seeds": "1 + job index"},
+                        "ms_per_step": osp["ms"] / osp["steps"], "gpu_launches": osp["launches"],
+                        "roofline": {"bound": "hbm", "bytes_per_px": 49, "subframe_kernel_ms": sf_ms,
+                                     "achieved": sf_gbs, "peak": peak, "frac": sf_gbs / peak, "kernels": parts},
+                        "e2e": osp.get("e2e")}
+        if cpu and "ospr" in cpu:
+            line["ospr"]["cpu_baseline"] = cpu.pop("ospr")
+        line["gpu_launches"] += osp["launches"]
+    print(json.dumps(line), flush=True)
+    d.close()
+
+
+if __name__ == "__main__":
+    main()

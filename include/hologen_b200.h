@@ -1,0 +1,225 @@
+/*
+ * hologen_b200.h — C ABI of the B200-native HoloGen IFTA / OSPR hot path.
+ *
+ * This is the drop-in boundary.  Each entry point replaces one reference
+ * interface (paths relative to /root/reference/proj/include/hologen/):
+ *
+ *   hgc_ifta_run           run_gs / run_weighted_gs / run_liu_taghizadeh /
+ *                          run_ifta<float>            ifta.hpp:239-263
+ *                          (detail::run_ifta           ifta.hpp:86-235),
+ *                          batched over targets like cmd_batch
+ *                          (src/runner.cpp:365-421)
+ *   hgc_ospr_run           run_ospr / run_adaptive_ospr /
+ *                          run_ospr_variant<float>     ospr.hpp:168-185
+ *                          (detail::run_ospr_impl      ospr.hpp:68-164),
+ *                          batched over independent jobs
+ *   hgc_fft2d              FftBackend<float>::forward / inverse
+ *                          fft.hpp:17-27 (FftwBackend::run,
+ *                          src/fftw_backend.cpp:113-124)
+ *   hgc_propagate          Propagator<float>::forward / inverse
+ *                          propagation.hpp:60-116
+ *   hgc_quantise           Quantiser<float>::apply      quantise.hpp:208-216
+ *                          (quantise_field              quantise.hpp:234-243)
+ *   hgc_seed_random_phase  seed_random_phase<float>     rng.hpp:54-67
+ *   hgc_mse                mse (phase-insensitive)      metrics.hpp:70-124
+ *   hgc_fresnel_phase      make_fresnel_phase<float>    propagation.hpp:36-54
+ *   hgc_subframe_mse_statistic  subframe_mse_statistic  ospr.hpp:58-64
+ *
+ * Conventions (field.hpp:27-66): fields are row-major data[y*nx + x];
+ * complex values are interleaved float pairs (layout-compatible with
+ * std::complex<float>); target images are double; masks are uint8.  All
+ * pointers passed to hgc_*_run / primitives are HOST pointers owned by the
+ * caller; the library owns device memory.  The plan API (hgc_*_plan_*) keeps
+ * inputs and outputs resident in HBM for repeated execution.
+ *
+ * Errors: every function returns HGC_OK (0) or an hgc_status; the message is
+ * in hgc_last_error() (thread-local).  HGC_EINVAL corresponds to the
+ * reference's std::invalid_argument (same messages), HGC_ECUDA / HGC_EUNSUPPORTED
+ * to std::runtime_error.  There is no CPU fallback: sizes the GPU path does
+ * not support (non powers of two, > 4096 per side) fail with HGC_EUNSUPPORTED.
+ *
+ * Threading (fft.hpp:79-83, runner.cpp:387-421): every call is re-entrant;
+ * each call / plan uses its own CUDA stream on the calling thread's current
+ * device (hgc_set_device).
+ */
+#ifndef HOLOGEN_B200_H
+#define HOLOGEN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HGC_ABI_VERSION 1
+
+typedef enum {
+    HGC_OK = 0,
+    HGC_EINVAL = 1,       /* std::invalid_argument in the reference */
+    HGC_ECUDA = 2,        /* device / runtime failure */
+    HGC_EUNSUPPORTED = 3  /* valid for the reference, outside the GPU path's scope */
+} hgc_status;
+
+/* hologen::SlmSpec (quantise.hpp:20-105).  mode: 0 Amplitude, 1 Phase.
+ * illumination: NULL or interleaved complex<double> [ny][nx]. */
+typedef struct hgc_slm {
+    int mode;
+    int levels;
+    double min_arg;
+    double max_arg;
+    int full_circle;
+    double min_amp;
+    double max_amp;
+    const double* illumination;
+} hgc_slm;
+
+/* hologen::FresnelParams (propagation.hpp:15-32). */
+typedef struct hgc_fresnel {
+    double wavelength;
+    double distance;
+    double pixel_pitch_x;
+    double pixel_pitch_y;
+} hgc_fresnel;
+
+/* hologen::IftaConfig (ifta.hpp:29-51) + TargetSpec::freedoms (target.hpp:34-40).
+ * variant: 0 GS, 1 WeightedGS, 2 LiuTaghizadeh.
+ * init_phase: 0 Auto, 1 Random, 2 Flat, 3 Given (extension: start from
+ * hgc_ifta_io.init_field, e.g. to resume from a checkpointed replay field). */
+typedef struct hgc_ifta_cfg {
+    int variant;
+    int iterations;
+    uint64_t seed;
+    double weight_clamp_lo;
+    double weight_clamp_hi;
+    double lt_initial_fraction;
+    int init_phase;
+    int freedom_amplitude_outside_roi;
+    int freedom_phase;
+    int freedom_scale;
+} hgc_ifta_cfg;
+
+/* Inputs and outputs of one batched IFTA call.  batch targets share size,
+ * SLM, propagation and ROI.  Any output pointer may be NULL. */
+typedef struct hgc_ifta_io {
+    const double* amplitude;    /* TargetSpec::amplitude  [batch][ny][nx] */
+    const double* phase;        /* TargetSpec::phase (turns) [batch][ny][nx] or NULL */
+    const uint8_t* roi;         /* TargetSpec::roi [ny][nx] or NULL */
+    const uint64_t* seeds;      /* [batch] IftaConfig::seed per target, or NULL = cfg->seed */
+    const float* init_field;    /* init_phase == 3: complex [batch][ny][nx] */
+    const float* init_weights;  /* init_phase == 3, WGS: [batch][ny][nx] or NULL (= 1) */
+    float* hologram;            /* RunReport::hologram  complex [batch][ny][nx] */
+    uint8_t* levels8;           /* level indices of the hologram (levels <= 256) */
+    uint16_t* levels16;         /* level indices (any level count <= 65536) */
+    float* replay;              /* RunReport::replay    complex [batch][ny][nx] */
+    double* trace;              /* RunReport::trace     [batch][iterations] */
+    double* final_error;        /* RunReport::final_error [batch] */
+    double* seconds;            /* RunReport::seconds (whole call) */
+} hgc_ifta_io;
+
+/* hologen::OsprConfig (ospr.hpp:20-38).  variant: 0 Ospr, 1 AdaptiveOspr.
+ * freedom_scale: TargetSpec::freedoms.scale (scale-free MSE). */
+typedef struct hgc_ospr_cfg {
+    int variant;
+    int subframes;
+    uint64_t seed;
+    double feedback_gain;
+    int freedom_scale;
+} hgc_ospr_cfg;
+
+/* One batched OSPR call over `jobs` independent runs (one seed each). */
+typedef struct hgc_ospr_io {
+    const double* amplitude;    /* [ny][nx] shared by all jobs, or [jobs][ny][nx] */
+    int per_job_target;         /* 0: amplitude shared, 1: one target per job */
+    const uint8_t* roi;         /* [ny][nx] or NULL */
+    const uint64_t* seeds;      /* [jobs] or NULL = cfg->seed */
+    uint8_t* levels8;           /* SubframeSet::frames as levels [jobs][subframes][ny][nx] */
+    uint16_t* levels16;
+    float* frames;              /* SubframeSet::frames complex [jobs][subframes][ny][nx] */
+    double* frame_mse;          /* SubframeSet::per_frame_mse [jobs][subframes] */
+    double* cumulative_mse;     /* RunReport::trace "cumulative_mse" [jobs][subframes] */
+    double* mean_intensity;     /* SubframeSet::mean_intensity [jobs][ny][nx] */
+    float* replay;              /* RunReport::replay complex [jobs][ny][nx] */
+    double* final_error;        /* [jobs] */
+    double* seconds;
+} hgc_ospr_io;
+
+/* ------------------------------------------------------------ library */
+int hgc_abi_version(void);
+const char* hgc_last_error(void);
+int hgc_device_count(int* count);
+int hgc_set_device(int device);
+/* Largest supported power-of-two side length (4096). */
+int hgc_max_side(void);
+
+/* ------------------------------------------------- algorithm entry points */
+int hgc_ifta_run(const hgc_ifta_cfg* cfg, const hgc_slm* slm, const hgc_fresnel* fresnel,
+                 int nx, int ny, int batch, hgc_ifta_io* io);
+int hgc_ospr_run(const hgc_ospr_cfg* cfg, const hgc_slm* slm, int nx, int ny, int jobs,
+                 hgc_ospr_io* io);
+
+/* ------------------------------------------ device-resident plan API */
+typedef struct hgc_ifta_plan hgc_ifta_plan;
+typedef struct hgc_ospr_plan hgc_ospr_plan;
+
+int hgc_ifta_plan_create(hgc_ifta_plan** plan, const hgc_ifta_cfg* cfg, const hgc_slm* slm,
+                         const hgc_fresnel* fresnel, int nx, int ny, int batch);
+/* Host->device copy of io's inputs (amplitude, phase, roi, seeds, init_*). */
+int hgc_ifta_plan_upload(hgc_ifta_plan* plan, const hgc_ifta_io* io);
+/* Enqueue one full run (init + iterations + trace reduction) on `stream`
+ * (a cudaStream_t, or NULL for the plan's own stream).  Asynchronous. */
+int hgc_ifta_plan_execute(hgc_ifta_plan* plan, void* stream);
+/* Synchronise the plan's stream and copy io's requested outputs to the host. */
+int hgc_ifta_plan_download(hgc_ifta_plan* plan, hgc_ifta_io* io);
+/* Device pointers of the resident buffers (any may be NULL on input):
+ * field = replay after execute (complex float [batch][ny][nx]),
+ * levels = uint8 or uint16 [batch][ny][nx], trace = double [batch][iterations]. */
+int hgc_ifta_plan_device_ptrs(hgc_ifta_plan* plan, void** field, void** levels, void** trace);
+/* Kernel launches one execute enqueues. */
+int hgc_ifta_plan_launches(hgc_ifta_plan* plan);
+/* Average device time (ms) of the seed kernel, the fused row pass and the
+ * fused column pass, each launched `reps` times on the plan's stream (CUDA
+ * events).  Advances the resident state: call after the timed work. */
+int hgc_ifta_plan_profile(hgc_ifta_plan* plan, int reps, double* ms_seed, double* ms_row, double* ms_col);
+int hgc_ifta_plan_destroy(hgc_ifta_plan* plan);
+
+int hgc_ospr_plan_create(hgc_ospr_plan** plan, const hgc_ospr_cfg* cfg, const hgc_slm* slm, int nx,
+                         int ny, int jobs, int per_job_target);
+int hgc_ospr_plan_upload(hgc_ospr_plan* plan, const hgc_ospr_io* io);
+int hgc_ospr_plan_execute(hgc_ospr_plan* plan, void* stream);
+int hgc_ospr_plan_download(hgc_ospr_plan* plan, hgc_ospr_io* io);
+/* levels = uint8/uint16 [jobs][subframes][ny][nx]; traces = double
+ * [jobs][subframes][2] (frame mse, cumulative mse); intensity = float [jobs][ny][nx]. */
+int hgc_ospr_plan_device_ptrs(hgc_ospr_plan* plan, void** levels, void** traces, void** intensity);
+int hgc_ospr_plan_launches(hgc_ospr_plan* plan);
+/* Average device time (ms) of one subframe's seed / inverse-column / fused
+ * row / accumulating-column passes (CUDA events, `reps` launches each). */
+int hgc_ospr_plan_profile(hgc_ospr_plan* plan, int reps, double* ms_seed, double* ms_col_inv, double* ms_row,
+                          double* ms_col_acc);
+int hgc_ospr_plan_destroy(hgc_ospr_plan* plan);
+
+/* ------------------------------------------------------- primitives */
+/* Unitary 2-D DFT of `batch` fields, sign -1 forward / +1 inverse; in == out allowed. */
+int hgc_fft2d(int nx, int ny, int sign, int batch, const float* in, float* out);
+/* Propagator<float>::forward (sign -1: FFT(f*Q)) / inverse (sign +1:
+ * IFFT(F)*conj(Q)), propagation.hpp:81-95; fresnel == NULL is the Fourier
+ * propagator (= hgc_fft2d). */
+int hgc_propagate(int nx, int ny, int sign, const hgc_fresnel* fresnel, int batch, const float* in, float* out);
+/* Snap every pixel of `batch` fields in place; levels (int32, may be NULL). */
+int hgc_quantise(const hgc_slm* slm, int nx, int ny, int batch, float* field, int32_t* levels);
+/* seed_random_phase<float>(amp, Rng) with the engine seeded by
+ * `engine_seed` (Rng(seed).fork(0) uses hgc_fork_seed(seed, 0)) after
+ * discarding `skip` draws. */
+int hgc_seed_random_phase(const double* amplitude, int nx, int ny, uint64_t engine_seed,
+                          uint64_t skip, float* out);
+uint64_t hgc_fork_seed(uint64_t seed, uint64_t stream);
+/* mse(target, replay, {mask, scale_free}) phase-insensitive. */
+int hgc_mse(const double* target, const float* replay, const uint8_t* mask, int nx, int ny,
+            int scale_free, double* out);
+int hgc_fresnel_phase(int nx, int ny, const hgc_fresnel* params, float* q);
+double hgc_subframe_mse_statistic(const double* per_frame_mse, int n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HOLOGEN_B200_H */

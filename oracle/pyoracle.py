@@ -80,7 +80,8 @@ def _p(a):
 
 def _slm(slm, keep):
     s = HgoSlm()
-    s.mode = 1 if str(getattr(slm, "mode", "phase")).lower().endswith("phase") else 0
+    m = getattr(slm, "mode", 1)
+    s.mode = (1 if m.lower().endswith("phase") else 0) if isinstance(m, str) else int(m)
     s.levels = int(slm.levels)
     s.min_arg = float(slm.min_arg)
     s.max_arg = float(slm.max_arg)

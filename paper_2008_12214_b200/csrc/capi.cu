@@ -1,0 +1,1379 @@
+// capi.cu — host side of the B200 HoloGen hot path behind the C ABI in
+// include/hologen_b200.h.  Owns device memory, builds the fused pass
+// sequence of run_ifta / run_ospr_impl as one CUDA graph per plan, and maps
+// errors to the reference's exception semantics (status + message).
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/hologen_b200.h"
+#include "errors.h"
+#include "launch.h"
+#include "mt64.cuh"
+#include "passes.cuh"
+
+namespace hg {
+
+
+// ------------------------------------------------------------------ errors
+thread_local std::string g_err;
+
+template <class F>
+static int guarded(F&& f) {
+    try {
+        f();
+        return HGC_OK;
+    } catch (const Failure& e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return HGC_ECUDA;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return HGC_ECUDA;
+    }
+}
+
+// ---------------------------------------------------------- device memory
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() { reset(); }
+    void alloc(size_t count) {
+        reset();
+        if (count == 0) return;
+        CK(cudaMalloc(&p, count * sizeof(T)));
+        n = count;
+    }
+    void reset() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    // Allocate unless already holding exactly `count` elements (keeps device
+    // pointers stable across uploads so a captured graph stays valid).
+    void ensure(size_t count) {
+        if (n != count) alloc(count);
+    }
+};
+
+// ------------------------------------------------------- twiddle tables
+// tw[N + m] = exp(-2*pi*i*m/N) for N = 1..4096 (fft.cuh), in double then
+// rounded to float, one table per device.
+__global__ void k_init_twiddles(float2* tw) {
+    int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx < 1 || idx >= 2 * kMaxLine) return;
+    int N = 1;
+    while (N * 2 <= idx) N *= 2;
+    int m = idx - N;
+    double s, c;
+    sincospi(-2.0 * (double)m / (double)N, &s, &c);
+    tw[idx] = make_float2((float)c, (float)s);
+}
+
+static std::mutex g_init_mu;
+static std::map<int, float2*> g_tw_tables;
+
+// Per-device one-time setup; returns the device's twiddle table.
+static const float2* device_twiddles() {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_init_mu);
+    auto it = g_tw_tables.find(dev);
+    if (it != g_tw_tables.end()) return it->second;
+    float2* tw = nullptr;
+    CK(cudaMalloc(&tw, sizeof(float2) * 2 * kMaxLine));
+    k_init_twiddles<<<(2 * kMaxLine + 255) / 256, 256>>>(tw);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    g_tw_tables[dev] = tw;
+    return tw;
+}
+
+// ---------------------------------------------------- size dispatch
+static bool is_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
+static void check_size(int nx, int ny) {
+    if (nx <= 0 || ny <= 0) invalid("ComplexField: dimensions must be positive");
+    if (!is_pow2(nx) || !is_pow2(ny) || nx > kMaxLine || ny > kMaxLine || nx < 2 || ny < 2)
+        fail(HGC_EUNSUPPORTED, "hologen_b200: field " + std::to_string(nx) + "x" + std::to_string(ny) +
+                                   " unsupported (GPU path: powers of two, 2..4096 per side)");
+}
+
+static void prepare_kernels(int nx, int ny) {
+    RowArgs ra{};
+    ColArgs ca{};
+    ca.nx = nx;
+    row_fused(nx, ra, 1, nullptr, true);
+    row_plain(nx, ra, 1, nullptr, true);
+    col_plain(ny, ca, 1, nullptr, true);
+    col_gs(ny, ca, 1, nullptr, true);
+    col_ospr(ny, ca, 1, nullptr, true);
+    CK(cudaFuncSetAttribute(k_seed_random_phase, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSeedSmem));
+}
+
+// ------------------------------------------------------- small kernels
+__global__ void k_fill_f(float* p, size_t n, float v) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = v;
+}
+__global__ void k_d2f(const double* a, float* o, size_t n) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        o[i] = (float)a[i];
+}
+// InitPhase::Flat, ifta.hpp:128-130
+__global__ void k_init_flat(const double* a, float2* f, size_t n) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        f[i] = make_float2((float)a[i], 0.f);
+}
+// target-phase init, ifta.hpp:131-136 (tphase = 2*pi*turns, ifta.hpp:107-111)
+__global__ void k_init_target_phase(const double* a, const double* turns, float2* f, size_t n) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        double ph = __dmul_rn(HG_TWO_PI, turns[i]);
+        double s, c;
+        sincos(ph, &s, &c);
+        f[i] = make_float2((float)__dmul_rn(a[i], c), (float)__dmul_rn(a[i], s));
+    }
+}
+// (cos, sin) of the target phase for the no-phase-freedom constraint (ifta.hpp:215-219)
+__global__ void k_phase_cs(const double* turns, float2* cs, size_t n) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        double s, c;
+        sincos(__dmul_rn(HG_TWO_PI, turns[i]), &s, &c);
+        cs[i] = make_float2((float)c, (float)s);
+    }
+}
+// make_fresnel_phase<float>, propagation.hpp:36-54 (no FMA contraction)
+__global__ void k_fresnel_q(int nx, int ny, double scale, double px, double py, float2* q) {
+    size_t n = (size_t)nx * ny;
+    const double cx = nx / 2.0, cy = ny / 2.0;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        int y = (int)(i / nx), x = (int)(i % nx);
+        double dy = __dmul_rn(__dsub_rn((double)y, cy), py);
+        double ty = __dmul_rn(dy, dy);
+        double dx = __dmul_rn(__dsub_rn((double)x, cx), px);
+        double ph = __dmul_rn(scale, __dadd_rn(__dmul_rn(dx, dx), ty));
+        double s, c;
+        sincos(ph, &s, &c);
+        q[i] = make_float2((float)c, (float)s);
+    }
+}
+// Quantiser::apply over a batch (primitive entry point)
+__global__ void k_quantise(float2* f, int32_t* lv, size_t npix, size_t total, QuantParams q) {
+    for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < total; g += (size_t)gridDim.x * blockDim.x) {
+        size_t i = g % npix;
+        float2 v = f[g];
+        int k = quant_decide(q, v.x, v.y, i);
+        f[g] = quant_state(q, k, i);
+        if (lv) lv[g] = k;
+    }
+}
+// mse partials in double (primitive): sum (T-r)^2, T r, r^2, T^2, count
+__global__ void k_mse_partials(const double* t, const float2* r, const uint8_t* m, size_t n, double* out) {
+    double acc[5] = {0, 0, 0, 0, 0};
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        if (m && m[i] == 0) continue;
+        double re = r[i].x, im = r[i].y;
+        double rr = __dsqrt_rn(__dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im)));
+        double d = __dsub_rn(t[i], rr);
+        acc[0] += d * d;
+        acc[1] += t[i] * rr;
+        acc[2] += rr * rr;
+        acc[3] += t[i] * t[i];
+        acc[4] += 1.0;
+    }
+    block_sum_store<5>(acc, out + blockIdx.x * 5);
+}
+
+// Deterministic per-(target, iteration) reduction of the column-pass
+// partials into MSE values (metrics.hpp:70-124; scale-free gain :213-225).
+// partials: [slots][targets][tiles][8]; out: [targets][slots][nout]
+__global__ void k_finalize(const double* part, int slots, int targets, int tiles, double M, int scale_free,
+                           int ospr, double* out) {
+    const int b = blockIdx.x, lane = threadIdx.x;
+    for (int k = 0; k < slots; ++k) {
+        double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        const double* p = part + ((size_t)k * targets + b) * (size_t)tiles * 8;
+        for (int j = lane; j < tiles; j += 32)
+#pragma unroll
+            for (int v = 0; v < 8; ++v) acc[v] += p[(size_t)j * 8 + v];
+#pragma unroll
+        for (int v = 0; v < 8; ++v) acc[v] = warp_sum(acc[v]);
+        if (lane == 0) {
+            auto mse_of = [&](double sdd, double str, double srr, double stt) {
+                if (!scale_free) return sdd / M;
+                double g = srr > 0.0 ? str / srr : 0.0;
+                if (g < 0.0) g = 0.0;
+                double v = stt - 2.0 * g * str + g * g * srr;
+                return (v < 0.0 ? 0.0 : v) / M;
+            };
+            if (!ospr) {
+                out[(size_t)b * slots + k] = mse_of(acc[0], acc[1], acc[2], acc[3]);
+            } else {
+                out[((size_t)b * slots + k) * 2 + 0] = mse_of(acc[0], acc[1], acc[2], acc[3]);
+                out[((size_t)b * slots + k) * 2 + 1] = mse_of(acc[4], acc[5], acc[6], acc[3]);
+            }
+        }
+    }
+}
+
+// TargetSpec::validate on the device (target.hpp:52-73): bit 0 = non-finite
+// amplitude, bit 1 = negative amplitude, bit 2 = non-finite phase.
+__global__ void k_validate(const double* amp, const double* phase, size_t n, int* flags) {
+    int f = 0;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        double a = amp[i];
+        if (!isfinite(a)) f |= 1;
+        else if (a < 0) f |= 2;
+        if (phase && !isfinite(phase[i])) f |= 4;
+    }
+    f = __reduce_or_sync(0xffffffffu, f);
+    if ((threadIdx.x & 31) == 0 && f) atomicOr(flags, f);
+}
+
+static dim3 ew_grid(size_t n) {
+    size_t b = (n + 255) / 256;
+    if (b > 148 * 16) b = 148 * 16;
+    if (b < 1) b = 1;
+    return dim3((unsigned)b);
+}
+
+// ---------------------------------------------------------- validation
+static const double kTwoPi = 6.283185307179586476925286766559;
+
+static void require_finite_img(const double* p, size_t n, const char* what) {
+    for (size_t i = 0; i < n; ++i)
+        if (!std::isfinite(p[i])) invalid(std::string(what) + ": image contains non-finite values");
+}
+
+// SlmSpec::validate, quantise.hpp:71-96
+static void validate_slm(const hgc_slm* s, size_t npix) {
+    if (!s) invalid("SlmSpec: missing");
+    if (s->levels < 2) invalid("SlmSpec: levels must be >= 2");
+    if (s->mode == 1) {
+        if (!std::isfinite(s->min_arg) || !std::isfinite(s->max_arg)) invalid("SlmSpec: phase range must be finite");
+        if (!(s->min_arg < s->max_arg) || s->max_arg - s->min_arg > kTwoPi * (1 + 1e-12))
+            invalid("SlmSpec: phase range must satisfy min_arg < max_arg <= min_arg + 2*pi");
+        if (s->full_circle && std::abs((s->max_arg - s->min_arg) - kTwoPi) > 1e-9)
+            invalid("SlmSpec: full_circle requires a 2*pi range");
+    } else if (s->mode == 0) {
+        if (!std::isfinite(s->min_amp) || !std::isfinite(s->max_amp)) invalid("SlmSpec: amplitude range must be finite");
+        if (!(s->min_amp >= 0) || !(s->min_amp < s->max_amp)) invalid("SlmSpec: need 0 <= min_amp < max_amp");
+    } else {
+        invalid("SlmSpec: unknown mode");
+    }
+    if (s->illumination)
+        for (size_t i = 0; i < npix; ++i) {
+            double re = s->illumination[2 * i], im = s->illumination[2 * i + 1];
+            if (!std::isfinite(re) || !std::isfinite(im)) invalid("SlmSpec: illumination must be finite");
+            if (re == 0.0 && im == 0.0) invalid("SlmSpec: illumination must be nowhere zero");
+        }
+    if (s->levels > 65536) fail(HGC_EUNSUPPORTED, "SlmSpec: more than 65536 levels unsupported on the GPU path");
+}
+
+// TargetSpec::validate, target.hpp:52-73, for a batch already copied to the
+// device (amplitude + optional phase), and the shared roi on the host.
+// Returns the roi coverage M (npix without roi).
+static size_t validate_target_dev(const double* d_amp, const double* d_phase, const uint8_t* roi, size_t npix,
+                                  size_t total, cudaStream_t st) {
+    DBuf<int> flag;
+    flag.alloc(1);
+    CK(cudaMemsetAsync(flag.p, 0, sizeof(int), st));
+    k_validate<<<ew_grid(total), 256, 0, st>>>(d_amp, d_phase, total, flag.p);
+    CK(cudaGetLastError());
+    int h = 0;
+    CK(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (h & 1) invalid("TargetSpec.amplitude: image contains non-finite values");
+    if (h & 2) invalid("TargetSpec: amplitude must be non-negative");
+    if (h & 4) invalid("TargetSpec.phase: image contains non-finite values");
+    size_t m = npix;
+    if (roi) {
+        m = 0;
+        for (size_t i = 0; i < npix; ++i) m += roi[i] != 0;
+        if (m == 0) invalid("TargetSpec: roi covers no pixels");
+    }
+    return m;
+}
+
+// --------------------------------------------------------- quantiser state
+struct QuantDev {
+    QuantParams p{};
+    DBuf<float2> states, illum, illum_unit;
+    DBuf<double> illum_arg;
+    std::vector<float2> h_states, h_illum, h_illum_unit;  // for host-side state_value
+    int mode = 1;
+};
+
+// Quantiser ctor, quantise.hpp:139-166 (host arithmetic identical to the reference)
+static void build_quant(const hgc_slm* s, int nx, int ny, QuantDev& q) {
+    const size_t npix = (size_t)nx * ny;
+    const int L = s->levels;
+    double spac = s->mode == 1 ? (s->full_circle ? kTwoPi / L : (s->max_arg - s->min_arg) / (L - 1))
+                               : (s->max_amp - s->min_amp) / (L - 1);
+    double inv = 1.0 / spac;
+    double range = s->mode == 1 ? s->max_arg - s->min_arg : 0.0;
+    q.mode = s->mode;
+    q.h_states.resize(L);
+    for (int k = 0; k < L; ++k) {
+        if (s->mode == 1) {
+            double a = s->min_arg + k * spac;
+            q.h_states[k] = make_float2((float)std::cos(a), (float)std::sin(a));
+        } else {
+            q.h_states[k] = make_float2((float)(s->min_amp + k * spac), 0.f);
+        }
+    }
+    q.states.alloc(L);
+    CK(cudaMemcpy(q.states.p, q.h_states.data(), sizeof(float2) * L, cudaMemcpyHostToDevice));
+    QuantParams& p = q.p;
+    p.mode = s->mode;
+    p.levels = L;
+    p.full_circle = s->full_circle ? 1 : 0;
+    p.min_arg = s->min_arg;
+    p.inv_spac = inv;
+    p.range = range;
+    p.min_amp = s->min_amp;
+    p.min_arg_f = (float)s->min_arg;
+    p.inv_spac_f = (float)inv;
+    p.range_f = (float)range;
+    p.min_amp_f = (float)s->min_amp;
+    p.wshed_f = (float)(3.1415926535897932384626433832795 + range / 2.0);
+    p.margin_rad = 1e-5f;
+    p.margin_u = (float)(1e-5 * inv + L * 4e-7 + 1e-6);
+    p.states = q.states.p;
+    if (s->illumination) {
+        std::vector<double> arg(npix);
+        q.h_illum.resize(npix);
+        q.h_illum_unit.resize(npix);
+        for (size_t i = 0; i < npix; ++i) {
+            double re = s->illumination[2 * i], im = s->illumination[2 * i + 1];
+            double a = std::hypot(re, im);  // std::abs(complex<double>)
+            arg[i] = std::atan2(im, re);
+            q.h_illum_unit[i] = make_float2((float)(re / a), (float)(im / a));
+            q.h_illum[i] = make_float2((float)re, (float)im);
+        }
+        q.illum_arg.alloc(npix);
+        CK(cudaMemcpy(q.illum_arg.p, arg.data(), sizeof(double) * npix, cudaMemcpyHostToDevice));
+        p.illum_arg = q.illum_arg.p;
+        if (s->mode == 1) {
+            q.illum.alloc(npix);
+            CK(cudaMemcpy(q.illum.p, q.h_illum.data(), sizeof(float2) * npix, cudaMemcpyHostToDevice));
+            p.illum = q.illum.p;
+        } else {
+            q.illum_unit.alloc(npix);
+            CK(cudaMemcpy(q.illum_unit.p, q.h_illum_unit.data(), sizeof(float2) * npix, cudaMemcpyHostToDevice));
+            p.illum_unit = q.illum_unit.p;
+            p.illum_arg = nullptr;  // amplitude mode ignores the illumination phase in decide()
+        }
+    }
+}
+
+// complex<float> product as GCC evaluates it (host, no FMA): reference state_value
+static inline float2 hcmul(float2 a, float2 b) {
+    volatile float ac = a.x * b.x, bd = a.y * b.y, ad = a.x * b.y, bc = a.y * b.x;
+    return make_float2(ac - bd, ad + bc);
+}
+static void levels_to_states(const QuantDev& q, const uint16_t* lv16, const uint8_t* lv8, size_t npix, size_t total,
+                             float* out) {
+    for (size_t g = 0; g < total; ++g) {
+        int k = lv16 ? lv16[g] : lv8[g];
+        size_t i = g % npix;
+        float2 s = q.h_states[k];
+        if (q.mode == 1 && !q.h_illum.empty()) s = hcmul(q.h_illum[i], s);
+        if (q.mode == 0 && !q.h_illum_unit.empty()) s = hcmul(q.h_illum_unit[i], s);
+        out[2 * g] = s.x;
+        out[2 * g + 1] = s.y;
+    }
+}
+
+}  // namespace hg
+
+using namespace hg;
+
+// =================================================================== IFTA
+struct hgc_ifta_plan {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    hgc_ifta_cfg cfg{};
+    int nx = 0, ny = 0, batch = 0;
+    size_t npix = 0;
+    bool fresnel = false;
+    hgc_fresnel fp{};
+    QuantDev q;
+    bool wide_levels = false;
+    bool has_phase = false, has_roi = false;
+    size_t M = 0;
+    int tiles = 0;
+    int bx0 = 0, by0 = 0, bw = 0, bh = 0;  // LT roi bounding box
+    DBuf<float2> field, Q, tphase_cs, init_field;
+    DBuf<float> target_f, weights, init_weights;
+    DBuf<double> amp_d, phase_d, partials, trace;
+    DBuf<uint8_t> roi, lv8;
+    DBuf<uint16_t> lv16;
+    DBuf<MtState> mt;
+    DBuf<uint64_t> seeds;
+    const float2* tw = nullptr;
+    cudaGraphExec_t graph = nullptr;
+    uint64_t graph_sig = 0;
+    int launches = 0;
+    bool uploaded = false;
+    bool init_weights_given = false;
+
+    ~hgc_ifta_plan() {
+        if (graph) cudaGraphExecDestroy(graph);
+        if (stream) cudaStreamDestroy(stream);
+    }
+
+    bool random_init() const {
+        bool target_phase_init = cfg.init_phase == 0 && has_phase && !cfg.freedom_phase;
+        return cfg.init_phase != 2 && cfg.init_phase != 3 && !target_phase_init;
+    }
+
+    float norm() const { return (float)(1.0 / std::sqrt((double)nx * ny)); }
+
+    SeedArgs seed_args() const {
+        SeedArgs sa{};
+        sa.states = mt.p;
+        sa.seeds = seeds.p;
+        sa.amp = amp_d.p;
+        sa.amp_stride = npix;
+        sa.out = field.p;
+        sa.out_stride = npix;
+        sa.npix = npix;
+        return sa;
+    }
+
+    // Aperture-plane pass of iteration k (levels only on the last one).
+    RowArgs row_args(bool last) const {
+        RowArgs ra{};
+        ra.tw = tw;
+        ra.field = field.p;
+        ra.bstride = npix;
+        ra.ny = ny;
+        ra.norm = norm();
+        ra.fresnel_q = fresnel ? Q.p : nullptr;
+        ra.q = q.p;
+        if (last) {
+            ra.levels8 = wide_levels ? nullptr : lv8.p;
+            ra.levels16 = wide_levels ? lv16.p : nullptr;
+        }
+        ra.lv_bstride = npix;
+        return ra;
+    }
+
+    // Replay-plane pass of iteration k (1-based), ifta.hpp:176-224.
+    ColArgs col_args(int k) const {
+        const bool last = k == cfg.iterations;
+        ColArgs cg{};
+        cg.tw = tw;
+        cg.field = field.p;
+        cg.bstride = npix;
+        cg.nx = nx;
+        cg.norm = norm();
+        cg.target = target_f.p;
+        cg.t_bstride = npix;
+        cg.roi = has_roi ? roi.p : nullptr;
+        cg.weights = cfg.variant == 1 ? weights.p : nullptr;
+        cg.tphase_cs = cfg.freedom_phase ? nullptr : tphase_cs.p;
+        cg.phase_freedom = cfg.freedom_phase;
+        cg.amp_outside_roi = cfg.freedom_amplitude_outside_roi;
+        cg.scale_free = cfg.freedom_scale;
+        cg.clamp_lo = (float)cfg.weight_clamp_lo;
+        cg.clamp_hi = (float)cfg.weight_clamp_hi;
+        if (cfg.variant == 2 && !last) {  // LT schedule, ifta.hpp:55-63, :74-84, :189
+            const int K = cfg.iterations;
+            double frac = cfg.lt_initial_fraction + (1.0 - cfg.lt_initial_fraction) * (k - 1) / (K - 1);
+            double side = std::sqrt(frac);
+            int aw = std::max(1, (int)std::lround(bw * side));
+            int ah = std::max(1, (int)std::lround(bh * side));
+            cg.lt = 1;
+            cg.lt_x0 = bx0 + (bw - aw) / 2;
+            cg.lt_y0 = by0 + (bh - ah) / 2;
+            cg.lt_x1 = cg.lt_x0 + aw;
+            cg.lt_y1 = cg.lt_y0 + ah;
+        }
+        cg.last = last ? 1 : 0;
+        cg.replay_out = field.p;
+        cg.partials = partials.p + (size_t)(k - 1) * batch * tiles * 8;
+        return cg;
+    }
+
+    // The whole run_ifta sequence (ifta.hpp:124-226) as stream work.
+    void record(cudaStream_t st) {
+        launches = 0;
+        const size_t tot = npix * batch;
+        // ---- initial replay field R0
+        if (cfg.init_phase == 3) {
+            CK(cudaMemcpyAsync(field.p, init_field.p, sizeof(float2) * tot, cudaMemcpyDeviceToDevice, st));
+        } else if (cfg.init_phase == 2) {
+            k_init_flat<<<ew_grid(tot), 256, 0, st>>>(amp_d.p, field.p, tot);
+            ++launches;
+        } else if (!random_init()) {
+            k_init_target_phase<<<ew_grid(tot), 256, 0, st>>>(amp_d.p, phase_d.p, field.p, tot);
+            ++launches;
+        } else {
+            k_seed_random_phase<<<batch, kSeedThreads, kSeedSmem, st>>>(seed_args());
+            ++launches;
+        }
+        CK(cudaGetLastError());
+        if (cfg.variant == 1) {
+            if (init_weights_given)
+                CK(cudaMemcpyAsync(weights.p, init_weights.p, sizeof(float) * tot, cudaMemcpyDeviceToDevice, st));
+            else {
+                k_fill_f<<<ew_grid(tot), 256, 0, st>>>(weights.p, tot, 1.0f);
+                ++launches;
+            }
+        }
+        // ---- first half of P^-1(R0): inverse column transforms
+        ColArgs ca{};
+        ca.tw = tw;
+        ca.field = field.p;
+        ca.bstride = npix;
+        ca.nx = nx;
+        ca.sign = +1;
+        col_plain(ny, ca, batch, st);
+        ++launches;
+        for (int k = 1; k <= cfg.iterations; ++k) {
+            row_fused(nx, row_args(k == cfg.iterations), batch, st);
+            col_gs(ny, col_args(k), batch, st);
+            launches += 2;
+        }
+        k_finalize<<<batch, 32, 0, st>>>(partials.p, cfg.iterations, batch, tiles, (double)M, cfg.freedom_scale, 0,
+                                         trace.p);
+        ++launches;
+        CK(cudaGetLastError());
+    }
+};
+
+// Average device time (ms) of `reps` launches of f on stream st.
+template <class F>
+static double time_launches(cudaStream_t st, int reps, F&& f) {
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    f();  // warm
+    CK(cudaEventRecord(a, st));
+    for (int r = 0; r < reps; ++r) f();
+    CK(cudaEventRecord(b, st));
+    CK(cudaEventSynchronize(b));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return ms / reps;
+}
+
+extern "C" {
+
+int hgc_abi_version(void) { return HGC_ABI_VERSION; }
+const char* hgc_last_error(void) { return g_err.c_str(); }
+int hgc_max_side(void) { return kMaxLine; }
+
+int hgc_device_count(int* count) {
+    return guarded([&] { CK(cudaGetDeviceCount(count)); });
+}
+int hgc_set_device(int device) {
+    return guarded([&] { CK(cudaSetDevice(device)); });
+}
+uint64_t hgc_fork_seed(uint64_t seed, uint64_t stream) { return fork_seed(seed, stream); }
+
+double hgc_subframe_mse_statistic(const double* v, int n) {  // ospr.hpp:58-64
+    if (!v || n <= 0) {
+        g_err = "subframe_mse_statistic: empty list";
+        return std::nan("");
+    }
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += v[i];
+    return s / std::sqrt((double)n);
+}
+
+static void validate_ifta_cfg(const hgc_ifta_cfg* c) {  // IftaConfig::validate, ifta.hpp:41-50
+    if (!c) invalid("IftaConfig: missing");
+    if (c->iterations < 1) invalid("IftaConfig: iterations must be >= 1");
+    if (!(c->weight_clamp_lo > 0) || !(c->weight_clamp_hi >= c->weight_clamp_lo))
+        invalid("IftaConfig: weight clamp bounds invalid");
+    if (!(c->lt_initial_fraction > 0) || !(c->lt_initial_fraction <= 1))
+        invalid("IftaConfig: lt_initial_fraction must be in (0,1]");
+    if (c->variant < 0 || c->variant > 2) invalid("IftaConfig: unknown variant");
+    if (c->init_phase < 0 || c->init_phase > 3) invalid("IftaConfig: unknown init phase");
+}
+
+static void validate_fresnel(const hgc_fresnel* p) {  // FresnelParams::validate, propagation.hpp:21-29
+    if (!(p->wavelength > 0) || !std::isfinite(p->wavelength)) invalid("FresnelParams: wavelength must be positive");
+    if (p->distance == 0 || !std::isfinite(p->distance)) invalid("FresnelParams: distance must be non-zero");
+    if (!(p->pixel_pitch_x > 0) || !(p->pixel_pitch_y > 0) || !std::isfinite(p->pixel_pitch_x) ||
+        !std::isfinite(p->pixel_pitch_y))
+        invalid("FresnelParams: pixel pitches must be positive");
+}
+
+int hgc_ifta_plan_create(hgc_ifta_plan** out, const hgc_ifta_cfg* cfg, const hgc_slm* slm, const hgc_fresnel* fresnel,
+                         int nx, int ny, int batch) {
+    return guarded([&] {
+        if (!out) invalid("hgc_ifta_plan_create: null plan pointer");
+        *out = nullptr;
+        validate_ifta_cfg(cfg);
+        if (nx <= 0 || ny <= 0) invalid("ComplexField: dimensions must be positive");
+        validate_slm(slm, (size_t)nx * ny);
+        if (fresnel) validate_fresnel(fresnel);
+        if (batch < 1) invalid("hgc_ifta_plan_create: batch must be >= 1");
+        check_size(nx, ny);
+        const float2* tw = device_twiddles();
+        auto p = std::make_unique<hgc_ifta_plan>();
+        p->tw = tw;
+        CK(cudaGetDevice(&p->device));
+        CK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+        p->cfg = *cfg;
+        p->nx = nx;
+        p->ny = ny;
+        p->batch = batch;
+        p->npix = (size_t)nx * ny;
+        p->fresnel = fresnel != nullptr;
+        if (fresnel) p->fp = *fresnel;
+        build_quant(slm, nx, ny, p->q);
+        p->wide_levels = slm->levels > 256;
+        p->tiles = col_tiles(nx, ny);
+        const size_t tot = p->npix * batch;
+        p->field.alloc(tot);
+        p->target_f.alloc(tot);
+        p->amp_d.alloc(tot);
+        if (cfg->variant == 1) p->weights.alloc(tot);
+        if (p->wide_levels) p->lv16.alloc(tot);
+        else p->lv8.alloc(tot);
+        p->partials.alloc((size_t)cfg->iterations * batch * p->tiles * 8);
+        p->trace.alloc((size_t)cfg->iterations * batch);
+        p->mt.alloc(batch);
+        p->seeds.alloc(batch);
+        if (fresnel) {
+            p->Q.alloc(p->npix);
+            double scale = 3.1415926535897932384626433832795 / (fresnel->wavelength * fresnel->distance);
+            k_fresnel_q<<<ew_grid(p->npix), 256>>>(nx, ny, scale, fresnel->pixel_pitch_x, fresnel->pixel_pitch_y, p->Q.p);
+            CK(cudaGetLastError());
+        }
+        prepare_kernels(nx, ny);
+        CK(cudaDeviceSynchronize());
+        *out = p.release();
+    });
+}
+
+int hgc_ifta_plan_upload(hgc_ifta_plan* p, const hgc_ifta_io* io) {
+    return guarded([&] {
+        if (!p || !io) invalid("hgc_ifta_plan_upload: null argument");
+        CK(cudaSetDevice(p->device));
+        const size_t npix = p->npix, tot = npix * p->batch;
+        if (!io->amplitude) invalid("TargetSpec: amplitude image is empty");
+        CK(cudaMemcpyAsync(p->amp_d.p, io->amplitude, sizeof(double) * tot, cudaMemcpyHostToDevice, p->stream));
+        p->has_phase = io->phase != nullptr;
+        if (io->phase) {
+            p->phase_d.ensure(tot);
+            CK(cudaMemcpyAsync(p->phase_d.p, io->phase, sizeof(double) * tot, cudaMemcpyHostToDevice, p->stream));
+        }
+        p->M = validate_target_dev(p->amp_d.p, io->phase ? p->phase_d.p : nullptr, io->roi, npix, tot, p->stream);
+        k_d2f<<<ew_grid(tot), 256, 0, p->stream>>>(p->amp_d.p, p->target_f.p, tot);
+        CK(cudaGetLastError());
+        if (io->phase) {
+            if (!p->cfg.freedom_phase) {
+                p->tphase_cs.ensure(tot);
+                k_phase_cs<<<ew_grid(tot), 256, 0, p->stream>>>(p->phase_d.p, p->tphase_cs.p, tot);
+            }
+        } else if (!p->cfg.freedom_phase) {
+            // no target phase: the constraint enforces phase 0 (ifta.hpp:216)
+            p->tphase_cs.ensure(tot);
+            std::vector<float2> ones(tot, make_float2(1.f, 0.f));
+            CK(cudaMemcpyAsync(p->tphase_cs.p, ones.data(), sizeof(float2) * tot, cudaMemcpyHostToDevice, p->stream));
+            CK(cudaStreamSynchronize(p->stream));
+        }
+        p->has_roi = io->roi != nullptr;
+        p->bx0 = 0;
+        p->by0 = 0;
+        p->bw = p->nx;
+        p->bh = p->ny;
+        if (io->roi) {
+            p->roi.ensure(npix);
+            CK(cudaMemcpyAsync(p->roi.p, io->roi, npix, cudaMemcpyHostToDevice, p->stream));
+            if (p->cfg.variant == 2) {  // roi bounding box, ifta.hpp:148-161
+                int bx0 = p->nx, by0 = p->ny, bx1 = -1, by1 = -1;
+                for (int y = 0; y < p->ny; ++y)
+                    for (int x = 0; x < p->nx; ++x)
+                        if (io->roi[(size_t)y * p->nx + x]) {
+                            bx0 = std::min(bx0, x);
+                            bx1 = std::max(bx1, x);
+                            by0 = std::min(by0, y);
+                            by1 = std::max(by1, y);
+                        }
+                p->bx0 = bx0;
+                p->by0 = by0;
+                p->bw = bx1 - bx0 + 1;
+                p->bh = by1 - by0 + 1;
+            }
+        }
+        std::vector<uint64_t> es(p->batch);
+        for (int b = 0; b < p->batch; ++b) es[b] = fork_seed(io->seeds ? io->seeds[b] : p->cfg.seed, 0);  // ifta.hpp:124
+        CK(cudaMemcpyAsync(p->seeds.p, es.data(), sizeof(uint64_t) * p->batch, cudaMemcpyHostToDevice, p->stream));
+        if (p->cfg.init_phase == 3) {
+            if (!io->init_field) invalid("IftaConfig: init_phase Given requires init_field");
+            p->init_field.ensure(tot);
+            CK(cudaMemcpyAsync(p->init_field.p, io->init_field, sizeof(float2) * tot, cudaMemcpyHostToDevice, p->stream));
+            p->init_weights_given = io->init_weights != nullptr && p->cfg.variant == 1;
+            if (p->init_weights_given) {
+                p->init_weights.ensure(tot);
+                CK(cudaMemcpyAsync(p->init_weights.p, io->init_weights, sizeof(float) * tot, cudaMemcpyHostToDevice,
+                                   p->stream));
+            }
+        }
+        CK(cudaStreamSynchronize(p->stream));
+        const uint64_t sig = (uint64_t)(uintptr_t)p->roi.p ^ ((uint64_t)(uintptr_t)p->phase_d.p << 1) ^
+                             ((uint64_t)(uintptr_t)p->tphase_cs.p << 2) ^ ((uint64_t)(uintptr_t)p->init_field.p << 3) ^
+                             ((uint64_t)(uintptr_t)p->init_weights.p << 4) ^ ((uint64_t)p->has_roi << 60) ^
+                             ((uint64_t)p->has_phase << 61) ^ ((uint64_t)p->init_weights_given << 62) ^ p->M;
+        if (p->graph && sig != p->graph_sig) {  // recorded structure changed: rebuild
+            cudaGraphExecDestroy(p->graph);
+            p->graph = nullptr;
+        }
+        p->graph_sig = sig;
+        p->uploaded = true;
+    });
+}
+
+int hgc_ifta_plan_execute(hgc_ifta_plan* p, void* stream) {
+    return guarded([&] {
+        if (!p) invalid("hgc_ifta_plan_execute: null plan");
+        if (!p->uploaded) invalid("hgc_ifta_plan_execute: inputs not uploaded");
+        CK(cudaSetDevice(p->device));
+        cudaStream_t st = stream ? (cudaStream_t)stream : p->stream;
+        if (!p->graph) {
+            cudaGraph_t g;
+            CK(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
+            try {
+                p->record(p->stream);
+            } catch (...) {
+                cudaStreamEndCapture(p->stream, &g);
+                throw;
+            }
+            CK(cudaStreamEndCapture(p->stream, &g));
+            CK(cudaGraphInstantiate(&p->graph, g, 0));
+            cudaGraphDestroy(g);
+        }
+        CK(cudaGraphLaunch(p->graph, st));
+    });
+}
+
+int hgc_ifta_plan_download(hgc_ifta_plan* p, hgc_ifta_io* io) {
+    return guarded([&] {
+        if (!p || !io) invalid("hgc_ifta_plan_download: null argument");
+        CK(cudaSetDevice(p->device));
+        CK(cudaDeviceSynchronize());
+        const size_t tot = p->npix * p->batch;
+        const int K = p->cfg.iterations;
+        if (io->replay) CK(cudaMemcpy(io->replay, p->field.p, sizeof(float2) * tot, cudaMemcpyDeviceToHost));
+        std::vector<double> tr;
+        if (io->trace || io->final_error) {
+            tr.resize((size_t)K * p->batch);
+            CK(cudaMemcpy(tr.data(), p->trace.p, sizeof(double) * tr.size(), cudaMemcpyDeviceToHost));
+            if (io->trace) std::memcpy(io->trace, tr.data(), sizeof(double) * tr.size());
+            if (io->final_error)
+                for (int b = 0; b < p->batch; ++b) io->final_error[b] = tr[(size_t)b * K + K - 1];
+        }
+        if (!p->wide_levels && io->levels8 && !io->levels16 && !io->hologram) {
+            CK(cudaMemcpy(io->levels8, p->lv8.p, tot, cudaMemcpyDeviceToHost));  // straight into the caller's buffer
+        } else if (io->levels8 || io->levels16 || io->hologram) {
+            std::vector<uint8_t> l8;
+            std::vector<uint16_t> l16;
+            if (p->wide_levels) {
+                l16.resize(tot);
+                CK(cudaMemcpy(l16.data(), p->lv16.p, sizeof(uint16_t) * tot, cudaMemcpyDeviceToHost));
+                if (io->levels8) invalid("hgc_ifta_io: levels8 requested with more than 256 levels");
+                if (io->levels16) std::memcpy(io->levels16, l16.data(), sizeof(uint16_t) * tot);
+            } else {
+                l8.resize(tot);
+                CK(cudaMemcpy(l8.data(), p->lv8.p, tot, cudaMemcpyDeviceToHost));
+                if (io->levels8) std::memcpy(io->levels8, l8.data(), tot);
+                if (io->levels16)
+                    for (size_t i = 0; i < tot; ++i) io->levels16[i] = l8[i];
+            }
+            if (io->hologram)
+                levels_to_states(p->q, p->wide_levels ? l16.data() : nullptr, p->wide_levels ? nullptr : l8.data(),
+                                 p->npix, tot, io->hologram);
+        }
+    });
+}
+
+int hgc_ifta_plan_device_ptrs(hgc_ifta_plan* p, void** field, void** levels, void** trace) {
+    return guarded([&] {
+        if (!p) invalid("null plan");
+        if (field) *field = p->field.p;
+        if (levels) *levels = p->wide_levels ? (void*)p->lv16.p : (void*)p->lv8.p;
+        if (trace) *trace = p->trace.p;
+    });
+}
+
+int hgc_ifta_plan_launches(hgc_ifta_plan* p) { return p ? p->launches : -1; }
+
+// Per-kernel device time of the plan's passes (CUDA events on the plan's
+// stream, `reps` back-to-back launches each).  Runs extra iterations on the
+// resident field: call after the timed work.
+int hgc_ifta_plan_profile(hgc_ifta_plan* p, int reps, double* ms_seed, double* ms_row, double* ms_col) {
+    return guarded([&] {
+        if (!p || !p->uploaded) invalid("hgc_ifta_plan_profile: plan not ready");
+        CK(cudaSetDevice(p->device));
+        cudaStream_t st = p->stream;
+        const int b = p->batch;
+        if (ms_seed)
+            *ms_seed = time_launches(st, reps, [&] {
+                k_seed_random_phase<<<b, kSeedThreads, kSeedSmem, st>>>(p->seed_args());
+            });
+        const int k = p->cfg.iterations > 1 ? 1 : p->cfg.iterations;  // a constraining iteration when K > 1
+        if (ms_row) *ms_row = time_launches(st, reps, [&] { row_fused(p->nx, p->row_args(false), b, st); });
+        if (ms_col) *ms_col = time_launches(st, reps, [&] { col_gs(p->ny, p->col_args(k), b, st); });
+        CK(cudaGetLastError());
+    });
+}
+
+int hgc_ifta_plan_destroy(hgc_ifta_plan* p) {
+    return guarded([&] {
+        if (p) {
+            cudaSetDevice(p->device);
+            cudaStreamSynchronize(p->stream);
+        }
+        delete p;
+    });
+}
+
+int hgc_ifta_run(const hgc_ifta_cfg* cfg, const hgc_slm* slm, const hgc_fresnel* fresnel, int nx, int ny, int batch,
+                 hgc_ifta_io* io) {
+    auto t0 = std::chrono::steady_clock::now();
+    hgc_ifta_plan* p = nullptr;
+    int rc = hgc_ifta_plan_create(&p, cfg, slm, fresnel, nx, ny, batch);
+    if (rc == HGC_OK) rc = hgc_ifta_plan_upload(p, io);
+    if (rc == HGC_OK) rc = hgc_ifta_plan_execute(p, nullptr);
+    if (rc == HGC_OK) rc = hgc_ifta_plan_download(p, io);
+    if (p) {
+        std::string keep = g_err;
+        hgc_ifta_plan_destroy(p);
+        g_err = keep;
+    }
+    if (rc == HGC_OK && io && io->seconds)
+        *io->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return rc;
+}
+
+}  // extern "C"
+
+// =================================================================== OSPR
+struct hgc_ospr_plan {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    hgc_ospr_cfg cfg{};
+    int nx = 0, ny = 0, jobs = 0, per_job = 0;
+    size_t npix = 0;
+    QuantDev q;
+    bool wide_levels = false, has_roi = false;
+    size_t M = 0;
+    int tiles = 0;
+    DBuf<float2> field;
+    DBuf<float> target_f, S;
+    DBuf<double> amp_d, partials, traces;
+    DBuf<uint8_t> roi, lv8;
+    DBuf<uint16_t> lv16;
+    DBuf<MtState> mt;
+    DBuf<uint64_t> seeds;
+    const float2* tw = nullptr;
+    cudaGraphExec_t graph = nullptr;
+    uint64_t graph_sig = 0;
+    int launches = 0;
+    bool uploaded = false;
+
+    ~hgc_ospr_plan() {
+        if (graph) cudaGraphExecDestroy(graph);
+        if (stream) cudaStreamDestroy(stream);
+    }
+
+    float norm() const { return (float)(1.0 / std::sqrt((double)nx * ny)); }
+
+    // Seed of subframe n (1-based): fresh stream at n = 1, continued after.
+    SeedArgs seed_args(int n) const {
+        SeedArgs sa{};
+        sa.states = mt.p;
+        sa.seeds = n == 1 ? seeds.p : nullptr;
+        sa.amp = amp_d.p;
+        sa.amp_stride = per_job ? npix : 0;
+        sa.out = field.p;
+        sa.out_stride = npix;
+        sa.npix = npix;
+        if (cfg.variant == 1 && n > 1) {  // adaptive budget, ospr.hpp:106-116
+            sa.S = S.p;
+            sa.S_stride = npix;
+            sa.n = n;
+            sa.gain = cfg.feedback_gain;
+        }
+        return sa;
+    }
+    ColArgs col_inv_args() const {
+        ColArgs ci{};
+        ci.tw = tw;
+        ci.field = field.p;
+        ci.bstride = npix;
+        ci.nx = nx;
+        ci.sign = +1;
+        return ci;
+    }
+    RowArgs row_args(int n) const {
+        const int N = cfg.subframes;
+        RowArgs ra{};
+        ra.tw = tw;
+        ra.field = field.p;
+        ra.bstride = npix;
+        ra.ny = ny;
+        ra.norm = norm();
+        ra.q = q.p;
+        ra.levels8 = wide_levels ? nullptr : lv8.p + (size_t)(n - 1) * npix;
+        ra.levels16 = wide_levels ? lv16.p + (size_t)(n - 1) * npix : nullptr;
+        ra.lv_bstride = (size_t)N * npix;
+        return ra;
+    }
+    ColArgs col_acc_args(int n) const {
+        ColArgs co{};
+        co.tw = tw;
+        co.field = field.p;
+        co.bstride = npix;
+        co.nx = nx;
+        co.norm = norm();
+        co.target = target_f.p;
+        co.t_bstride = per_job ? npix : 0;
+        co.roi = has_roi ? roi.p : nullptr;
+        co.scale_free = cfg.freedom_scale;
+        co.partials = partials.p + (size_t)(n - 1) * jobs * tiles * 8;
+        co.S = S.p;  // per job, even when the target is shared
+        co.S_bstride = npix;
+        co.inv_n = 1.0f / (float)n;
+        return co;
+    }
+
+    // run_ospr_impl's subframe loop (ospr.hpp:105-147), all jobs at once.
+    void record(cudaStream_t st) {
+        launches = 0;
+        const int N = cfg.subframes;
+        CK(cudaMemsetAsync(S.p, 0, sizeof(float) * npix * jobs, st));
+        for (int n = 1; n <= N; ++n) {
+            k_seed_random_phase<<<jobs, kSeedThreads, kSeedSmem, st>>>(seed_args(n));
+            CK(cudaGetLastError());
+            col_plain(ny, col_inv_args(), jobs, st);
+            row_fused(nx, row_args(n), jobs, st);
+            col_ospr(ny, col_acc_args(n), jobs, st);
+            launches += 4;
+        }
+        k_finalize<<<jobs, 32, 0, st>>>(partials.p, N, jobs, tiles, (double)M, cfg.freedom_scale, 1, traces.p);
+        ++launches;
+        CK(cudaGetLastError());
+    }
+};
+
+extern "C" {
+
+static void validate_ospr_cfg(const hgc_ospr_cfg* c) {  // OsprConfig::validate, ospr.hpp:30-37
+    if (!c) invalid("OsprConfig: missing");
+    if (c->subframes < 1) invalid("OsprConfig: subframes must be >= 1");
+    if (!(c->feedback_gain >= 0.0 && c->feedback_gain <= 1.0)) invalid("OsprConfig: feedback_gain must be in [0,1]");
+    if (c->variant < 0 || c->variant > 1) invalid("OsprConfig: unknown variant");
+}
+
+int hgc_ospr_plan_create(hgc_ospr_plan** out, const hgc_ospr_cfg* cfg, const hgc_slm* slm, int nx, int ny, int jobs,
+                         int per_job_target) {
+    return guarded([&] {
+        if (!out) invalid("hgc_ospr_plan_create: null plan pointer");
+        *out = nullptr;
+        validate_ospr_cfg(cfg);
+        if (nx <= 0 || ny <= 0) invalid("ComplexField: dimensions must be positive");
+        validate_slm(slm, (size_t)nx * ny);
+        if (jobs < 1) invalid("hgc_ospr_plan_create: jobs must be >= 1");
+        check_size(nx, ny);
+        const float2* tw = device_twiddles();
+        auto p = std::make_unique<hgc_ospr_plan>();
+        p->tw = tw;
+        CK(cudaGetDevice(&p->device));
+        CK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+        p->cfg = *cfg;
+        p->nx = nx;
+        p->ny = ny;
+        p->jobs = jobs;
+        p->per_job = per_job_target ? 1 : 0;
+        p->npix = (size_t)nx * ny;
+        build_quant(slm, nx, ny, p->q);
+        p->wide_levels = slm->levels > 256;
+        p->tiles = col_tiles(nx, ny);
+        const size_t tot = p->npix * jobs;
+        const size_t ttot = p->per_job ? tot : p->npix;
+        p->field.alloc(tot);
+        p->S.alloc(tot);
+        p->target_f.alloc(ttot);
+        p->amp_d.alloc(ttot);
+        const size_t lvtot = tot * cfg->subframes;
+        if (p->wide_levels) p->lv16.alloc(lvtot);
+        else p->lv8.alloc(lvtot);
+        p->partials.alloc((size_t)cfg->subframes * jobs * p->tiles * 8);
+        p->traces.alloc((size_t)cfg->subframes * jobs * 2);
+        p->mt.alloc(jobs);
+        p->seeds.alloc(jobs);
+        prepare_kernels(nx, ny);
+        CK(cudaDeviceSynchronize());
+        *out = p.release();
+    });
+}
+
+int hgc_ospr_plan_upload(hgc_ospr_plan* p, const hgc_ospr_io* io) {
+    return guarded([&] {
+        if (!p || !io) invalid("hgc_ospr_plan_upload: null argument");
+        CK(cudaSetDevice(p->device));
+        const size_t ttot = p->per_job ? p->npix * p->jobs : p->npix;
+        if (!io->amplitude) invalid("TargetSpec: amplitude image is empty");
+        CK(cudaMemcpyAsync(p->amp_d.p, io->amplitude, sizeof(double) * ttot, cudaMemcpyHostToDevice, p->stream));
+        p->M = validate_target_dev(p->amp_d.p, nullptr, io->roi, p->npix, ttot, p->stream);
+        k_d2f<<<ew_grid(ttot), 256, 0, p->stream>>>(p->amp_d.p, p->target_f.p, ttot);
+        CK(cudaGetLastError());
+        p->has_roi = io->roi != nullptr;
+        if (io->roi) {
+            p->roi.ensure(p->npix);
+            CK(cudaMemcpyAsync(p->roi.p, io->roi, p->npix, cudaMemcpyHostToDevice, p->stream));
+        }
+        std::vector<uint64_t> es(p->jobs);
+        for (int j = 0; j < p->jobs; ++j) es[j] = fork_seed(io->seeds ? io->seeds[j] : p->cfg.seed, 0);  // ospr.hpp:89
+        CK(cudaMemcpyAsync(p->seeds.p, es.data(), sizeof(uint64_t) * p->jobs, cudaMemcpyHostToDevice, p->stream));
+        CK(cudaStreamSynchronize(p->stream));
+        const uint64_t sig = (uint64_t)(uintptr_t)p->roi.p ^ ((uint64_t)p->has_roi << 60) ^ p->M;
+        if (p->graph && sig != p->graph_sig) {
+            cudaGraphExecDestroy(p->graph);
+            p->graph = nullptr;
+        }
+        p->graph_sig = sig;
+        p->uploaded = true;
+    });
+}
+
+int hgc_ospr_plan_execute(hgc_ospr_plan* p, void* stream) {
+    return guarded([&] {
+        if (!p) invalid("hgc_ospr_plan_execute: null plan");
+        if (!p->uploaded) invalid("hgc_ospr_plan_execute: inputs not uploaded");
+        CK(cudaSetDevice(p->device));
+        cudaStream_t st = stream ? (cudaStream_t)stream : p->stream;
+        if (!p->graph) {
+            cudaGraph_t g;
+            CK(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
+            try {
+                p->record(p->stream);
+            } catch (...) {
+                cudaStreamEndCapture(p->stream, &g);
+                throw;
+            }
+            CK(cudaStreamEndCapture(p->stream, &g));
+            CK(cudaGraphInstantiate(&p->graph, g, 0));
+            cudaGraphDestroy(g);
+        }
+        CK(cudaGraphLaunch(p->graph, st));
+    });
+}
+
+int hgc_ospr_plan_download(hgc_ospr_plan* p, hgc_ospr_io* io) {
+    return guarded([&] {
+        if (!p || !io) invalid("hgc_ospr_plan_download: null argument");
+        CK(cudaSetDevice(p->device));
+        CK(cudaDeviceSynchronize());
+        const int N = p->cfg.subframes;
+        const size_t npix = p->npix, tot = npix * p->jobs, lvtot = tot * N;
+        std::vector<double> tr((size_t)N * p->jobs * 2);
+        CK(cudaMemcpy(tr.data(), p->traces.p, sizeof(double) * tr.size(), cudaMemcpyDeviceToHost));
+        for (int j = 0; j < p->jobs; ++j)
+            for (int n = 0; n < N; ++n) {
+                size_t o = ((size_t)j * N + n);
+                if (io->frame_mse) io->frame_mse[o] = tr[o * 2];
+                if (io->cumulative_mse) io->cumulative_mse[o] = tr[o * 2 + 1];
+            }
+        if (io->final_error)
+            for (int j = 0; j < p->jobs; ++j) io->final_error[j] = tr[((size_t)j * N + N - 1) * 2 + 1];
+        if (io->mean_intensity || io->replay) {  // ospr.hpp:149-156
+            std::vector<float> S(tot);
+            CK(cudaMemcpy(S.data(), p->S.p, sizeof(float) * tot, cudaMemcpyDeviceToHost));
+            for (size_t i = 0; i < tot; ++i) {
+                double m = (double)S[i] / N;
+                if (io->mean_intensity) io->mean_intensity[i] = m;
+                if (io->replay) {
+                    io->replay[2 * i] = (float)std::sqrt(m);
+                    io->replay[2 * i + 1] = 0.f;
+                }
+            }
+        }
+        if (!p->wide_levels && io->levels8 && !io->levels16 && !io->frames) {
+            CK(cudaMemcpy(io->levels8, p->lv8.p, lvtot, cudaMemcpyDeviceToHost));
+        } else if (io->levels8 || io->levels16 || io->frames) {
+            std::vector<uint8_t> l8;
+            std::vector<uint16_t> l16;
+            if (p->wide_levels) {
+                l16.resize(lvtot);
+                CK(cudaMemcpy(l16.data(), p->lv16.p, sizeof(uint16_t) * lvtot, cudaMemcpyDeviceToHost));
+                if (io->levels8) invalid("hgc_ospr_io: levels8 requested with more than 256 levels");
+                if (io->levels16) std::memcpy(io->levels16, l16.data(), sizeof(uint16_t) * lvtot);
+            } else {
+                l8.resize(lvtot);
+                CK(cudaMemcpy(l8.data(), p->lv8.p, lvtot, cudaMemcpyDeviceToHost));
+                if (io->levels8) std::memcpy(io->levels8, l8.data(), lvtot);
+                if (io->levels16)
+                    for (size_t i = 0; i < lvtot; ++i) io->levels16[i] = l8[i];
+            }
+            if (io->frames)
+                levels_to_states(p->q, p->wide_levels ? l16.data() : nullptr, p->wide_levels ? nullptr : l8.data(), npix,
+                                 lvtot, io->frames);
+        }
+    });
+}
+
+int hgc_ospr_plan_device_ptrs(hgc_ospr_plan* p, void** levels, void** traces, void** intensity) {
+    return guarded([&] {
+        if (!p) invalid("null plan");
+        if (levels) *levels = p->wide_levels ? (void*)p->lv16.p : (void*)p->lv8.p;
+        if (traces) *traces = p->traces.p;
+        if (intensity) *intensity = p->S.p;
+    });
+}
+
+int hgc_ospr_plan_launches(hgc_ospr_plan* p) { return p ? p->launches : -1; }
+
+// Per-kernel device time of one subframe's four passes (see hgc_ifta_plan_profile).
+int hgc_ospr_plan_profile(hgc_ospr_plan* p, int reps, double* ms_seed, double* ms_col_inv, double* ms_row,
+                          double* ms_col_acc) {
+    return guarded([&] {
+        if (!p || !p->uploaded) invalid("hgc_ospr_plan_profile: plan not ready");
+        CK(cudaSetDevice(p->device));
+        cudaStream_t st = p->stream;
+        const int j = p->jobs;
+        if (ms_seed)
+            *ms_seed = time_launches(st, reps, [&] {
+                k_seed_random_phase<<<j, kSeedThreads, kSeedSmem, st>>>(p->seed_args(1));
+            });
+        if (ms_col_inv) *ms_col_inv = time_launches(st, reps, [&] { col_plain(p->ny, p->col_inv_args(), j, st); });
+        if (ms_row) *ms_row = time_launches(st, reps, [&] { row_fused(p->nx, p->row_args(1), j, st); });
+        if (ms_col_acc) *ms_col_acc = time_launches(st, reps, [&] { col_ospr(p->ny, p->col_acc_args(1), j, st); });
+        CK(cudaGetLastError());
+    });
+}
+
+int hgc_ospr_plan_destroy(hgc_ospr_plan* p) {
+    return guarded([&] {
+        if (p) {
+            cudaSetDevice(p->device);
+            cudaStreamSynchronize(p->stream);
+        }
+        delete p;
+    });
+}
+
+int hgc_ospr_run(const hgc_ospr_cfg* cfg, const hgc_slm* slm, int nx, int ny, int jobs, hgc_ospr_io* io) {
+    auto t0 = std::chrono::steady_clock::now();
+    hgc_ospr_plan* p = nullptr;
+    int rc = hgc_ospr_plan_create(&p, cfg, slm, nx, ny, jobs, io ? io->per_job_target : 0);
+    if (rc == HGC_OK) rc = hgc_ospr_plan_upload(p, io);
+    if (rc == HGC_OK) rc = hgc_ospr_plan_execute(p, nullptr);
+    if (rc == HGC_OK) rc = hgc_ospr_plan_download(p, io);
+    if (p) {
+        std::string keep = g_err;
+        hgc_ospr_plan_destroy(p);
+        g_err = keep;
+    }
+    if (rc == HGC_OK && io && io->seconds)
+        *io->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return rc;
+}
+
+// ============================================================ primitives
+// Propagator<float>::forward / inverse (propagation.hpp:81-95); Fourier when
+// fresnel == NULL (fft_forward / fft_inverse, fft.hpp:93-113).  Same pass
+// order as the fused loop: forward = rows then columns (+norm), inverse =
+// columns then rows (+norm, *conj(Q)).
+int hgc_propagate(int nx, int ny, int sign, const hgc_fresnel* fresnel, int batch, const float* in, float* out) {
+    return guarded([&] {
+        if (!in || !out) invalid("fft: null buffer");
+        if (sign != -1 && sign != 1) invalid("fft: sign must be -1 or +1");
+        if (batch < 1) invalid("fft: batch must be >= 1");
+        if (fresnel) validate_fresnel(fresnel);
+        check_size(nx, ny);
+        const float2* tw = device_twiddles();
+        prepare_kernels(nx, ny);
+        const size_t npix = (size_t)nx * ny, tot = npix * batch;
+        for (size_t i = 0; i < 2 * tot; ++i)  // require_finite, fft.hpp:95-97 / :106-108
+            if (!std::isfinite(in[i]))
+                invalid(std::string(sign < 0 ? "fft_forward" : "fft_inverse") + ": field contains non-finite values");
+        DBuf<float2> f, q;
+        f.alloc(tot);
+        cudaStream_t st;
+        CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        if (fresnel) {
+            q.alloc(npix);
+            double scale = 3.1415926535897932384626433832795 / (fresnel->wavelength * fresnel->distance);
+            k_fresnel_q<<<ew_grid(npix), 256, 0, st>>>(nx, ny, scale, fresnel->pixel_pitch_x, fresnel->pixel_pitch_y,
+                                                       q.p);
+        }
+        CK(cudaMemcpyAsync(f.p, in, sizeof(float2) * tot, cudaMemcpyHostToDevice, st));
+        const float norm = (float)(1.0 / std::sqrt((double)nx * ny));  // fftw_backend.cpp:121
+        RowArgs ra{};
+        ra.tw = tw;
+        ra.field = f.p;
+        ra.bstride = npix;
+        ra.ny = ny;
+        ra.sign = sign;
+        ra.norm = norm;
+        ra.apply_norm = sign > 0;
+        ra.fresnel_q = q.p;
+        ColArgs ca{};
+        ca.tw = tw;
+        ca.field = f.p;
+        ca.bstride = npix;
+        ca.nx = nx;
+        ca.sign = sign;
+        ca.norm = norm;
+        ca.apply_norm = sign < 0;
+        if (sign < 0) {
+            row_plain(nx, ra, batch, st);
+            col_plain(ny, ca, batch, st);
+        } else {
+            col_plain(ny, ca, batch, st);
+            row_plain(nx, ra, batch, st);
+        }
+        CK(cudaMemcpyAsync(out, f.p, sizeof(float2) * tot, cudaMemcpyDeviceToHost, st));
+        cudaError_t e = cudaStreamSynchronize(st);
+        cudaStreamDestroy(st);
+        CK(e);
+    });
+}
+
+int hgc_fft2d(int nx, int ny, int sign, int batch, const float* in, float* out) {
+    return hgc_propagate(nx, ny, sign, nullptr, batch, in, out);
+}
+
+int hgc_quantise(const hgc_slm* slm, int nx, int ny, int batch, float* field, int32_t* levels) {
+    return guarded([&] {
+        if (!field) invalid("quantise: null field");
+        if (nx <= 0 || ny <= 0 || batch < 1) invalid("Quantiser: field dimensions mismatch");
+        const size_t npix = (size_t)nx * ny, tot = npix * batch;
+        validate_slm(slm, npix);
+        const float2* tw = device_twiddles();
+        QuantDev q;
+        build_quant(slm, nx, ny, q);
+        DBuf<float2> f;
+        DBuf<int32_t> lv;
+        f.alloc(tot);
+        if (levels) lv.alloc(tot);
+        CK(cudaMemcpy(f.p, field, sizeof(float2) * tot, cudaMemcpyHostToDevice));
+        k_quantise<<<ew_grid(tot), 256>>>(f.p, lv.p, npix, tot, q.p);
+        CK(cudaGetLastError());
+        CK(cudaMemcpy(field, f.p, sizeof(float2) * tot, cudaMemcpyDeviceToHost));
+        if (levels) CK(cudaMemcpy(levels, lv.p, sizeof(int32_t) * tot, cudaMemcpyDeviceToHost));
+    });
+}
+
+int hgc_seed_random_phase(const double* amplitude, int nx, int ny, uint64_t engine_seed, uint64_t skip, float* out) {
+    return guarded([&] {
+        if (!amplitude || !out) invalid("seed_random_phase: null buffer");
+        if (nx <= 0 || ny <= 0) invalid("RealImage: dimensions must be positive");
+        const size_t npix = (size_t)nx * ny;
+        require_finite_img(amplitude, npix, "seed_random_phase");
+        const float2* tw = device_twiddles();
+        CK(cudaFuncSetAttribute(k_seed_random_phase, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSeedSmem));
+        DBuf<double> a;
+        DBuf<float2> f;
+        DBuf<MtState> mt;
+        DBuf<uint64_t> sd;
+        a.alloc(npix);
+        f.alloc(npix);
+        mt.alloc(1);
+        sd.alloc(1);
+        CK(cudaMemcpy(a.p, amplitude, sizeof(double) * npix, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(sd.p, &engine_seed, sizeof(uint64_t), cudaMemcpyHostToDevice));
+        SeedArgs sa{};
+        sa.states = mt.p;
+        sa.seeds = sd.p;
+        if (skip) {  // advance the stream without producing output
+            sa.npix = skip;
+            k_seed_random_phase<<<1, kSeedThreads, kSeedSmem>>>(sa);
+            CK(cudaGetLastError());
+            sa.seeds = nullptr;
+        }
+        sa.amp = a.p;
+        sa.out = f.p;
+        sa.npix = npix;
+        k_seed_random_phase<<<1, kSeedThreads, kSeedSmem>>>(sa);
+        CK(cudaGetLastError());
+        CK(cudaMemcpy(out, f.p, sizeof(float2) * npix, cudaMemcpyDeviceToHost));
+    });
+}
+
+int hgc_mse(const double* target, const float* replay, const uint8_t* mask, int nx, int ny, int scale_free,
+            double* out) {
+    return guarded([&] {
+        if (!target || !replay || !out) invalid("metric: null buffer");
+        if (nx <= 0 || ny <= 0) invalid("metric: target and replay dimensions mismatch");
+        const size_t n = (size_t)nx * ny;
+        require_finite_img(target, n, "metric");
+        for (size_t i = 0; i < 2 * n; ++i)
+            if (!std::isfinite(replay[i])) invalid("metric: field contains non-finite values");
+        if (mask) {
+            size_t m = 0;
+            for (size_t i = 0; i < n; ++i) m += mask[i] != 0;
+            if (m == 0) invalid("MetricConfig: mask covers no pixels");
+        }
+        const float2* tw = device_twiddles();
+        DBuf<double> t, part;
+        DBuf<float2> r;
+        DBuf<uint8_t> m;
+        t.alloc(n);
+        r.alloc(n);
+        const int blocks = 148 * 2;
+        part.alloc((size_t)blocks * 5);
+        CK(cudaMemcpy(t.p, target, sizeof(double) * n, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(r.p, replay, sizeof(float2) * n, cudaMemcpyHostToDevice));
+        if (mask) {
+            m.alloc(n);
+            CK(cudaMemcpy(m.p, mask, n, cudaMemcpyHostToDevice));
+        }
+        k_mse_partials<<<blocks, 256>>>(t.p, r.p, m.p, n, part.p);
+        CK(cudaGetLastError());
+        std::vector<double> h((size_t)blocks * 5);
+        CK(cudaMemcpy(h.data(), part.p, sizeof(double) * h.size(), cudaMemcpyDeviceToHost));
+        double s[5] = {0, 0, 0, 0, 0};
+        for (int b = 0; b < blocks; ++b)
+            for (int v = 0; v < 5; ++v) s[v] += h[(size_t)b * 5 + v];
+        if (!scale_free) {
+            *out = s[0] / s[4];
+        } else {
+            double g = s[2] > 0.0 ? s[1] / s[2] : 0.0;
+            if (g < 0.0) g = 0.0;
+            double v = s[3] - 2.0 * g * s[1] + g * g * s[2];
+            *out = (v < 0 ? 0.0 : v) / s[4];
+        }
+    });
+}
+
+int hgc_fresnel_phase(int nx, int ny, const hgc_fresnel* prm, float* q) {
+    return guarded([&] {
+        if (!prm || !q) invalid("make_fresnel_phase: null argument");
+        validate_fresnel(prm);
+        if (nx <= 0 || ny <= 0) invalid("ComplexField: dimensions must be positive");
+        const size_t n = (size_t)nx * ny;
+        DBuf<float2> d;
+        d.alloc(n);
+        double scale = 3.1415926535897932384626433832795 / (prm->wavelength * prm->distance);
+        k_fresnel_q<<<ew_grid(n), 256>>>(nx, ny, scale, prm->pixel_pitch_x, prm->pixel_pitch_y, d.p);
+        CK(cudaGetLastError());
+        CK(cudaMemcpy(q, d.p, sizeof(float2) * n, cudaMemcpyDeviceToHost));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,58 @@
+// common.cuh — shared device helpers for the HoloGen B200 hot path.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define HG_TWO_PI 6.283185307179586476925286766559
+#define HG_PI 3.1415926535897932384626433832795
+
+// Complex products with every product/sum rounded separately (no FMA
+// contraction), i.e. the way GCC evaluates std::complex<float> operator* on
+// baseline x86-64: (a+bi)(c+di) = (ac - bd) + (ad + bc)i.  Used wherever the
+// reference multiplies complex<T> values (quantise.hpp:201-205,
+// propagation.hpp:85, :93) so results match bit for bit.
+__device__ __forceinline__ float2 cmul_rn(float2 a, float2 b) {
+    float ac = __fmul_rn(a.x, b.x), bd = __fmul_rn(a.y, b.y);
+    float ad = __fmul_rn(a.x, b.y), bc = __fmul_rn(a.y, b.x);
+    return make_float2(__fsub_rn(ac, bd), __fadd_rn(ad, bc));
+}
+
+// a * conj(b), evaluated as GCC does for z *= std::conj(q):
+// (a+bi)(c-di): real = ac - b(-d) = ac + bd, imag = a(-d) + bc.
+__device__ __forceinline__ float2 cmul_conj_rn(float2 a, float2 b) {
+    float ac = __fmul_rn(a.x, b.x), bd = __fmul_rn(a.y, b.y);
+    float ad = __fmul_rn(a.x, b.y), bc = __fmul_rn(a.y, b.x);
+    return make_float2(__fadd_rn(ac, bd), __fsub_rn(bc, ad));
+}
+
+// Fast complex product for FFT butterflies (FMA allowed).
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cscale(float2 a, float s) {
+    return make_float2(__fmul_rn(a.x, s), __fmul_rn(a.y, s));
+}
+
+// Opaque copies: the compiler must recompute anything derived from the
+// result instead of keeping it live in registers (used to stop 16 64-bit
+// load addresses from staying live across an FFT until the stores).
+__device__ __forceinline__ int opaque(int x) {
+    int y;
+    asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
+    return y;
+}
+template <class T>
+__device__ __forceinline__ T* opaque(T* p) {
+    unsigned long long y;
+    asm volatile("mov.b64 %0, %1;" : "=l"(y) : "l"((unsigned long long)p));
+    return (T*)y;
+}
+
+template <int V>
+struct IntC {
+    static constexpr int value = V;
+};
+
+constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n >> 1); }

@@ -1,0 +1,250 @@
+// fft.cuh — register/shared-memory Stockham FFT for one line (row or column)
+// of a complex64 field, the building block of the fused passes.
+//
+// Replaces the FFTW 2-D c2c transform behind FftBackend<float>
+// (fft.hpp:17-27, fftw_backend.cpp:113-124).  A line of N points is owned by
+// T = N/E threads; thread t holds elements t + e*T (e < E) in registers
+// ("strided ownership") — the natural layout of a coalesced load/store.
+// Each Stockham radix-R pass takes its butterfly inputs from the thread's
+// own registers; outputs of every pass but the last are exchanged through
+// shared memory; the last pass lands back in strided ownership, so the line
+// is stored with the same coalesced pattern it was loaded with.
+//
+// Twiddles come from a per-length table tw[N + m] = exp(-2*pi*i*m/N)
+// (N = 1..4096, 8192 entries), computed in double once per device and read
+// through the read-only path.  SIGN = -1 forward, +1 inverse (unnormalised, like FFTW;
+// the unitary 1/sqrt(nx*ny) scale is applied by the fused passes exactly
+// where fftw_backend.cpp:121-123 applies it).
+#pragma once
+#include "common.cuh"
+
+namespace hg {
+
+constexpr int kMaxLine = 4096;
+
+// ---------------------------------------------------------------- radix-R
+template <int SIGN>
+__device__ __forceinline__ float2 mul_si(float2 a) {  // a * (SIGN * i)
+    return SIGN < 0 ? make_float2(a.y, -a.x) : make_float2(-a.y, a.x);
+}
+
+// W16^m = exp(SIGN*2*pi*i*m/16), applied to a (compile-time m).
+template <int SIGN, int M>
+__device__ __forceinline__ float2 tw16(float2 a) {
+    constexpr int m = M & 15;
+    constexpr float c1 = 0.92387953251128674f, s1 = 0.38268343236508978f, h = 0.70710678118654752f;
+    if constexpr (m == 0) return a;
+    else if constexpr (m == 4) return mul_si<SIGN>(a);
+    else if constexpr (m == 8) return make_float2(-a.x, -a.y);
+    else if constexpr (m == 12) return mul_si<-SIGN>(a);
+    else {
+        // cos/sin of 2*pi*m/16 for the remaining m
+        constexpr float cs[16] = {1.f, c1, h, s1, 0.f, -s1, -h, -c1, -1.f, -c1, -h, -s1, 0.f, s1, h, c1};
+        constexpr float sn[16] = {0.f, s1, h, c1, 1.f, c1, h, s1, 0.f, -s1, -h, -c1, -1.f, -c1, -h, -s1};
+        return cmul(a, make_float2(cs[m], SIGN * sn[m]));
+    }
+}
+
+template <int SIGN>
+__device__ __forceinline__ void dft2(float2& a, float2& b) {
+    float2 t = a;
+    a = cadd(t, b);
+    b = csub(t, b);
+}
+
+template <int SIGN>
+__device__ __forceinline__ void dft4(float2& v0, float2& v1, float2& v2, float2& v3) {
+    float2 t0 = cadd(v0, v2), t1 = csub(v0, v2);
+    float2 t2 = cadd(v1, v3), t3 = mul_si<SIGN>(csub(v1, v3));
+    v0 = cadd(t0, t2);
+    v2 = csub(t0, t2);
+    v1 = cadd(t1, t3);
+    v3 = csub(t1, t3);
+}
+
+// In-place DFT of R values, natural order in and out:
+//   x[k] <- sum_r x[r] exp(SIGN*2*pi*i*r*k/R)
+template <int R, int SIGN>
+__device__ __forceinline__ void dft(float2* x) {
+    if constexpr (R == 1) {
+    } else if constexpr (R == 2) {
+        dft2<SIGN>(x[0], x[1]);
+    } else if constexpr (R == 4) {
+        dft4<SIGN>(x[0], x[1], x[2], x[3]);
+    } else if constexpr (R == 8) {
+        // r = 2a + b; Y_b = DFT4_a(x[2a+b]); Y_b[k1] *= W8^(b k1); X[k1+4k2] = DFT2_b
+        float2 y0[4] = {x[0], x[2], x[4], x[6]};
+        float2 y1[4] = {x[1], x[3], x[5], x[7]};
+        dft4<SIGN>(y0[0], y0[1], y0[2], y0[3]);
+        dft4<SIGN>(y1[0], y1[1], y1[2], y1[3]);
+        y1[1] = tw16<SIGN, 2>(y1[1]);
+        y1[2] = tw16<SIGN, 4>(y1[2]);
+        y1[3] = tw16<SIGN, 6>(y1[3]);
+#pragma unroll
+        for (int k1 = 0; k1 < 4; ++k1) {
+            x[k1] = cadd(y0[k1], y1[k1]);
+            x[k1 + 4] = csub(y0[k1], y1[k1]);
+        }
+    } else if constexpr (R == 16) {
+        // r = 4a + b; Y_b = DFT4_a(x[4a+b]); Y_b[k1] *= W16^(b k1); X[k1+4k2] = DFT4_b
+        float2 y[4][4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            y[b][0] = x[b];
+            y[b][1] = x[4 + b];
+            y[b][2] = x[8 + b];
+            y[b][3] = x[12 + b];
+            dft4<SIGN>(y[b][0], y[b][1], y[b][2], y[b][3]);
+        }
+        y[1][1] = tw16<SIGN, 1>(y[1][1]);
+        y[1][2] = tw16<SIGN, 2>(y[1][2]);
+        y[1][3] = tw16<SIGN, 3>(y[1][3]);
+        y[2][1] = tw16<SIGN, 2>(y[2][1]);
+        y[2][2] = tw16<SIGN, 4>(y[2][2]);
+        y[2][3] = tw16<SIGN, 6>(y[2][3]);
+        y[3][1] = tw16<SIGN, 3>(y[3][1]);
+        y[3][2] = tw16<SIGN, 6>(y[3][2]);
+        y[3][3] = tw16<SIGN, 9>(y[3][3]);
+#pragma unroll
+        for (int k1 = 0; k1 < 4; ++k1) {
+            dft4<SIGN>(y[0][k1], y[1][k1], y[2][k1], y[3][k1]);
+            x[k1] = y[0][k1];
+            x[k1 + 4] = y[1][k1];
+            x[k1 + 8] = y[2][k1];
+            x[k1 + 12] = y[3][k1];
+        }
+    }
+}
+
+// Elements per thread for a line of N points.
+template <int N>
+struct LineCfg {
+    static constexpr int E = N < 16 ? N : 16;
+    static constexpr int T = N / E;
+};
+
+// Twiddle exp(SIGN*2*pi*i*m/N) from the forward table.
+template <int N, int SIGN>
+__device__ __forceinline__ float2 twiddle(const float2* __restrict__ tw, int m) {
+    float2 w = __ldg(&tw[N + m]);
+    if constexpr (SIGN > 0) w.y = -w.y;
+    return w;
+}
+
+// x[r] *= w^r, w = exp(SIGN*2*pi*i*m/N), r = 1..R-1.  For R = 16 only w, w^4
+// and w^8 come from the table (the rest are <= 2 products of table values,
+// error <= ~2 ulp): 3 loads instead of 15 keeps the pass within the register
+// budget of a 1024-thread CTA.
+template <int N, int SIGN, int R>
+__device__ __forceinline__ void apply_twiddles(float2* x, const float2* __restrict__ tw, int m) {
+    if constexpr (R == 16) {
+        const float2 w1 = twiddle<N, SIGN>(tw, m);
+        const float2 w4 = twiddle<N, SIGN>(tw, 4 * m);
+        const float2 w8 = twiddle<N, SIGN>(tw, 8 * m);
+        const float2 w2 = cmul(w1, w1), w3 = cmul(w2, w1), w12 = cmul(w8, w4);
+        x[1] = cmul(x[1], w1);
+        x[2] = cmul(x[2], w2);
+        x[3] = cmul(x[3], w3);
+        x[4] = cmul(x[4], w4);
+        x[8] = cmul(x[8], w8);
+        x[12] = cmul(x[12], w12);
+        x[5] = cmul(x[5], cmul(w4, w1));
+        x[6] = cmul(x[6], cmul(w4, w2));
+        x[7] = cmul(x[7], cmul(w4, w3));
+        x[9] = cmul(x[9], cmul(w8, w1));
+        x[10] = cmul(x[10], cmul(w8, w2));
+        x[11] = cmul(x[11], cmul(w8, w3));
+        x[13] = cmul(x[13], cmul(w12, w1));
+        x[14] = cmul(x[14], cmul(w12, w2));
+        x[15] = cmul(x[15], cmul(w12, w3));
+    } else {
+#pragma unroll
+        for (int r = 1; r < R; ++r) x[r] = cmul(x[r], twiddle<N, SIGN>(tw, r * m));
+    }
+}
+
+// One Stockham pass (span NS) and, recursively, the rest.
+//   butterfly j = t + b*T (b < E/R) reads elements b + r*(E/R);
+//   twiddle by W_{NS*R}^{r*(j mod NS)}; DFT_R;
+//   output r goes to position (j/NS)*NS*R + (j mod NS) + r*NS.
+// SmemIdx maps a line position to a shared-memory slot for this thread's line.
+template <int N, int SIGN, int NS>
+struct StockhamPass {
+    template <class SmemIdx>
+    __device__ __forceinline__ static void run(float2 (&v)[LineCfg<N>::E], int t, float2* sm,
+                                               const SmemIdx& idx, const float2* __restrict__ tw) {
+        constexpr int E = LineCfg<N>::E, T = LineCfg<N>::T;
+        constexpr int R = (N / NS >= E) ? E : N / NS;
+        constexpr int B = E / R;
+        constexpr bool last = (NS * R == N);
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+            float2 x[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) x[r] = v[b + r * B];
+            const int j = t + b * T;
+            const int k = j & (NS - 1);
+            if constexpr (NS > 1) apply_twiddles<N, SIGN, R>(x, tw, k * (N / (NS * R)));
+            dft<R, SIGN>(x);
+            if constexpr (last) {
+#pragma unroll
+                for (int r = 0; r < R; ++r) v[b + r * B] = x[r];
+            } else {
+                // positions base + r*NS; with NS == 1 (R <= 16) or NS % 16 == 0
+                // the padded slots are linear in r: slot(base) + r*stride
+                const int base = (j / NS) * NS * R + k;
+                const int s0 = idx(base);
+                constexpr int rs = (NS == 1) ? 1 : NS + NS / 16;
+#pragma unroll
+                for (int r = 0; r < R; ++r) sm[s0 + r * rs * SmemIdx::kLineStride] = x[r];
+            }
+        }
+        if constexpr (!last) {
+            __syncthreads();
+            if constexpr (T % 16 == 0) {
+                const int s0 = idx(t);
+                constexpr int es = T + T / 16;
+#pragma unroll
+                for (int e = 0; e < E; ++e) v[e] = sm[s0 + e * es * SmemIdx::kLineStride];
+            } else {
+#pragma unroll
+                for (int e = 0; e < E; ++e) v[e] = sm[idx(t + e * T)];
+            }
+            __syncthreads();
+            StockhamPass<N, SIGN, NS * R>::run(v, t, sm, idx, tw);
+        }
+    }
+};
+
+// Full unnormalised 1-D transform of one line held in strided ownership.
+// Every thread of the CTA must call it (it contains __syncthreads when N > E).
+template <int N, int SIGN, class SmemIdx>
+__device__ __forceinline__ void fft_line(float2 (&v)[LineCfg<N>::E], int t, float2* sm, const SmemIdx& idx,
+                                         const float2* __restrict__ tw) {
+    StockhamPass<N, SIGN, 1>::run(v, t, sm, idx, tw);
+}
+
+// Padded slot for position q of a line: one pad slot every 16 keeps the
+// radix-16 scatter (stride 16) free of bank conflicts.
+__device__ __forceinline__ int pad16(int q) { return q + (q >> 4); }
+template <int N>
+struct PaddedLen {
+    static constexpr int value = N + (N >> 4) + 1;
+};
+
+// Row layout: each line owns a contiguous padded region.
+struct RowSmemIdx {
+    static constexpr int kLineStride = 1;  // slot step per position step
+    int off;
+    __device__ __forceinline__ int operator()(int q) const { return off + pad16(q); }
+};
+// Column layout: C lines interleaved (slot * C + c) so a warp spanning
+// C adjacent columns hits adjacent banks.
+template <int C>
+struct ColSmemIdx {
+    static constexpr int kLineStride = C;
+    int c;
+    __device__ __forceinline__ int operator()(int q) const { return pad16(q) * C + c; }
+};
+
+}  // namespace hg

@@ -1,0 +1,9 @@
+// k_col_ospr.cu — OSPR replay pass: forward columns + intensity accumulation
+// + per-frame and cumulative MSE partials.
+#include "launch_impl.cuh"
+
+namespace hg {
+void col_ospr(int ny, const ColArgs& a, int batch, cudaStream_t st, bool prepare) {
+    col_dispatch<COL_OSPR>(ny, a, batch, st, prepare);
+}
+}  // namespace hg

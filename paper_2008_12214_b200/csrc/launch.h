@@ -1,0 +1,20 @@
+// launch.h — host entry points of the per-size kernel instantiations, one
+// translation unit per pass family so they compile in parallel.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "passes.cuh"
+
+namespace hg {
+
+// prepare = true only sets the kernel attributes (dynamic shared memory);
+// call it outside stream capture before the first launch of a size.
+void row_fused(int nx, const RowArgs& a, int batch, cudaStream_t st, bool prepare = false);
+void row_plain(int nx, const RowArgs& a, int batch, cudaStream_t st, bool prepare = false);
+void col_plain(int ny, const ColArgs& a, int batch, cudaStream_t st, bool prepare = false);
+void col_gs(int ny, const ColArgs& a, int batch, cudaStream_t st, bool prepare = false);
+void col_ospr(int ny, const ColArgs& a, int batch, cudaStream_t st, bool prepare = false);
+// Column tiles (CTAs) per target of the column pass for an nx x ny field.
+int col_tiles(int nx, int ny);
+
+}  // namespace hg

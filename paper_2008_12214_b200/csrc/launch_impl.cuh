@@ -1,0 +1,81 @@
+// launch_impl.cuh — size dispatch shared by the k_*.cu translation units.
+#pragma once
+#include "errors.h"
+#include "launch.h"
+
+namespace hg {
+
+template <class K>
+inline void set_smem(K kernel, int bytes) {
+    if (bytes > 48 * 1024) CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+}
+
+template <int NX, int MODE>
+inline void row_launch(const RowArgs& a, int batch, cudaStream_t st, bool prepare) {
+    using Cfg = RowCfg<NX>;
+    auto kern = k_row<NX, MODE>;
+    if (prepare) {
+        set_smem(kern, Cfg::SMEM);
+        return;
+    }
+    dim3 grid((a.ny + Cfg::RPC - 1) / Cfg::RPC, batch);
+    kern<<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(a);
+    CK(cudaGetLastError());
+}
+
+template <int MODE>
+inline void row_dispatch(int nx, const RowArgs& a, int batch, cudaStream_t st, bool prepare) {
+    switch (nx) {
+#define HG_ROW(N) \
+    case N: row_launch<N, MODE>(a, batch, st, prepare); break;
+        HG_ROW(2) HG_ROW(4) HG_ROW(8) HG_ROW(16) HG_ROW(32) HG_ROW(64) HG_ROW(128) HG_ROW(256)
+        HG_ROW(512) HG_ROW(1024) HG_ROW(2048) HG_ROW(4096)
+#undef HG_ROW
+        default: fail(HGC_EUNSUPPORTED, "row length unsupported");
+    }
+}
+
+template <int NY>
+inline int col_width(int nx) {
+    int c = ColCfg<NY>::C;
+    return c < nx ? c : nx;
+}
+
+template <int NY, int C, int MODE>
+inline void col_launch_c(const ColArgs& a, int batch, cudaStream_t st, bool prepare) {
+    auto kern = k_col<NY, C, MODE>;
+    constexpr int smem = (NY > LineCfg<NY>::E) ? PaddedLen<NY>::value * C * (int)sizeof(float2) : 0;
+    if (prepare) {
+        set_smem(kern, smem);
+        return;
+    }
+    dim3 grid(a.nx / C, batch);
+    kern<<<grid, LineCfg<NY>::T * C, smem, st>>>(a);
+    CK(cudaGetLastError());
+}
+
+template <int NY, int MODE>
+inline void col_launch(const ColArgs& a, int batch, cudaStream_t st, bool prepare) {
+    switch (col_width<NY>(a.nx)) {
+        case 1: if constexpr (ColCfg<NY>::C >= 1) col_launch_c<NY, 1, MODE>(a, batch, st, prepare); break;
+        case 2: if constexpr (ColCfg<NY>::C >= 2) col_launch_c<NY, 2, MODE>(a, batch, st, prepare); break;
+        case 4: if constexpr (ColCfg<NY>::C >= 4) col_launch_c<NY, 4, MODE>(a, batch, st, prepare); break;
+        case 8: if constexpr (ColCfg<NY>::C >= 8) col_launch_c<NY, 8, MODE>(a, batch, st, prepare); break;
+        case 16: if constexpr (ColCfg<NY>::C >= 16) col_launch_c<NY, 16, MODE>(a, batch, st, prepare); break;
+        default: fail(HGC_EUNSUPPORTED, "column tile unsupported");
+    }
+}
+
+template <int MODE>
+inline void col_dispatch(int ny, const ColArgs& a, int batch, cudaStream_t st, bool prepare) {
+    switch (ny) {
+#define HG_COL(N) \
+    case N: col_launch<N, MODE>(a, batch, st, prepare); break;
+        HG_COL(2) HG_COL(4) HG_COL(8) HG_COL(16) HG_COL(32) HG_COL(64) HG_COL(128) HG_COL(256)
+        HG_COL(512) HG_COL(1024) HG_COL(2048) HG_COL(4096)
+#undef HG_COL
+        default: fail(HGC_EUNSUPPORTED, "column length unsupported");
+    }
+}
+
+}  // namespace hg

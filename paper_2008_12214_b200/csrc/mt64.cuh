@@ -1,0 +1,184 @@
+// mt64.cuh — bit-exact std::mt19937_64 stream on the GPU and the fused
+// random-phase seed (seed_random_phase<float>, rng.hpp:54-67).
+//
+// The reference draws every random phase from ONE std::mt19937_64 stream
+// seeded with Rng(seed).fork(0) (rng.hpp:42-44; ifta.hpp:124; ospr.hpp:89),
+// one draw per pixel in row-major order, OSPR subframe k consuming draws
+// [k*npix, (k+1)*npix).  The engine's 312-word twist is parallel within a
+// block of 312 words, so one warp regenerates the raw-word sequence into a
+// shared-memory ring while the rest of the CTA tempers the words and
+// evaluates (T)(a*cos(2*pi*u)), (T)(a*sin(2*pi*u)) in double — the DP sincos
+// is the real cost and is spread across 15 warps.  The stream state (the
+// twist block holding the next draw + position) is saved to global memory at
+// the end of a launch so the next subframe continues the same stream.
+#pragma once
+#include "common.cuh"
+
+namespace hg {
+
+constexpr int kMtN = 312;
+constexpr int kMtM = 156;
+constexpr uint64_t kMtUM = 0xFFFFFFFF80000000ull;
+constexpr uint64_t kMtLM = 0x000000007FFFFFFFull;
+constexpr uint64_t kMtA = 0xB5026F5AA96619E9ull;
+
+// Saved stream position: the twist block that holds the next draw, and the
+// index of that draw within the block (312 = block exhausted).
+struct MtState {
+    uint64_t w[kMtN];
+    int pos;
+    int pad_;
+};
+
+__host__ __device__ inline uint64_t mix64(uint64_t z) {  // rng.hpp:12-17
+    z += 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d4a2c62a2b3b9full;
+    return z ^ (z >> 31);
+}
+__host__ __device__ inline uint64_t fork_seed(uint64_t seed, uint64_t stream) {  // rng.hpp:42-44
+    return mix64(seed ^ mix64(stream + 1));
+}
+
+__device__ __forceinline__ uint64_t mt_temper(uint64_t x) {
+    x ^= (x >> 29) & 0x5555555555555555ull;
+    x ^= (x << 17) & 0x71D67FFFEDA60000ull;
+    x ^= (x << 37) & 0xFFF7EEE000000000ull;
+    x ^= (x >> 43);
+    return x;
+}
+
+__device__ __forceinline__ uint64_t mt_mix(uint64_t hi, uint64_t lo) {
+    uint64_t x = (hi & kMtUM) | (lo & kMtLM);
+    return (x >> 1) ^ ((x & 1ull) ? kMtA : 0ull);
+}
+
+// One twist by a single warp: nw <- twist(ow).  Same recurrence as the
+// in-place libstdc++ _M_gen_rand, written out-of-place.
+__device__ __forceinline__ void mt_twist_warp(const uint64_t* ow, uint64_t* nw, int lane) {
+    for (int i = lane; i < kMtN - kMtM; i += 32) nw[i] = ow[i + kMtM] ^ mt_mix(ow[i], ow[i + 1]);
+    __syncwarp();
+    for (int i = kMtN - kMtM + lane; i < kMtN - 1; i += 32) nw[i] = nw[i - (kMtN - kMtM)] ^ mt_mix(ow[i], ow[i + 1]);
+    if (lane == 0) nw[kMtN - 1] = nw[kMtM - 1] ^ mt_mix(ow[kMtN - 1], nw[0]);
+    __syncwarp();
+}
+
+constexpr int kSeedThreads = 512;
+constexpr int kTwistsPerGroup = 8;
+constexpr int kRingSlots = 2 * kTwistsPerGroup;  // two groups: one produced while one is consumed
+constexpr size_t kSeedSmem = sizeof(uint64_t) * kMtN * kRingSlots;
+
+struct SeedArgs {
+    MtState* states;           // [streams]
+    const uint64_t* seeds;     // [streams] engine seeds (already forked) or nullptr = continue
+    const double* amp;         // amplitude (double, as RealImage), per stream stride amp_stride
+    size_t amp_stride;
+    float2* out;               // seeded field, per stream stride out_stride
+    size_t out_stride;
+    size_t npix;               // draws (pixels) this launch
+    // adaptive OSPR intensity budget (ospr.hpp:106-116): amp for frame n >= 2
+    // is (1-g)*T + g*sqrt(max(0, n*T^2 - (n-1)*(S/(n-1)))), S = running sum.
+    const float* S;            // [streams][npix] or nullptr (plain amplitude)
+    size_t S_stride;
+    int n;
+    double gain;
+};
+
+// One CTA per stream.  Warp 0 produces twists; warps 1.. consume.
+__global__ void __launch_bounds__(kSeedThreads) k_seed_random_phase(SeedArgs a) {
+    extern __shared__ uint64_t ring[];  // kRingSlots * 312 words
+    __shared__ int s_pos;
+    const int s = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    MtState* st = a.states + s;
+    uint64_t* init = ring + (kRingSlots - 1) * kMtN;  // twist "-1" lives in the last slot
+    if (a.seeds) {
+        if (tid == 0) {  // std::mt19937_64::seed
+            uint64_t x = a.seeds[s];
+            init[0] = x;
+            for (int i = 1; i < kMtN; ++i) {
+                x = 6364136223846793005ull * (x ^ (x >> 62)) + (uint64_t)i;
+                init[i] = x;
+            }
+            s_pos = kMtN;
+        }
+    } else {
+        for (int i = tid; i < kMtN; i += blockDim.x) init[i] = st->w[i];
+        if (tid == 0) s_pos = st->pos;
+    }
+    __syncthreads();
+    const int pos0 = s_pos;
+    const size_t npix = a.npix;
+    const double* amp = a.amp + a.amp_stride * s;
+    float2* out = a.out + a.out_stride * s;
+
+    // draws available from the initial block, then 8-twist groups
+    const size_t first = (size_t)(kMtN - pos0) < npix ? (size_t)(kMtN - pos0) : npix;
+    const size_t rest = npix - first;
+    const long long ngroups = (long long)((rest + (size_t)kMtN * kTwistsPerGroup - 1) / ((size_t)kMtN * kTwistsPerGroup));
+
+    const int cthreads = blockDim.x - 32;
+    const int ctid = tid - 32;
+    // step g: producer writes group g (g < ngroups); consumers process group g-1
+    // (g = 0: the initial partial block).
+    for (long long g = 0; g <= ngroups; ++g) {
+        if (warp == 0) {
+            if (g < ngroups) {
+                for (int k = 0; k < kTwistsPerGroup; ++k) {
+                    int t = (int)(g * kTwistsPerGroup + k);
+                    const uint64_t* ow = ring + ((t - 1 + kRingSlots) % kRingSlots) * kMtN;
+                    uint64_t* nw = ring + (t % kRingSlots) * kMtN;
+                    mt_twist_warp(ow, nw, lane);
+                }
+            }
+        } else {
+            const uint64_t* src;
+            size_t d0, cnt;
+            if (g == 0) {
+                src = init + pos0;
+                d0 = 0;
+                cnt = first;
+            } else {
+                src = ring + (((g - 1) & 1) * kTwistsPerGroup) * kMtN;
+                d0 = first + (size_t)(g - 1) * kMtN * kTwistsPerGroup;
+                size_t left = npix - d0;
+                cnt = left < (size_t)kMtN * kTwistsPerGroup ? left : (size_t)kMtN * kTwistsPerGroup;
+            }
+            if (a.out)  // out == nullptr: advance the stream only (skip draws)
+            for (size_t j = ctid; j < cnt; j += cthreads) {
+                uint64_t x = mt_temper(src[j]);
+                double u = (double)(x >> 11) * 0x1.0p-53;             // Rng::uniform01, rng.hpp:32
+                double theta = __dmul_rn(HG_TWO_PI, u);               // rng.hpp:62
+                double sn, cs;
+                sincos(theta, &sn, &cs);
+                double av = amp[d0 + j];
+                if (a.S) {
+                    const double tv = av, t2 = __dmul_rn(tv, tv);
+                    const double sv = (double)a.S[a.S_stride * s + d0 + j];
+                    const double n = a.n;
+                    double budget = __dsub_rn(__dmul_rn(n, t2), __dmul_rn(n - 1.0, __ddiv_rn(sv, n - 1.0)));
+                    double tn = __dsqrt_rn(budget > 0.0 ? budget : 0.0);
+                    av = __dadd_rn(__dmul_rn(1.0 - a.gain, tv), __dmul_rn(a.gain, tn));
+                }
+                out[d0 + j] = make_float2(__double2float_rn(__dmul_rn(av, cs)),
+                                          __double2float_rn(__dmul_rn(av, sn)));
+            }
+        }
+        __syncthreads();
+    }
+    // save the block holding the next draw
+    const uint64_t* keep;
+    int pos;
+    if (rest == 0) {
+        keep = init;
+        pos = pos0 + (int)npix;
+    } else {
+        long long tl = (long long)((rest - 1) / kMtN);
+        keep = ring + (tl % kRingSlots) * kMtN;
+        pos = (int)((rest - 1) % kMtN) + 1;
+    }
+    for (int i = tid; i < kMtN; i += blockDim.x) st->w[i] = keep[i];
+    if (tid == 0) st->pos = pos;
+}
+
+}  // namespace hg

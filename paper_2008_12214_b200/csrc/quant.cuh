@@ -1,0 +1,114 @@
+// quant.cuh — the SLM quantiser (Quantiser<T>::decide / state_value,
+// quantise.hpp:175-205) as a device function fused into the row pass.
+//
+// Decision rule (phase mode): d = wrap_2pi(atan2(im, re) - illum_arg - min_arg);
+//   full circle: k = lround(d/spac), k == L -> 0;
+//   restricted : d <= range ? min(lround(d/spac), L-1)
+//                           : (d - range <= 2pi - d ? L-1 : 0)   (watershed)
+// amplitude mode: k = clamp(lround((|f| - min_amp)/spac), 0, L-1).
+//
+// The reference evaluates this in double (atan2/floor/lround).  Here a float
+// fast path (atan2f) decides every pixel whose value is farther than a
+// conservative margin from any decision boundary; pixels inside the margin
+// (~1e-3 of them at 256 levels) are re-decided with the reference's exact
+// double sequence (IEEE-rounded ops, no FMA contraction).  The margin bounds
+// the float path's worst-case error, so the fast path never disagrees with
+// the exact path; the only residual difference to the CPU is the ulp-level
+// difference between CUDA's and glibc's double atan2 on exact-threshold inputs.
+#pragma once
+#include "common.cuh"
+
+namespace hg {
+
+struct QuantParams {
+    int mode;  // 0 amplitude, 1 phase (SlmMode, quantise.hpp:14)
+    int levels;
+    int full_circle;
+    int pad_;
+    double min_arg, inv_spac, range, min_amp;  // exact (double) parameters
+    float min_arg_f, inv_spac_f, range_f, min_amp_f;
+    float wshed_f;    // watershed angle pi + range/2 (restricted phase mode)
+    float margin_rad; // decision margin in radians (phase mode)
+    float margin_u;   // same margin in level units
+    float pad2_;
+    const float2* states;      // [levels] (T)allowed_states, quantise.hpp:147-149
+    const double* illum_arg;   // [npix] arg(illumination) or nullptr
+    const float2* illum;       // [npix] (T)illumination (phase mode) or nullptr
+    const float2* illum_unit;  // [npix] (T)(illumination/|illumination|) or nullptr
+};
+
+// Exact reference sequence, quantise.hpp:175-198.  Out of line (scalar
+// arguments, no struct copy) so the ~1e-3 of pixels that need it do not
+// inflate every inlined copy of the fast path.
+__device__ __noinline__ int quant_decide_exact(int mode, int L, int full_circle, double min_arg, double inv_spac,
+                                               double range, double min_amp, double illum_arg, float vr, float vi) {
+    if (mode == 1) {
+        double ang = atan2((double)vi, (double)vr);
+        ang = __dsub_rn(ang, illum_arg);  // illum_arg = 0 without illumination (exact no-op)
+        double d = __dsub_rn(ang, min_arg);
+        d = __dsub_rn(d, __dmul_rn(HG_TWO_PI, floor(__ddiv_rn(d, HG_TWO_PI))));
+        if (full_circle) {
+            int k = (int)llround(__dmul_rn(d, inv_spac));
+            return k >= L ? 0 : k;
+        }
+        if (d <= range) {
+            int k = (int)llround(__dmul_rn(d, inv_spac));
+            return k > L - 1 ? L - 1 : k;
+        }
+        return (__dsub_rn(d, range) <= __dsub_rn(HG_TWO_PI, d)) ? L - 1 : 0;
+    }
+    double re = vr, im = vi;
+    double a = __dsqrt_rn(__dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im)));
+    long long k = llround(__dmul_rn(__dsub_rn(a, min_amp), inv_spac));
+    if (k < 0) k = 0;
+    if (k > L - 1) k = L - 1;
+    return (int)k;
+}
+
+__device__ __forceinline__ int quant_decide(const QuantParams& q, float vr, float vi, size_t i) {
+    const int L = q.levels;
+    bool near;
+    int k;
+    if (q.mode == 1) {
+        const float two_pi_f = 6.28318530717958648f;
+        float ang = atan2f(vi, vr);
+        if (q.illum_arg) ang -= (float)__ldg(&q.illum_arg[i]);
+        float d = ang - q.min_arg_f;
+        d -= two_pi_f * floorf(d * (1.0f / two_pi_f));
+        float u = d * q.inv_spac_f;
+        float fu = floorf(u);
+        float fr = u - fu;
+        near = fabsf(fr - 0.5f) < q.margin_u || d < q.margin_rad || d > two_pi_f - q.margin_rad;
+        int kr = (int)fu + (fr >= 0.5f ? 1 : 0);
+        if (q.full_circle) {
+            k = kr >= L ? 0 : kr;
+        } else if (d <= q.range_f) {
+            k = kr > L - 1 ? L - 1 : kr;
+        } else {
+            near = near || fabsf(d - q.wshed_f) < q.margin_rad;
+            k = d <= q.wshed_f ? L - 1 : 0;
+        }
+    } else {
+        float a = sqrtf(vr * vr + vi * vi);
+        float u = (a - q.min_amp_f) * q.inv_spac_f;
+        float fu = floorf(u);
+        float fr = u - fu;
+        float m = (a * 4e-7f + fabsf(q.min_amp_f) * 2e-7f) * q.inv_spac_f + fabsf(u) * 4e-7f + 1e-6f;
+        near = fabsf(fr - 0.5f) < m;
+        int kr = (int)fu + (fr >= 0.5f ? 1 : 0);
+        k = kr < 0 ? 0 : (kr > L - 1 ? L - 1 : kr);
+    }
+    if (near)
+        k = quant_decide_exact(q.mode, L, q.full_circle, q.min_arg, q.inv_spac, q.range, q.min_amp,
+                               q.illum_arg ? q.illum_arg[i] : 0.0, vr, vi);
+    return k;
+}
+
+// Quantiser::state_value, quantise.hpp:201-205
+__device__ __forceinline__ float2 quant_state(const QuantParams& q, int k, size_t i) {
+    float2 s = __ldg(&q.states[k]);
+    if (q.mode == 1) return q.illum ? cmul_rn(__ldg(&q.illum[i]), s) : s;
+    return q.illum_unit ? cmul_rn(__ldg(&q.illum_unit[i]), s) : s;
+}
+
+}  // namespace hg

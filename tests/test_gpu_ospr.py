@@ -1,0 +1,91 @@
+"""GPU parity of OSPR subframe generation (run_ospr_impl, ospr.hpp:68-164).
+
+Binary OSPR is checked free-running (0 level differences between
+f32 and f64 FFTs), at the BASELINE config 3 size (1024^2, 24 subframes).
+"""
+import numpy as np
+import pytest
+
+from helpers import level_mismatches, rel
+
+pytestmark = pytest.mark.gpu
+hg = pytest.importorskip("paper_2008_12214_b200")
+
+
+def ocfg(amp, N, seed, adaptive=False, gain=1.0):
+    return hg.OsprConfig(variant=hg.OsprVariant.AdaptiveOspr if adaptive else hg.OsprVariant.Ospr, subframes=N,
+                         slm=hg.SlmSpec.binary_phase(), target=hg.TargetSpec(amp), seed=seed, feedback_gain=gain)
+
+
+def test_ospr_small_matches_reference_fixture():
+    g = np.load(__file__.replace("test_gpu_ospr.py", "golden/ref_runs.npz"))
+    run = hg.run_ospr(ocfg(g["amp32"], 6, 42))
+    assert level_mismatches(run.set.levels, g["ospr32_levels"]).sum() <= 2
+    assert np.max(np.abs(np.array(run.set.per_frame_mse) - g["ospr32_frame_mse"]) / g["ospr32_frame_mse"]) < 1e-4
+    assert np.max(np.abs(run.report.trace.values() - g["ospr32_cum_mse"]) / g["ospr32_cum_mse"]) < 1e-4
+    assert np.allclose(run.set.mean_intensity, g["ospr32_mean_intensity"], rtol=1e-4, atol=1e-7)
+
+
+def test_config3_ospr_1024_binary_24_subframes(oracle):
+    amp = hg.patterns.bench_target(1024)
+    run = hg.run_ospr(ocfg(amp, 24, 1))
+    ref = oracle.ospr(amp, hg.SlmSpec.binary_phase(), 24, seed=1)
+    mism = level_mismatches(run.set.levels, ref.levels).sum()
+    assert mism <= 24, mism  # SURVEY §0.5 probe: 0 of 1,572,864 at 256^2
+    assert np.max(np.abs(np.array(run.set.per_frame_mse) - ref.frame_mse) / ref.frame_mse) < 1e-4
+    assert np.max(np.abs(run.report.trace.values() - ref.cumulative_mse) / ref.cumulative_mse) < 1e-4
+    assert rel(hg.subframe_mse_statistic(run.set.per_frame_mse), oracle.subframe_mse_statistic(ref.frame_mse)) < 1e-4
+
+
+def test_single_subframe_is_one_shot_pipeline():
+    # test_ospr.cpp:25-42: N=1 == quantise(ifft(seed(fork(0))))
+    amp = hg.patterns.bench_target(64)
+    run = hg.run_ospr(ocfg(amp, 1, 41))
+    f = hg.quantise_field(hg.fft_inverse(hg.seed_random_phase(amp, 41)), hg.SlmSpec.binary_phase())
+    assert np.array_equal(run.set.frames[0], f)
+    R = hg.fft_forward(f)
+    assert rel(run.set.per_frame_mse[0], hg.mse(amp, R)) < 1e-5
+
+
+def test_adaptive_matches_oracle_and_reductions(oracle):
+    amp = hg.patterns.bench_target(64)
+    plain = hg.run_ospr(ocfg(amp, 6, 42))
+    a0 = hg.run_adaptive_ospr(ocfg(amp, 6, 42, adaptive=True, gain=0.0))
+    assert np.array_equal(a0.set.levels, plain.set.levels)  # test_ospr.cpp:44-58
+    assert a0.report.algorithm == "adaptive_ospr" and plain.report.algorithm == "ospr"
+    a1 = hg.run_adaptive_ospr(ocfg(amp, 4, 43, adaptive=True, gain=1.0))
+    ref = oracle.ospr(amp, hg.SlmSpec.binary_phase(), 4, seed=43, adaptive=True, gain=1.0)
+    assert level_mismatches(a1.set.levels, ref.levels).sum() <= 8
+    assert np.max(np.abs(a1.report.trace.values() - ref.cumulative_mse) / ref.cumulative_mse) < 1e-3
+
+
+def test_batch_jobs_equal_single_runs():
+    amp = hg.patterns.bench_target(128)
+    runs = hg.run_ospr_batch(ocfg(amp, 5, 1), seeds=[1, 2, 3])
+    for j, s in enumerate([1, 2, 3]):
+        single = hg.run_ospr(ocfg(amp, 5, s))
+        assert np.array_equal(runs[j].set.levels, single.set.levels)
+        assert runs[j].report.final_error == single.report.final_error
+
+
+def test_traces_and_averaging():
+    amp = hg.patterns.bench_target(64)
+    run = hg.run_ospr(ocfg(amp, 16, 1))
+    tr = run.report.trace.values()
+    assert run.report.trace.name == "cumulative_mse" and len(tr) == 16
+    assert run.report.extra_traces[0].name == "frame_mse"
+    assert tr[-1] < 0.5 * tr[0]  # test_ospr.cpp:466-479
+    assert run.report.evaluations == 16
+    for fr in run.set.frames:
+        d = np.minimum(np.abs(fr - 1), np.abs(fr + 1))
+        assert np.max(d) < 1e-6
+
+
+def test_ospr_validation():
+    amp = hg.patterns.bench_target(16)
+    with pytest.raises(ValueError, match="subframes"):
+        hg.run_ospr(ocfg(amp, 0, 1))
+    with pytest.raises(ValueError, match="feedback_gain"):
+        hg.run_adaptive_ospr(ocfg(amp, 3, 1, adaptive=True, gain=1.5))
+    with pytest.raises(ValueError, match="variant mismatch"):
+        hg.run_adaptive_ospr(ocfg(amp, 3, 1))

@@ -353,6 +353,8 @@ static void build_quant(const hgc_slm* s, int nx, int ny, QuantDev& q) {
     p.margin_rad = 1e-5f;
     p.margin_u = (float)(1e-5 * inv + L * 4e-7 + 1e-6);
     p.states = q.states.p;
+    p.s0 = q.h_states[0];
+    p.s1 = q.h_states[L > 1 ? 1 : 0];
     if (s->illumination) {
         std::vector<double> arg(npix);
         q.h_illum.resize(npix);

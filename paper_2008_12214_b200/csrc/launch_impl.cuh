@@ -10,10 +10,10 @@ inline void set_smem(K kernel, int bytes) {
     if (bytes > 48 * 1024) CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
 }
 
-template <int NX, int MODE>
+template <int NX, int MODE, int QK>
 inline void row_launch(const RowArgs& a, int batch, cudaStream_t st, bool prepare) {
     using Cfg = RowCfg<NX>;
-    auto kern = k_row<NX, MODE>;
+    auto kern = k_row<NX, MODE, QK>;
     if (prepare) {
         set_smem(kern, Cfg::SMEM);
         return;
@@ -23,15 +23,42 @@ inline void row_launch(const RowArgs& a, int batch, cudaStream_t st, bool prepar
     CK(cudaGetLastError());
 }
 
-template <int MODE>
-inline void row_dispatch(int nx, const RowArgs& a, int batch, cudaStream_t st, bool prepare) {
+// Which specialised quantiser a fused row pass can use (quant.cuh).
+inline int quant_kind(const QuantParams& q) {
+    const bool illum = q.illum_arg || q.illum || q.illum_unit;
+    if (q.mode == 1 && !illum && !q.full_circle && q.levels == 2 && q.min_arg == 0.0 &&
+        q.range == 3.1415926535897932384626433832795)
+        return QK_BINARY;
+    if (q.mode == 1 && !illum && q.full_circle) return QK_FULL;
+    return QK_GENERIC;
+}
+
+template <int MODE, int QK>
+inline void row_dispatch_q(int nx, const RowArgs& a, int batch, cudaStream_t st, bool prepare) {
     switch (nx) {
 #define HG_ROW(N) \
-    case N: row_launch<N, MODE>(a, batch, st, prepare); break;
+    case N: row_launch<N, MODE, QK>(a, batch, st, prepare); break;
         HG_ROW(2) HG_ROW(4) HG_ROW(8) HG_ROW(16) HG_ROW(32) HG_ROW(64) HG_ROW(128) HG_ROW(256)
         HG_ROW(512) HG_ROW(1024) HG_ROW(2048) HG_ROW(4096)
 #undef HG_ROW
         default: fail(HGC_EUNSUPPORTED, "row length unsupported");
+    }
+}
+
+template <int MODE>
+inline void row_dispatch(int nx, const RowArgs& a, int batch, cudaStream_t st, bool prepare) {
+    if constexpr (MODE == ROW_PLAIN) {
+        row_dispatch_q<MODE, QK_GENERIC>(nx, a, batch, st, prepare);
+    } else if (prepare) {
+        row_dispatch_q<MODE, QK_GENERIC>(nx, a, batch, st, true);
+        row_dispatch_q<MODE, QK_BINARY>(nx, a, batch, st, true);
+        row_dispatch_q<MODE, QK_FULL>(nx, a, batch, st, true);
+    } else {
+        switch (quant_kind(a.q)) {
+            case QK_BINARY: row_dispatch_q<MODE, QK_BINARY>(nx, a, batch, st, false); break;
+            case QK_FULL: row_dispatch_q<MODE, QK_FULL>(nx, a, batch, st, false); break;
+            default: row_dispatch_q<MODE, QK_GENERIC>(nx, a, batch, st, false); break;
+        }
     }
 }
 

@@ -77,7 +77,7 @@ struct RowCfg {
     static constexpr int SMEM = (NX > E) ? RPC * PaddedLen<NX>::value * (int)sizeof(float2) : 0;
 };
 
-template <int NX, int MODE>
+template <int NX, int MODE, int QK>
 __global__ void __launch_bounds__(RowCfg<NX>::THREADS) k_row(RowArgs a) {
     using Cfg = RowCfg<NX>;
     constexpr int E = Cfg::E, T = Cfg::T;
@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(RowCfg<NX>::THREADS) k_row(RowArgs a) {
     const int y = blockIdx.x * Cfg::RPC + lr;
     const int b = blockIdx.y;
     RowSmemIdx idx{lr * PaddedLen<NX>::value};
-    const bool valid = y < a.ny;  // (ny is a multiple of RPC for supported sizes; guard anyway)
+    const bool valid = y < a.ny;  // (ny is a multiple of RPC except for tiny fields)
     float2* row = a.field + a.bstride * b + (size_t)(valid ? y : 0) * NX;
     float2 v[E];
 #pragma unroll
@@ -112,20 +112,22 @@ __global__ void __launch_bounds__(RowCfg<NX>::THREADS) k_row(RowArgs a) {
             for (int e = 0; e < E; ++e) v[e] = cmul_conj_rn(v[e], __ldg(&a.fresnel_q[rowbase + t + e * T]));
     } else {
         fft_line<NX, +1>(v, t, smem, idx, a.tw);  // completes the 2-D inverse (propagation.hpp:89-95)
-        const size_t rowbase = (size_t)y * NX;
+        const int rowbase = y * NX;
+        const float norm = a.norm;
+        const float2* __restrict__ fq = a.fresnel_q;
+        uint8_t* __restrict__ lv8 = a.levels8 ? a.levels8 + a.lv_bstride * b : nullptr;
+        uint16_t* __restrict__ lv16 = a.levels16 ? a.levels16 + a.lv_bstride * b : nullptr;
 #pragma unroll
         for (int e = 0; e < E; ++e) {
-            const int x = t + e * T;
-            const size_t i = rowbase + x;
-            float2 f = cscale(v[e], a.norm);  // fftw_backend.cpp:121-123
-            if (a.fresnel_q) f = cmul_conj_rn(f, __ldg(&a.fresnel_q[i]));  // propagation.hpp:93
-            int k = quant_decide(a.q, f.x, f.y, i);                       // quantise.hpp:211-215
-            f = quant_state(a.q, k, i);
-            if (valid) {
-                if (a.levels8) a.levels8[a.lv_bstride * b + i] = (uint8_t)k;
-                if (a.levels16) a.levels16[a.lv_bstride * b + i] = (uint16_t)k;
-            }
-            if (a.fresnel_q) f = cmul_rn(f, __ldg(&a.fresnel_q[i]));       // propagation.hpp:85
+            const int i = rowbase + t + e * T;
+            float2 f = cscale(v[e], norm);                        // fftw_backend.cpp:121-123
+            if (fq) f = cmul_conj_rn(f, __ldg(&fq[i]));           // propagation.hpp:93
+            const int k = quant_decide_kind<QK>(a.q, f.x, f.y, i);  // quantise.hpp:211-215
+            if constexpr (QK == QK_BINARY) f = k ? a.q.s1 : a.q.s0;
+            else f = quant_state(a.q, k, i);
+            if (lv8 && valid) lv8[i] = (uint8_t)k;
+            if (lv16 && valid) lv16[i] = (uint16_t)k;
+            if (fq) f = cmul_rn(f, __ldg(&fq[i]));                // propagation.hpp:85
             v[e] = f;
         }
         fft_line<NX, -1>(v, t, smem, idx, a.tw);  // starts the forward transform

@@ -31,6 +31,7 @@ struct QuantParams {
     float margin_rad; // decision margin in radians (phase mode)
     float margin_u;   // same margin in level units
     float pad2_;
+    float2 s0, s1;    // states 0 and 1 (binary fast path)
     const float2* states;      // [levels] (T)allowed_states, quantise.hpp:147-149
     const double* illum_arg;   // [npix] arg(illumination) or nullptr
     const float2* illum;       // [npix] (T)illumination (phase mode) or nullptr
@@ -40,7 +41,7 @@ struct QuantParams {
 // Exact reference sequence, quantise.hpp:175-198.  Out of line (scalar
 // arguments, no struct copy) so the ~1e-3 of pixels that need it do not
 // inflate every inlined copy of the fast path.
-__device__ __noinline__ int quant_decide_exact(int mode, int L, int full_circle, double min_arg, double inv_spac,
+static __device__ __noinline__ int quant_decide_exact(int mode, int L, int full_circle, double min_arg, double inv_spac,
                                                double range, double min_amp, double illum_arg, float vr, float vi) {
     if (mode == 1) {
         double ang = atan2((double)vi, (double)vr);
@@ -102,6 +103,60 @@ __device__ __forceinline__ int quant_decide(const QuantParams& q, float vr, floa
         k = quant_decide_exact(q.mode, L, q.full_circle, q.min_arg, q.inv_spac, q.range, q.min_amp,
                                q.illum_arg ? q.illum_arg[i] : 0.0, vr, vi);
     return k;
+}
+
+// ------------------------------------------------ specialised fast paths
+// Quantiser kinds resolved on the host (launch template parameter):
+//   QK_GENERIC  any SlmSpec (restricted ranges, amplitude, illumination)
+//   QK_BINARY   SlmSpec::binary_phase() without illumination: the decision
+//               is the sign of Re(f) (level 1 = pi state iff Re(f) < 0)
+//   QK_FULL     full-circle phase without illumination
+enum QuantKind { QK_GENERIC = 0, QK_BINARY = 1, QK_FULL = 2 };
+
+// atan2 in float without the library slow paths: odd degree-13 polynomial
+// on [0,1] (max error 3.5e-7 rad in float) + octant fix-ups; total error
+// < 2e-6 rad, far inside the 1e-5 rad decision margin.
+__device__ __forceinline__ float fast_atan2f(float y, float x) {
+    const float ax = fabsf(x), ay = fabsf(y);
+    const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
+    const float a = mn * __frcp_rn(mx);  // mx == 0 -> NaN; caller treats NaN as "near"
+    const float s = a * a;
+    float r = 0.0068426248975283f;
+    r = fmaf(r, s, -0.03372593810402613f);
+    r = fmaf(r, s, 0.07981120495604219f);
+    r = fmaf(r, s, -0.13247522771620535f);
+    r = fmaf(r, s, 0.19813213509066366f);
+    r = fmaf(r, s, -0.3331830289944654f);
+    r = fmaf(r, s, 0.999996634700673f);
+    r *= a;
+    r = ay > ax ? 1.5707963267948966f - r : r;
+    r = x < 0.f ? 3.1415926535897932f - r : r;
+    return copysignf(r, y);
+}
+
+template <int QK>
+__device__ __forceinline__ int quant_decide_kind(const QuantParams& q, float vr, float vi, size_t i) {
+    if constexpr (QK == QK_BINARY) {
+        // atan2 within 1e-5 rad of +-pi/2 (or f == 0): defer to the exact path
+        const bool near = !(fabsf(vr) > 1e-5f * fmaxf(fabsf(vr), fabsf(vi)));
+        int k = vr < 0.f ? 1 : 0;
+        if (near) k = quant_decide_exact(1, 2, 0, q.min_arg, q.inv_spac, q.range, 0.0, 0.0, vr, vi);
+        return k;
+    } else if constexpr (QK == QK_FULL) {
+        const float two_pi_f = 6.28318530717958648f;
+        float d = fast_atan2f(vi, vr) - q.min_arg_f;
+        d -= two_pi_f * floorf(d * (1.0f / two_pi_f));
+        const float u = d * q.inv_spac_f;
+        const float fu = floorf(u);
+        const float fr = u - fu;
+        const bool near = !(fabsf(fr - 0.5f) >= q.margin_u);  // NaN-safe
+        int k = (int)fu + (fr >= 0.5f ? 1 : 0);
+        k = k >= q.levels ? k - q.levels : k;
+        if (near) k = quant_decide_exact(1, q.levels, 1, q.min_arg, q.inv_spac, q.range, 0.0, 0.0, vr, vi);
+        return k;
+    } else {
+        return quant_decide(q, vr, vi, i);
+    }
 }
 
 // Quantiser::state_value, quantise.hpp:201-205

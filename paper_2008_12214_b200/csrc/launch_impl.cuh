@@ -1,5 +1,7 @@
 // launch_impl.cuh — size dispatch shared by the k_*.cu translation units.
 #pragma once
+#include <cstdlib>
+
 #include "errors.h"
 #include "launch.h"
 
@@ -65,6 +67,10 @@ inline void row_dispatch(int nx, const RowArgs& a, int batch, cudaStream_t st, b
 template <int NY>
 inline int col_width(int nx) {
     int c = ColCfg<NY>::C;
+    if (const char* ev = getenv("HG_COLW")) {  // tuning experiments only
+        int w = atoi(ev);
+        if (w >= 1 && w <= c && (w & (w - 1)) == 0) c = w;
+    }
     return c < nx ? c : nx;
 }
 

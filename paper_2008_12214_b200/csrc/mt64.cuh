@@ -54,12 +54,42 @@ __device__ __forceinline__ uint64_t mt_mix(uint64_t hi, uint64_t lo) {
 }
 
 // One twist by a single warp: nw <- twist(ow).  Same recurrence as the
-// in-place libstdc++ _M_gen_rand, written out-of-place.
-__device__ __forceinline__ void mt_twist_warp(const uint64_t* ow, uint64_t* nw, int lane) {
-    for (int i = lane; i < kMtN - kMtM; i += 32) nw[i] = ow[i + kMtM] ^ mt_mix(ow[i], ow[i + 1]);
+// in-place libstdc++ _M_gen_rand, written out-of-place: words i < 156 depend
+// only on the old block, words 156..311 on the old block and new words
+// i - 156 (and word 311 on new word 0).  All loads of a phase are issued
+// before any store so the smem latency is paid twice per twist, not per word.
+__device__ __forceinline__ void mt_twist_warp(const uint64_t* __restrict__ ow, uint64_t* __restrict__ nw, int lane) {
+    constexpr int H = kMtN - kMtM;  // 156
+    uint64_t a[5], b[5], c[5];
+#pragma unroll
+    for (int m = 0; m < 5; ++m) {
+        const int i = lane + 32 * m;
+        if (i < H) {
+            a[m] = ow[i];
+            b[m] = ow[i + 1];
+            c[m] = ow[i + kMtM];
+        }
+    }
+#pragma unroll
+    for (int m = 0; m < 5; ++m) {
+        const int i = lane + 32 * m;
+        if (i < H) nw[i] = c[m] ^ mt_mix(a[m], b[m]);
+    }
     __syncwarp();
-    for (int i = kMtN - kMtM + lane; i < kMtN - 1; i += 32) nw[i] = nw[i - (kMtN - kMtM)] ^ mt_mix(ow[i], ow[i + 1]);
-    if (lane == 0) nw[kMtN - 1] = nw[kMtM - 1] ^ mt_mix(ow[kMtN - 1], nw[0]);
+#pragma unroll
+    for (int m = 0; m < 5; ++m) {
+        const int i = H + lane + 32 * m;
+        if (i < kMtN) {
+            a[m] = ow[i];
+            b[m] = i + 1 < kMtN ? ow[i + 1] : nw[0];
+            c[m] = nw[i - H];
+        }
+    }
+#pragma unroll
+    for (int m = 0; m < 5; ++m) {
+        const int i = H + lane + 32 * m;
+        if (i < kMtN) nw[i] = c[m] ^ mt_mix(a[m], b[m]);
+    }
     __syncwarp();
 }
 

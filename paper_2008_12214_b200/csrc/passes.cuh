@@ -75,10 +75,11 @@ struct RowCfg {
     static constexpr int RPC = T >= 256 ? 1 : 256 / T;  // rows per CTA
     static constexpr int THREADS = T * RPC;
     static constexpr int SMEM = (NX > E) ? RPC * PaddedLen<NX>::value * (int)sizeof(float2) : 0;
+    static constexpr int MIN_BLOCKS = THREADS >= 256 ? 3 : 1;  // <= 85 registers: 24 warps / SM
 };
 
 template <int NX, int MODE, int QK>
-__global__ void __launch_bounds__(RowCfg<NX>::THREADS) k_row(RowArgs a) {
+__global__ void __launch_bounds__(RowCfg<NX>::THREADS, RowCfg<NX>::MIN_BLOCKS) k_row(RowArgs a) {
     using Cfg = RowCfg<NX>;
     constexpr int E = Cfg::E, T = Cfg::T;
     extern __shared__ float2 smem[];

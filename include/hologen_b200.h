@@ -115,6 +115,9 @@ typedef struct hgc_ifta_io {
     double* trace;              /* RunReport::trace     [batch][iterations] */
     double* final_error;        /* RunReport::final_error [batch] */
     double* seconds;            /* RunReport::seconds (whole call) */
+    const float* fresnel_q;     /* optional complex [ny][nx] quadratic phase Q to use instead of
+                                   computing it from hgc_fresnel (e.g. taken from an existing
+                                   Propagator<float>, propagation.hpp:97-103) */
 } hgc_ifta_io;
 
 /* hologen::OsprConfig (ospr.hpp:20-38).  variant: 0 Ospr, 1 AdaptiveOspr.

@@ -55,7 +55,8 @@ class HgcIftaIo(C.Structure):
     _fields_ = [("amplitude", C.c_void_p), ("phase", C.c_void_p), ("roi", C.c_void_p), ("seeds", C.c_void_p),
                 ("init_field", C.c_void_p), ("init_weights", C.c_void_p), ("hologram", C.c_void_p),
                 ("levels8", C.c_void_p), ("levels16", C.c_void_p), ("replay", C.c_void_p),
-                ("trace", C.c_void_p), ("final_error", C.c_void_p), ("seconds", C.c_void_p)]
+                ("trace", C.c_void_p), ("final_error", C.c_void_p), ("seconds", C.c_void_p),
+                ("fresnel_q", C.c_void_p)]
 
 
 class HgcOsprCfg(C.Structure):

@@ -658,7 +658,7 @@ int hgc_ifta_plan_create(hgc_ifta_plan** out, const hgc_ifta_cfg* cfg, const hgc
         p->mt.alloc(batch);
         p->seeds.alloc(batch);
         if (fresnel) {
-            p->Q.alloc(p->npix);
+            p->Q.ensure(p->npix);
             double scale = 3.1415926535897932384626433832795 / (fresnel->wavelength * fresnel->distance);
             k_fresnel_q<<<ew_grid(p->npix), 256>>>(nx, ny, scale, fresnel->pixel_pitch_x, fresnel->pixel_pitch_y, p->Q.p);
             CK(cudaGetLastError());
@@ -695,6 +695,11 @@ int hgc_ifta_plan_upload(hgc_ifta_plan* p, const hgc_ifta_io* io) {
             std::vector<float2> ones(tot, make_float2(1.f, 0.f));
             CK(cudaMemcpyAsync(p->tphase_cs.p, ones.data(), sizeof(float2) * tot, cudaMemcpyHostToDevice, p->stream));
             CK(cudaStreamSynchronize(p->stream));
+        }
+        if (io->fresnel_q) {  // caller-supplied Q (e.g. from a reference Propagator<float>)
+            p->Q.ensure(npix);
+            CK(cudaMemcpyAsync(p->Q.p, io->fresnel_q, sizeof(float2) * npix, cudaMemcpyHostToDevice, p->stream));
+            p->fresnel = true;
         }
         p->has_roi = io->roi != nullptr;
         p->bx0 = 0;
@@ -737,7 +742,8 @@ int hgc_ifta_plan_upload(hgc_ifta_plan* p, const hgc_ifta_io* io) {
         CK(cudaStreamSynchronize(p->stream));
         const uint64_t sig = (uint64_t)(uintptr_t)p->roi.p ^ ((uint64_t)(uintptr_t)p->phase_d.p << 1) ^
                              ((uint64_t)(uintptr_t)p->tphase_cs.p << 2) ^ ((uint64_t)(uintptr_t)p->init_field.p << 3) ^
-                             ((uint64_t)(uintptr_t)p->init_weights.p << 4) ^ ((uint64_t)p->has_roi << 60) ^
+                             ((uint64_t)(uintptr_t)p->init_weights.p << 4) ^ ((uint64_t)(uintptr_t)p->Q.p << 5) ^
+                             ((uint64_t)p->has_roi << 60) ^
                              ((uint64_t)p->has_phase << 61) ^ ((uint64_t)p->init_weights_given << 62) ^ p->M;
         if (p->graph && sig != p->graph_sig) {  // recorded structure changed: rebuild
             cudaGraphExecDestroy(p->graph);

@@ -1,0 +1,105 @@
+// dropin_test.cpp — the C++ drop-in (include/hologen_b200/dropin.hpp) used
+// exactly as a reference caller would: reference headers + explicit float
+// specialisations + libhologen_b200.so.  Built by __graft_entry__.build()
+// when /root/reference is present; run by tests/test_gpu_dropin.py.
+//
+// The reference's own loop (detail::run_ifta / run_ospr_impl) is run beside
+// the GPU path with default_fft_backend<float>() = the B200 FftBackend, so
+// both sides use the same transform and only the fused kernels differ.
+#include <cmath>
+#include <cstdio>
+#include <stdexcept>
+
+#include "hologen/ifta.hpp"
+#include "hologen/ospr.hpp"
+#include "hologen/patterns.hpp"
+#include "hologen_b200/dropin.hpp"
+
+namespace hologen {
+template <typename T>
+FftBackend<T>& default_fft_backend();
+template <>
+FftBackend<float>& default_fft_backend<float>() { return hologen_b200::fft_backend(); }
+}  // namespace hologen
+
+using namespace hologen;
+
+static int fails = 0;
+#define CHECK(c)                                                   \
+    do {                                                           \
+        if (!(c)) {                                                \
+            std::printf("CHECK failed line %d: %s\n", __LINE__, #c); \
+            ++fails;                                               \
+        }                                                          \
+    } while (0)
+
+static int level_mismatch(const SlmSpec& slm, const ComplexField<float>& a, const ComplexField<float>& b) {
+    Quantiser<float> q(slm, a.nx, a.ny);
+    int m = 0;
+    for (size_t i = 0; i < a.data.size(); ++i) m += q.decide(i, a.data[i]) != q.decide(i, b.data[i]);
+    return m;
+}
+
+int main() {
+    RealImage amp = patterns::smooth_blobs(128, 128);
+    normalize_image(amp, Normalization::UnitEnergy);
+
+    // GS binary, Fourier
+    IftaConfig cfg;
+    cfg.iterations = 20;
+    cfg.slm = SlmSpec::binary_phase();
+    cfg.target.amplitude = amp;
+    cfg.seed = 1;
+    auto gpu = run_gs<float>(cfg);                    // drop-in specialisation
+    auto ref = detail::run_ifta<float>(cfg, nullptr);  // the reference loop
+    int mm = level_mismatch(cfg.slm, gpu.hologram, ref.hologram);
+    double rel = std::abs(gpu.final_error - ref.final_error) / ref.final_error;
+    std::printf("gs binary 128^2: level mismatches %d, mse %.9g vs %.9g (rel %.2e)\n", mm, gpu.final_error,
+                ref.final_error, rel);
+    CHECK(mm <= 4 && rel < 1e-4 && gpu.trace.size() == 20 && gpu.algorithm == "gs");
+
+    // WGS 256-level with a Fresnel propagator (lock-step not needed at 3 iterations)
+    FresnelParams p{532e-9, 0.1, 8e-6, 8e-6};
+    auto prop = Propagator<float>::fresnel(128, 128, p);
+    IftaConfig w = cfg;
+    w.variant = IftaVariant::WeightedGS;
+    w.slm = SlmSpec::full_circle_phase(256);
+    w.iterations = 2;
+    auto gw = run_weighted_gs<float>(w, &prop);
+    auto rw = detail::run_ifta<float>(w, &prop);
+    rel = std::abs(gw.final_error - rw.final_error) / rw.final_error;
+    std::printf("wgs fresnel 256-level: mse %.9g vs %.9g (rel %.2e)\n", gw.final_error, rw.final_error, rel);
+    CHECK(rel < 1e-4 && gw.algorithm == "wgs");
+
+    // OSPR
+    OsprConfig o;
+    o.subframes = 6;
+    o.slm = SlmSpec::binary_phase();
+    o.target.amplitude = amp;
+    o.seed = 42;
+    auto go = run_ospr<float>(o);
+    auto ro = detail::run_ospr_impl<float>(o, nullptr);
+    int om = 0;
+    for (int k = 0; k < 6; ++k) om += level_mismatch(o.slm, go.set.frames[k], ro.set.frames[k]);
+    rel = std::abs(go.report.final_error - ro.report.final_error) / ro.report.final_error;
+    std::printf("ospr 6 frames: level mismatches %d, cumulative mse rel %.2e\n", om, rel);
+    CHECK(om <= 6 && rel < 1e-4 && go.report.algorithm == "ospr" && go.set.frames.size() == 6);
+
+    // errors keep the reference's exceptions and messages
+    IftaConfig bad = cfg;
+    bad.iterations = 0;
+    try {
+        (void)run_gs<float>(bad);
+        CHECK(false);
+    } catch (const std::invalid_argument& e) {
+        CHECK(std::string(e.what()) == "IftaConfig: iterations must be >= 1");
+    }
+    try {
+        (void)run_weighted_gs<float>(cfg);
+        CHECK(false);
+    } catch (const std::invalid_argument& e) {
+        CHECK(std::string(e.what()) == "run_weighted_gs: config variant mismatch");
+    }
+    std::printf(fails ? "DROPIN FAILED\n" : "DROPIN OK\n");
+    return fails ? 1 : 0;
+}

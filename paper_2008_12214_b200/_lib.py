@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhologen_b200.so")
+LIB_PATH = os.environ.get("HG_LIB") or os.path.join(_HERE, "libhologen_b200.so")  # HG_LIB: tuning builds
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "hologen_b200.h")
 
 if not os.path.exists(LIB_PATH):

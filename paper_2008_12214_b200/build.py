@@ -30,7 +30,13 @@ def _stale(obj: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, jobs: int | None = None) -> str:
+def build(verbose: bool = False, jobs: int | None = None, defines: list[str] | None = None,
+          out: str | None = None, objdir: str | None = None) -> str:
+    """defines/out/objdir: tuning variants (e.g. -DHG_ROWQ_MINB=1) built beside the default library."""
+    global OBJ, LIB
+    if out:
+        LIB, OBJ = out, objdir or out + ".obj"
+    extra = [f"-D{d}" for d in (defines or [])]
     os.makedirs(OBJ, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     headers = glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) + \
@@ -44,7 +50,7 @@ def build(verbose: bool = False, jobs: int | None = None) -> str:
 
     def compile_one(so):
         s, o = so
-        cmd = [NVCC, *FLAGS, "-c", s, "-o", o]
+        cmd = [NVCC, *FLAGS, *extra, "-c", s, "-o", o]
         r = subprocess.run(cmd, capture_output=True, text=True)
         with open(o + ".log", "w") as f:
             f.write(r.stdout + r.stderr)
@@ -68,5 +74,10 @@ def build(verbose: bool = False, jobs: int | None = None) -> str:
 
 
 if __name__ == "__main__":
-    build(verbose=True)
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("-D", action="append", default=[])
+    ap.add_argument("--out")
+    a = ap.parse_args()
+    build(verbose=True, defines=a.D, out=a.out)
     sys.exit(0)

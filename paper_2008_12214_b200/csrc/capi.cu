@@ -117,9 +117,12 @@ static void prepare_kernels(int nx, int ny) {
     RowArgs ra{};
     ColArgs ca{};
     ca.nx = nx;
+    ra.layout = LAY_QUAD;
     row_fused(nx, ra, 1, nullptr, true);
+    ra.layout = LAY_ROW;
     row_plain(nx, ra, 1, nullptr, true);
     col_plain(ny, ca, 1, nullptr, true);
+    ca.layout = LAY_QUAD;
     col_gs(ny, ca, 1, nullptr, true);
     col_ospr(ny, ca, 1, nullptr, true);
     CK(cudaFuncSetAttribute(k_seed_random_phase, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSeedSmem));
@@ -133,26 +136,74 @@ __global__ void k_d2f(const double* a, float* o, size_t n) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
         o[i] = (float)a[i];
 }
-// InitPhase::Flat, ifta.hpp:128-130
-__global__ void k_init_flat(const double* a, float2* f, size_t n) {
-    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-        f[i] = make_float2((float)a[i], 0.f);
+// Row-major (host order) <-> resident layouts (passes.cuh): one thread per
+// element of a batch of nx x ny images.
+struct Pix {
+    size_t b, i;  // batch index, row-major pixel index
+    int x, y;
+};
+__device__ __forceinline__ Pix pix_of(size_t g, int nx, size_t npix) {
+    Pix p;
+    p.b = g / npix;
+    p.i = g % npix;
+    p.y = (int)(p.i / nx);
+    p.x = (int)(p.i % nx);
+    return p;
 }
-// target-phase init, ifta.hpp:131-136 (tphase = 2*pi*turns, ifta.hpp:107-111)
-__global__ void k_init_target_phase(const double* a, const double* turns, float2* f, size_t n) {
-    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-        double ph = __dmul_rn(HG_TWO_PI, turns[i]);
-        double s, c;
-        sincos(ph, &s, &c);
-        f[i] = make_float2((float)__dmul_rn(a[i], c), (float)__dmul_rn(a[i], s));
+#define HG_GRID_LOOP(g, n) \
+    for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < (n); g += (size_t)gridDim.x * blockDim.x)
+
+template <class TI, class TO>
+__global__ void k_to_colpair(const TI* in, TO* out, int nx, int ny, size_t total) {
+    const size_t npix = (size_t)nx * ny;
+    HG_GRID_LOOP(g, total) {
+        Pix p = pix_of(g, nx, npix);
+        out[p.b * npix + colpair_index(p.x, p.y, ny)] = (TO)in[g];
     }
 }
-// (cos, sin) of the target phase for the no-phase-freedom constraint (ifta.hpp:215-219)
-__global__ void k_phase_cs(const double* turns, float2* cs, size_t n) {
-    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+__global__ void k_to_quad(const float2* in, float2* out, int nx, int ny, size_t total) {
+    const size_t npix = (size_t)nx * ny;
+    HG_GRID_LOOP(g, total) {
+        Pix p = pix_of(g, nx, npix);
+        out[p.b * npix + quad_index(p.x, p.y, nx)] = in[g];
+    }
+}
+__global__ void k_from_quad(const float2* in, float2* out, int nx, int ny, size_t total) {
+    const size_t npix = (size_t)nx * ny;
+    HG_GRID_LOOP(g, total) {
+        Pix p = pix_of(g, nx, npix);
+        out[g] = in[p.b * npix + quad_index(p.x, p.y, nx)];
+    }
+}
+// InitPhase::Flat, ifta.hpp:128-130 (quad output)
+__global__ void k_init_flat(const double* a, float2* f, int nx, int ny, size_t total) {
+    const size_t npix = (size_t)nx * ny;
+    HG_GRID_LOOP(g, total) {
+        Pix p = pix_of(g, nx, npix);
+        f[p.b * npix + quad_index(p.x, p.y, nx)] = make_float2((float)a[g], 0.f);
+    }
+}
+// target-phase init, ifta.hpp:131-136 (tphase = 2*pi*turns, ifta.hpp:107-111) (quad output)
+__global__ void k_init_target_phase(const double* a, const double* turns, float2* f, int nx, int ny, size_t total) {
+    const size_t npix = (size_t)nx * ny;
+    HG_GRID_LOOP(g, total) {
+        Pix p = pix_of(g, nx, npix);
+        double ph = __dmul_rn(HG_TWO_PI, turns[g]);
         double s, c;
-        sincos(__dmul_rn(HG_TWO_PI, turns[i]), &s, &c);
-        cs[i] = make_float2((float)c, (float)s);
+        sincos(ph, &s, &c);
+        f[p.b * npix + quad_index(p.x, p.y, nx)] =
+            make_float2((float)__dmul_rn(a[g], c), (float)__dmul_rn(a[g], s));
+    }
+}
+// (cos, sin) of the target phase for the no-phase-freedom constraint
+// (ifta.hpp:215-219), column-pair major
+__global__ void k_phase_cs(const double* turns, float2* cs, int nx, int ny, size_t total) {
+    const size_t npix = (size_t)nx * ny;
+    HG_GRID_LOOP(g, total) {
+        Pix p = pix_of(g, nx, npix);
+        double s, c;
+        sincos(__dmul_rn(HG_TWO_PI, turns[g]), &s, &c);
+        cs[p.b * npix + colpair_index(p.x, p.y, ny)] = make_float2((float)c, (float)s);
     }
 }
 // make_fresnel_phase<float>, propagation.hpp:36-54 (no FMA contraction)
@@ -419,10 +470,10 @@ struct hgc_ifta_plan {
     size_t M = 0;
     int tiles = 0;
     int bx0 = 0, by0 = 0, bw = 0, bh = 0;  // LT roi bounding box
-    DBuf<float2> field, Q, tphase_cs, init_field;
+    DBuf<float2> field, Q, tphase_cs, init_field, scratch;
     DBuf<float> target_f, weights, init_weights;
     DBuf<double> amp_d, phase_d, partials, trace;
-    DBuf<uint8_t> roi, lv8;
+    DBuf<uint8_t> roi, roi_rm, lv8;
     DBuf<uint16_t> lv16;
     DBuf<MtState> mt;
     DBuf<uint64_t> seeds;
@@ -445,6 +496,24 @@ struct hgc_ifta_plan {
 
     float norm() const { return (float)(1.0 / std::sqrt((double)nx * ny)); }
 
+    // Targets per launch: as many as keep ~70% of L2 for their working set,
+    // at least enough CTAs to fill the GPU twice.
+    int group_size() const {
+        if (const char* ev = getenv("HG_GROUP")) {  // tuning experiments
+            int g = atoi(ev);
+            if (g >= 1) return std::min(g, batch);
+        }
+        int dev = 0, l2 = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const double per = (double)npix * (8 + 4 + (cfg.variant == 1 ? 4 : 0));
+        int g = (int)std::floor(0.7 * l2 / per);
+        if (g < 1) return batch;  // one target overflows L2: no reuse to gain, keep the widest launches
+        const int min_g = std::max(1, (int)std::ceil(2.0 * sms / (double)tiles));
+        return std::min(std::max(g, min_g), batch);
+    }
+
     SeedArgs seed_args() const {
         SeedArgs sa{};
         sa.states = mt.p;
@@ -454,6 +523,9 @@ struct hgc_ifta_plan {
         sa.out = field.p;
         sa.out_stride = npix;
         sa.npix = npix;
+        sa.quad = 1;
+        sa.nx = nx;
+        sa.ny = ny;
         return sa;
     }
 
@@ -464,6 +536,7 @@ struct hgc_ifta_plan {
         ra.field = field.p;
         ra.bstride = npix;
         ra.ny = ny;
+        ra.layout = LAY_QUAD;
         ra.norm = norm();
         ra.fresnel_q = fresnel ? Q.p : nullptr;
         ra.q = q.p;
@@ -483,6 +556,7 @@ struct hgc_ifta_plan {
         cg.field = field.p;
         cg.bstride = npix;
         cg.nx = nx;
+        cg.layout = LAY_QUAD;
         cg.norm = norm();
         cg.target = target_f.p;
         cg.t_bstride = npix;
@@ -518,12 +592,13 @@ struct hgc_ifta_plan {
         const size_t tot = npix * batch;
         // ---- initial replay field R0
         if (cfg.init_phase == 3) {
-            CK(cudaMemcpyAsync(field.p, init_field.p, sizeof(float2) * tot, cudaMemcpyDeviceToDevice, st));
+            k_to_quad<<<ew_grid(tot), 256, 0, st>>>(init_field.p, field.p, nx, ny, tot);
+            ++launches;
         } else if (cfg.init_phase == 2) {
-            k_init_flat<<<ew_grid(tot), 256, 0, st>>>(amp_d.p, field.p, tot);
+            k_init_flat<<<ew_grid(tot), 256, 0, st>>>(amp_d.p, field.p, nx, ny, tot);
             ++launches;
         } else if (!random_init()) {
-            k_init_target_phase<<<ew_grid(tot), 256, 0, st>>>(amp_d.p, phase_d.p, field.p, tot);
+            k_init_target_phase<<<ew_grid(tot), 256, 0, st>>>(amp_d.p, phase_d.p, field.p, nx, ny, tot);
             ++launches;
         } else {
             k_seed_random_phase<<<batch, kSeedThreads, kSeedSmem, st>>>(seed_args());
@@ -531,9 +606,10 @@ struct hgc_ifta_plan {
         }
         CK(cudaGetLastError());
         if (cfg.variant == 1) {
-            if (init_weights_given)
-                CK(cudaMemcpyAsync(weights.p, init_weights.p, sizeof(float) * tot, cudaMemcpyDeviceToDevice, st));
-            else {
+            if (init_weights_given) {
+                k_to_colpair<float, float><<<ew_grid(tot), 256, 0, st>>>(init_weights.p, weights.p, nx, ny, tot);
+                ++launches;
+            } else {
                 k_fill_f<<<ew_grid(tot), 256, 0, st>>>(weights.p, tot, 1.0f);
                 ++launches;
             }
@@ -544,13 +620,32 @@ struct hgc_ifta_plan {
         ca.field = field.p;
         ca.bstride = npix;
         ca.nx = nx;
+        ca.layout = LAY_QUAD;
         ca.sign = +1;
         col_plain(ny, ca, batch, st);
         ++launches;
-        for (int k = 1; k <= cfg.iterations; ++k) {
-            row_fused(nx, row_args(k == cfg.iterations), batch, st);
-            col_gs(ny, col_args(k), batch, st);
-            launches += 2;
+        // Iterations run target-group by target-group: a group's field +
+        // target (+ weights) is sized to stay L2-resident across the two
+        // passes and successive iterations (126 MB L2 on B200).
+        const int G = group_size();
+        for (int g0 = 0; g0 < batch; g0 += G) {
+            const int gn = std::min(G, batch - g0);
+            for (int k = 1; k <= cfg.iterations; ++k) {
+                RowArgs ra = row_args(k == cfg.iterations);
+                ra.field += (size_t)g0 * npix;
+                if (ra.levels8) ra.levels8 += (size_t)g0 * npix;
+                if (ra.levels16) ra.levels16 += (size_t)g0 * npix;
+                row_fused(nx, ra, gn, st);
+                ColArgs cg = col_args(k);
+                cg.field += (size_t)g0 * npix;
+                cg.target += (size_t)g0 * npix;
+                if (cg.weights) cg.weights += (size_t)g0 * npix;
+                if (cg.tphase_cs) cg.tphase_cs += (size_t)g0 * npix;
+                cg.replay_out += (size_t)g0 * npix;
+                cg.partials += (size_t)g0 * tiles * 8;
+                col_gs(ny, cg, gn, st);
+                launches += 2;
+            }
         }
         k_finalize<<<batch, 32, 0, st>>>(partials.p, cfg.iterations, batch, tiles, (double)M, cfg.freedom_scale, 0,
                                          trace.p);
@@ -645,7 +740,7 @@ int hgc_ifta_plan_create(hgc_ifta_plan** out, const hgc_ifta_cfg* cfg, const hgc
         if (fresnel) p->fp = *fresnel;
         build_quant(slm, nx, ny, p->q);
         p->wide_levels = slm->levels > 256;
-        p->tiles = col_tiles(nx, ny);
+        p->tiles = col_tiles(nx, ny, LAY_QUAD);
         const size_t tot = p->npix * batch;
         p->field.alloc(tot);
         p->target_f.alloc(tot);
@@ -682,12 +777,12 @@ int hgc_ifta_plan_upload(hgc_ifta_plan* p, const hgc_ifta_io* io) {
             CK(cudaMemcpyAsync(p->phase_d.p, io->phase, sizeof(double) * tot, cudaMemcpyHostToDevice, p->stream));
         }
         p->M = validate_target_dev(p->amp_d.p, io->phase ? p->phase_d.p : nullptr, io->roi, npix, tot, p->stream);
-        k_d2f<<<ew_grid(tot), 256, 0, p->stream>>>(p->amp_d.p, p->target_f.p, tot);
+        k_to_colpair<double, float><<<ew_grid(tot), 256, 0, p->stream>>>(p->amp_d.p, p->target_f.p, p->nx, p->ny, tot);
         CK(cudaGetLastError());
         if (io->phase) {
             if (!p->cfg.freedom_phase) {
                 p->tphase_cs.ensure(tot);
-                k_phase_cs<<<ew_grid(tot), 256, 0, p->stream>>>(p->phase_d.p, p->tphase_cs.p, tot);
+                k_phase_cs<<<ew_grid(tot), 256, 0, p->stream>>>(p->phase_d.p, p->tphase_cs.p, p->nx, p->ny, tot);
             }
         } else if (!p->cfg.freedom_phase) {
             // no target phase: the constraint enforces phase 0 (ifta.hpp:216)
@@ -706,9 +801,13 @@ int hgc_ifta_plan_upload(hgc_ifta_plan* p, const hgc_ifta_io* io) {
         p->by0 = 0;
         p->bw = p->nx;
         p->bh = p->ny;
-        if (io->roi) {
+        if (io->roi) {  // column-pair major for the column pass
             p->roi.ensure(npix);
-            CK(cudaMemcpyAsync(p->roi.p, io->roi, npix, cudaMemcpyHostToDevice, p->stream));
+            p->roi_rm.ensure(npix);
+            CK(cudaMemcpyAsync(p->roi_rm.p, io->roi, npix, cudaMemcpyHostToDevice, p->stream));
+            k_to_colpair<uint8_t, uint8_t><<<ew_grid(npix), 256, 0, p->stream>>>(p->roi_rm.p, p->roi.p, p->nx, p->ny,
+                                                                               npix);
+            CK(cudaGetLastError());
             if (p->cfg.variant == 2) {  // roi bounding box, ifta.hpp:148-161
                 int bx0 = p->nx, by0 = p->ny, bx1 = -1, by1 = -1;
                 for (int y = 0; y < p->ny; ++y)
@@ -784,7 +883,13 @@ int hgc_ifta_plan_download(hgc_ifta_plan* p, hgc_ifta_io* io) {
         CK(cudaDeviceSynchronize());
         const size_t tot = p->npix * p->batch;
         const int K = p->cfg.iterations;
-        if (io->replay) CK(cudaMemcpy(io->replay, p->field.p, sizeof(float2) * tot, cudaMemcpyDeviceToHost));
+        if (io->replay) {  // resident quad layout -> row-major
+            p->scratch.ensure(tot);
+            k_from_quad<<<ew_grid(tot), 256, 0, p->stream>>>(p->field.p, p->scratch.p, p->nx, p->ny, tot);
+            CK(cudaGetLastError());
+            CK(cudaStreamSynchronize(p->stream));
+            CK(cudaMemcpy(io->replay, p->scratch.p, sizeof(float2) * tot, cudaMemcpyDeviceToHost));
+        }
         std::vector<double> tr;
         if (io->trace || io->final_error) {
             tr.resize((size_t)K * p->batch);
@@ -919,6 +1024,9 @@ struct hgc_ospr_plan {
         sa.out = field.p;
         sa.out_stride = npix;
         sa.npix = npix;
+        sa.quad = 1;
+        sa.nx = nx;
+        sa.ny = ny;
         if (cfg.variant == 1 && n > 1) {  // adaptive budget, ospr.hpp:106-116
             sa.S = S.p;
             sa.S_stride = npix;
@@ -933,6 +1041,7 @@ struct hgc_ospr_plan {
         ci.field = field.p;
         ci.bstride = npix;
         ci.nx = nx;
+        ci.layout = LAY_QUAD;
         ci.sign = +1;
         return ci;
     }
@@ -943,6 +1052,7 @@ struct hgc_ospr_plan {
         ra.field = field.p;
         ra.bstride = npix;
         ra.ny = ny;
+        ra.layout = LAY_QUAD;
         ra.norm = norm();
         ra.q = q.p;
         ra.levels8 = wide_levels ? nullptr : lv8.p + (size_t)(n - 1) * npix;
@@ -956,6 +1066,7 @@ struct hgc_ospr_plan {
         co.field = field.p;
         co.bstride = npix;
         co.nx = nx;
+        co.layout = LAY_QUAD;
         co.norm = norm();
         co.target = target_f.p;
         co.t_bstride = per_job ? npix : 0;
@@ -1019,7 +1130,7 @@ int hgc_ospr_plan_create(hgc_ospr_plan** out, const hgc_ospr_cfg* cfg, const hgc
         p->npix = (size_t)nx * ny;
         build_quant(slm, nx, ny, p->q);
         p->wide_levels = slm->levels > 256;
-        p->tiles = col_tiles(nx, ny);
+        p->tiles = col_tiles(nx, ny, LAY_QUAD);
         const size_t tot = p->npix * jobs;
         const size_t ttot = p->per_job ? tot : p->npix;
         p->field.alloc(tot);
@@ -1047,12 +1158,19 @@ int hgc_ospr_plan_upload(hgc_ospr_plan* p, const hgc_ospr_io* io) {
         if (!io->amplitude) invalid("TargetSpec: amplitude image is empty");
         CK(cudaMemcpyAsync(p->amp_d.p, io->amplitude, sizeof(double) * ttot, cudaMemcpyHostToDevice, p->stream));
         p->M = validate_target_dev(p->amp_d.p, nullptr, io->roi, p->npix, ttot, p->stream);
-        k_d2f<<<ew_grid(ttot), 256, 0, p->stream>>>(p->amp_d.p, p->target_f.p, ttot);
+        k_to_colpair<double, float><<<ew_grid(ttot), 256, 0, p->stream>>>(p->amp_d.p, p->target_f.p, p->nx, p->ny,
+                                                                          ttot);
         CK(cudaGetLastError());
         p->has_roi = io->roi != nullptr;
-        if (io->roi) {
+        if (io->roi) {  // column-pair major
             p->roi.ensure(p->npix);
-            CK(cudaMemcpyAsync(p->roi.p, io->roi, p->npix, cudaMemcpyHostToDevice, p->stream));
+            DBuf<uint8_t> rm;
+            rm.alloc(p->npix);
+            CK(cudaMemcpyAsync(rm.p, io->roi, p->npix, cudaMemcpyHostToDevice, p->stream));
+            k_to_colpair<uint8_t, uint8_t><<<ew_grid(p->npix), 256, 0, p->stream>>>(rm.p, p->roi.p, p->nx, p->ny,
+                                                                                  p->npix);
+            CK(cudaGetLastError());
+            CK(cudaStreamSynchronize(p->stream));
         }
         std::vector<uint64_t> es(p->jobs);
         for (int j = 0; j < p->jobs; ++j) es[j] = fork_seed(io->seeds ? io->seeds[j] : p->cfg.seed, 0);  // ospr.hpp:89
@@ -1111,8 +1229,10 @@ int hgc_ospr_plan_download(hgc_ospr_plan* p, hgc_ospr_io* io) {
         if (io->mean_intensity || io->replay) {  // ospr.hpp:149-156
             std::vector<float> S(tot);
             CK(cudaMemcpy(S.data(), p->S.p, sizeof(float) * tot, cudaMemcpyDeviceToHost));
-            for (size_t i = 0; i < tot; ++i) {
-                double m = (double)S[i] / N;
+            for (size_t i = 0; i < tot; ++i) {  // S is column-pair major per job
+                const size_t j = i / npix, pi = i % npix;
+                const int px = (int)(pi % p->nx), py = (int)(pi / p->nx);
+                double m = (double)S[j * npix + colpair_index(px, py, p->ny)] / N;
                 if (io->mean_intensity) io->mean_intensity[i] = m;
                 if (io->replay) {
                     io->replay[2 * i] = (float)std::sqrt(m);
@@ -1236,6 +1356,7 @@ int hgc_propagate(int nx, int ny, int sign, const hgc_fresnel* fresnel, int batc
         ra.field = f.p;
         ra.bstride = npix;
         ra.ny = ny;
+        ra.layout = LAY_ROW;
         ra.sign = sign;
         ra.norm = norm;
         ra.apply_norm = sign > 0;

@@ -50,6 +50,26 @@ __device__ __forceinline__ T* opaque(T* p) {
     return (T*)y;
 }
 
+// ------------------------------------------------------------------ layouts
+// LAY_ROW : row-major [y][x] (ComplexField order) — primitives, host I/O.
+// LAY_QUAD: the plans' resident layout.  32-byte quads of 2 rows x 2 columns,
+//   quad (y/2, x/2) at ((y/2)*(nx/2) + x/2)*4, inside it (y&1)*2 + (x&1).
+//   A row pair is one contiguous block (row pass: 2 rows per CTA) and a
+//   column pair reads whole 32 B sectors (column pass: 2 columns per CTA),
+//   so both passes move full sectors with 64 KiB tiles (2 CTAs / SM).
+// Per-pixel side arrays of the column pass (target, weights, OSPR sum, ROI)
+// are column-pair major in LAY_QUAD: ((x/2)*ny + y)*2 + (x&1).
+namespace hg {
+enum Layout { LAY_ROW = 0, LAY_QUAD = 1 };
+
+__host__ __device__ __forceinline__ size_t quad_index(int x, int y, int nx) {
+    return (((size_t)(y >> 1) * (nx >> 1) + (x >> 1)) << 2) + ((y & 1) << 1) + (x & 1);
+}
+__host__ __device__ __forceinline__ size_t colpair_index(int x, int y, int ny) {
+    return (((size_t)(x >> 1) * ny + y) << 1) + (x & 1);
+}
+}  // namespace hg
+
 template <int V>
 struct IntC {
     static constexpr int value = V;

@@ -1,8 +1,15 @@
-// k_col_gs.cu — fused replay-plane pass of the IFTA loop.
+// k_col_gs.cu — fused replay-plane pass of the IFTA loop (fast GS / WGS
+// specialisations; the generic constraint lives in k_col_gsg.cu).
 #include "launch_impl.cuh"
 
 namespace hg {
-void col_gs(int ny, const ColArgs& a, int batch, cudaStream_t st, bool prepare) {
-    col_dispatch<COL_GS>(ny, a, batch, st, prepare);
+void col_gs_fast(int ny, const ColArgs& a, int batch, cudaStream_t st, bool prepare) {
+    if (prepare) {
+        col_dispatch<COL_GS_FAST, LAY_QUAD>(ny, a, batch, st, true);
+        col_dispatch<COL_WGS_FAST, LAY_QUAD>(ny, a, batch, st, true);
+        return;
+    }
+    if (a.weights) col_dispatch<COL_WGS_FAST, LAY_QUAD>(ny, a, batch, st, false);
+    else col_dispatch<COL_GS_FAST, LAY_QUAD>(ny, a, batch, st, false);
 }
 }  // namespace hg

@@ -4,6 +4,7 @@
 
 namespace hg {
 void col_ospr(int ny, const ColArgs& a, int batch, cudaStream_t st, bool prepare) {
-    col_dispatch<COL_OSPR>(ny, a, batch, st, prepare);
+    require_layout(a.layout, LAY_QUAD, "col_ospr");
+    col_dispatch<COL_OSPR, LAY_QUAD>(ny, a, batch, st, prepare);
 }
 }  // namespace hg

@@ -1,12 +1,25 @@
-// k_row.cu — instantiations of the row pass (fused aperture-plane pass and
-// the plain row transform of the FftBackend primitive).
+// k_row.cu — instantiations of the row pass: the fused aperture-plane pass
+// (quad layout, three quantiser kinds) and the plain row transform of the
+// FftBackend / Propagator primitives (row-major).
 #include "launch_impl.cuh"
 
 namespace hg {
 void row_fused(int nx, const RowArgs& a, int batch, cudaStream_t st, bool prepare) {
-    row_dispatch<ROW_FUSED>(nx, a, batch, st, prepare);
+    require_layout(a.layout, LAY_QUAD, "row_fused");
+    if (prepare) {
+        row_dispatch_q<ROW_FUSED, QK_GENERIC, LAY_QUAD>(nx, a, batch, st, true);
+        row_dispatch_q<ROW_FUSED, QK_BINARY, LAY_QUAD>(nx, a, batch, st, true);
+        row_dispatch_q<ROW_FUSED, QK_FULL, LAY_QUAD>(nx, a, batch, st, true);
+        return;
+    }
+    switch (quant_kind(a.q)) {
+        case QK_BINARY: row_dispatch_q<ROW_FUSED, QK_BINARY, LAY_QUAD>(nx, a, batch, st, false); break;
+        case QK_FULL: row_dispatch_q<ROW_FUSED, QK_FULL, LAY_QUAD>(nx, a, batch, st, false); break;
+        default: row_dispatch_q<ROW_FUSED, QK_GENERIC, LAY_QUAD>(nx, a, batch, st, false); break;
+    }
 }
 void row_plain(int nx, const RowArgs& a, int batch, cudaStream_t st, bool prepare) {
-    row_dispatch<ROW_PLAIN>(nx, a, batch, st, prepare);
+    require_layout(a.layout, LAY_ROW, "row_plain");
+    row_dispatch_q<ROW_PLAIN, QK_GENERIC, LAY_ROW>(nx, a, batch, st, prepare);
 }
 }  // namespace hg

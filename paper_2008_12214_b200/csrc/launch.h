@@ -9,12 +9,14 @@ namespace hg {
 
 // prepare = true only sets the kernel attributes (dynamic shared memory);
 // call it outside stream capture before the first launch of a size.
+// The layout comes from args.layout: fused passes exist for LAY_QUAD (plans),
+// plain transforms for both layouts.
 void row_fused(int nx, const RowArgs& a, int batch, cudaStream_t st, bool prepare = false);
 void row_plain(int nx, const RowArgs& a, int batch, cudaStream_t st, bool prepare = false);
 void col_plain(int ny, const ColArgs& a, int batch, cudaStream_t st, bool prepare = false);
 void col_gs(int ny, const ColArgs& a, int batch, cudaStream_t st, bool prepare = false);
 void col_ospr(int ny, const ColArgs& a, int batch, cudaStream_t st, bool prepare = false);
 // Column tiles (CTAs) per target of the column pass for an nx x ny field.
-int col_tiles(int nx, int ny);
+int col_tiles(int nx, int ny, int layout);
 
 }  // namespace hg

@@ -1,4 +1,4 @@
-// launch_impl.cuh — size dispatch shared by the k_*.cu translation units.
+// launch_impl.cuh — size/layout dispatch shared by the k_*.cu translation units.
 #pragma once
 #include <cstdlib>
 
@@ -12,10 +12,11 @@ inline void set_smem(K kernel, int bytes) {
     if (bytes > 48 * 1024) CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
 }
 
-template <int NX, int MODE, int QK>
+// ------------------------------------------------------------------- rows
+template <int NX, int MODE, int QK, int LAY>
 inline void row_launch(const RowArgs& a, int batch, cudaStream_t st, bool prepare) {
-    using Cfg = RowCfg<NX>;
-    auto kern = k_row<NX, MODE, QK>;
+    using Cfg = RowCfg<NX, LAY>;
+    auto kern = k_row<NX, MODE, QK, LAY>;
     if (prepare) {
         set_smem(kern, Cfg::SMEM);
         return;
@@ -35,11 +36,11 @@ inline int quant_kind(const QuantParams& q) {
     return QK_GENERIC;
 }
 
-template <int MODE, int QK>
+template <int MODE, int QK, int LAY>
 inline void row_dispatch_q(int nx, const RowArgs& a, int batch, cudaStream_t st, bool prepare) {
     switch (nx) {
 #define HG_ROW(N) \
-    case N: row_launch<N, MODE, QK>(a, batch, st, prepare); break;
+    case N: row_launch<N, MODE, QK, LAY>(a, batch, st, prepare); break;
         HG_ROW(2) HG_ROW(4) HG_ROW(8) HG_ROW(16) HG_ROW(32) HG_ROW(64) HG_ROW(128) HG_ROW(256)
         HG_ROW(512) HG_ROW(1024) HG_ROW(2048) HG_ROW(4096)
 #undef HG_ROW
@@ -47,36 +48,16 @@ inline void row_dispatch_q(int nx, const RowArgs& a, int batch, cudaStream_t st,
     }
 }
 
-template <int MODE>
-inline void row_dispatch(int nx, const RowArgs& a, int batch, cudaStream_t st, bool prepare) {
-    if constexpr (MODE == ROW_PLAIN) {
-        row_dispatch_q<MODE, QK_GENERIC>(nx, a, batch, st, prepare);
-    } else if (prepare) {
-        row_dispatch_q<MODE, QK_GENERIC>(nx, a, batch, st, true);
-        row_dispatch_q<MODE, QK_BINARY>(nx, a, batch, st, true);
-        row_dispatch_q<MODE, QK_FULL>(nx, a, batch, st, true);
-    } else {
-        switch (quant_kind(a.q)) {
-            case QK_BINARY: row_dispatch_q<MODE, QK_BINARY>(nx, a, batch, st, false); break;
-            case QK_FULL: row_dispatch_q<MODE, QK_FULL>(nx, a, batch, st, false); break;
-            default: row_dispatch_q<MODE, QK_GENERIC>(nx, a, batch, st, false); break;
-        }
-    }
-}
-
-template <int NY>
+// ---------------------------------------------------------------- columns
+template <int NY, int LAY>
 inline int col_width(int nx) {
-    int c = ColCfg<NY>::C;
-    if (const char* ev = getenv("HG_COLW")) {  // tuning experiments only
-        int w = atoi(ev);
-        if (w >= 1 && w <= c && (w & (w - 1)) == 0) c = w;
-    }
+    int c = ColCfg<NY, LAY>::C;
     return c < nx ? c : nx;
 }
 
-template <int NY, int C, int MODE>
+template <int NY, int C, int MODE, int LAY>
 inline void col_launch_c(const ColArgs& a, int batch, cudaStream_t st, bool prepare) {
-    auto kern = k_col<NY, C, MODE>;
+    auto kern = k_col<NY, C, MODE, LAY>;
     constexpr int smem = (NY > LineCfg<NY>::E) ? PaddedLen<NY>::value * C * (int)sizeof(float2) : 0;
     if (prepare) {
         set_smem(kern, smem);
@@ -87,28 +68,46 @@ inline void col_launch_c(const ColArgs& a, int batch, cudaStream_t st, bool prep
     CK(cudaGetLastError());
 }
 
-template <int NY, int MODE>
+template <int NY, int MODE, int LAY>
 inline void col_launch(const ColArgs& a, int batch, cudaStream_t st, bool prepare) {
-    switch (col_width<NY>(a.nx)) {
-        case 1: if constexpr (ColCfg<NY>::C >= 1) col_launch_c<NY, 1, MODE>(a, batch, st, prepare); break;
-        case 2: if constexpr (ColCfg<NY>::C >= 2) col_launch_c<NY, 2, MODE>(a, batch, st, prepare); break;
-        case 4: if constexpr (ColCfg<NY>::C >= 4) col_launch_c<NY, 4, MODE>(a, batch, st, prepare); break;
-        case 8: if constexpr (ColCfg<NY>::C >= 8) col_launch_c<NY, 8, MODE>(a, batch, st, prepare); break;
-        case 16: if constexpr (ColCfg<NY>::C >= 16) col_launch_c<NY, 16, MODE>(a, batch, st, prepare); break;
+    constexpr int CM = ColCfg<NY, LAY>::C;
+    switch (col_width<NY, LAY>(a.nx)) {
+        case 1: if constexpr (CM >= 1 && LAY == LAY_ROW) col_launch_c<NY, 1, MODE, LAY>(a, batch, st, prepare); break;
+        case 2: if constexpr (CM >= 2) col_launch_c<NY, 2, MODE, LAY>(a, batch, st, prepare); break;
+        case 4: if constexpr (CM >= 4) col_launch_c<NY, 4, MODE, LAY>(a, batch, st, prepare); break;
+        case 8: if constexpr (CM >= 8) col_launch_c<NY, 8, MODE, LAY>(a, batch, st, prepare); break;
+        case 16: if constexpr (CM >= 16) col_launch_c<NY, 16, MODE, LAY>(a, batch, st, prepare); break;
         default: fail(HGC_EUNSUPPORTED, "column tile unsupported");
     }
 }
 
-template <int MODE>
+template <int MODE, int LAY>
 inline void col_dispatch(int ny, const ColArgs& a, int batch, cudaStream_t st, bool prepare) {
     switch (ny) {
 #define HG_COL(N) \
-    case N: col_launch<N, MODE>(a, batch, st, prepare); break;
+    case N: col_launch<N, MODE, LAY>(a, batch, st, prepare); break;
         HG_COL(2) HG_COL(4) HG_COL(8) HG_COL(16) HG_COL(32) HG_COL(64) HG_COL(128) HG_COL(256)
         HG_COL(512) HG_COL(1024) HG_COL(2048) HG_COL(4096)
 #undef HG_COL
         default: fail(HGC_EUNSUPPORTED, "column length unsupported");
     }
+}
+
+template <int LAY>
+inline int col_tiles_lay(int nx, int ny) {
+    int c = 1;
+    switch (ny) {
+#define HG_CT(N) \
+    case N: c = col_width<N, LAY>(nx); break;
+        HG_CT(2) HG_CT(4) HG_CT(8) HG_CT(16) HG_CT(32) HG_CT(64) HG_CT(128) HG_CT(256)
+        HG_CT(512) HG_CT(1024) HG_CT(2048) HG_CT(4096)
+#undef HG_CT
+    }
+    return nx / c;
+}
+
+inline void require_layout(int got, int want, const char* what) {
+    if (got != want) fail(HGC_EUNSUPPORTED, std::string(what) + ": layout not instantiated");
 }
 
 }  // namespace hg

@@ -112,6 +112,9 @@ struct SeedArgs {
     size_t S_stride;
     int n;
     double gain;
+    // output layout: quad != 0 writes the plans' LAY_QUAD field (and reads S
+    // column-pair major); otherwise row-major.  nx, ny used when quad != 0.
+    int quad, nx, ny;
 };
 
 // One CTA per stream.  Warp 0 produces twists; warps 1.. consume.
@@ -182,16 +185,22 @@ __global__ void __launch_bounds__(kSeedThreads) k_seed_random_phase(SeedArgs a) 
                 double sn, cs;
                 sincos(theta, &sn, &cs);
                 double av = amp[d0 + j];
+                const size_t p = d0 + j;  // row-major pixel index of this draw (rng.hpp:60)
+                size_t o = p, so = p;
+                if (a.quad) {
+                    const int py = (int)(p / (size_t)a.nx), px = (int)(p % (size_t)a.nx);
+                    o = quad_index(px, py, a.nx);
+                    so = colpair_index(px, py, a.ny);
+                }
                 if (a.S) {
                     const double tv = av, t2 = __dmul_rn(tv, tv);
-                    const double sv = (double)a.S[a.S_stride * s + d0 + j];
+                    const double sv = (double)a.S[a.S_stride * s + so];
                     const double n = a.n;
                     double budget = __dsub_rn(__dmul_rn(n, t2), __dmul_rn(n - 1.0, __ddiv_rn(sv, n - 1.0)));
                     double tn = __dsqrt_rn(budget > 0.0 ? budget : 0.0);
                     av = __dadd_rn(__dmul_rn(1.0 - a.gain, tv), __dmul_rn(a.gain, tn));
                 }
-                out[d0 + j] = make_float2(__double2float_rn(__dmul_rn(av, cs)),
-                                          __double2float_rn(__dmul_rn(av, sn)));
+                out[o] = make_float2(__double2float_rn(__dmul_rn(av, cs)), __double2float_rn(__dmul_rn(av, sn)));
             }
         }
         __syncthreads();

@@ -20,6 +20,13 @@
 #include "fft.cuh"
 #include "quant.cuh"
 
+#ifndef HG_ROWQ_MINB  // resident CTAs / SM asked of the quad-layout row pass (register cap)
+#define HG_ROWQ_MINB 2
+#endif
+#ifndef HG_COLQ_MINB
+#define HG_COLQ_MINB 2
+#endif
+
 namespace hg {
 
 // --------------------------------------------------------------- reductions
@@ -59,39 +66,75 @@ struct RowArgs {
     float2* field;
     size_t bstride;   // elements per target
     int ny;
+    int layout;       // Layout (dispatch)
     float norm;       // (float)(1/sqrt(nx*ny)) applied after the row IFFT (fused) / the row FFT (plain, if apply_norm)
     int sign;         // ROW_PLAIN: -1 forward, +1 inverse
     int apply_norm;   // ROW_PLAIN
-    const float2* fresnel_q;  // [ny][nx] or nullptr
+    const float2* fresnel_q;  // [ny][nx] row-major or nullptr
     QuantParams q;
-    uint8_t* levels8;         // [target][ny][nx] or nullptr
+    uint8_t* levels8;         // [target][ny][nx] row-major or nullptr
     uint16_t* levels16;
     size_t lv_bstride;
 };
 
-template <int NX>
-struct RowCfg {
-    static constexpr int E = LineCfg<NX>::E, T = LineCfg<NX>::T;
-    static constexpr int RPC = T >= 256 ? 1 : 256 / T;  // rows per CTA
-    static constexpr int THREADS = T * RPC;
-    static constexpr int SMEM = (NX > E) ? RPC * PaddedLen<NX>::value * (int)sizeof(float2) : 0;
-    static constexpr int MIN_BLOCKS = THREADS >= 256 ? 3 : 1;  // <= 85 registers: 24 warps / SM
+template <int N>
+struct RowStride {  // padded smem row; == 8 (mod 16) so a row pair sits 16 banks apart
+    static constexpr int p = PaddedLen<N>::value;
+    static constexpr int value = p + ((8 - p % 16) + 16) % 16;
 };
 
-template <int NX, int MODE, int QK>
-__global__ void __launch_bounds__(RowCfg<NX>::THREADS, RowCfg<NX>::MIN_BLOCKS) k_row(RowArgs a) {
-    using Cfg = RowCfg<NX>;
+template <int NX, int LAY>
+struct RowCfg {
+    static constexpr int E = LineCfg<NX>::E, T = LineCfg<NX>::T;
+    static constexpr int RPC = LAY == LAY_QUAD ? (512 / T < 2 ? 2 : 512 / T) : (T >= 256 ? 1 : 256 / T);
+    static constexpr int THREADS = T * RPC;
+    static constexpr int SMEM = (NX > E) ? RPC * RowStride<NX>::value * (int)sizeof(float2) : 0;
+    static constexpr int MIN_BLOCKS = LAY == LAY_QUAD ? (THREADS >= 512 ? HG_ROWQ_MINB : 1) : (THREADS >= 256 ? 3 : 1);
+};
+
+template <int NX, int MODE, int QK, int LAY>
+__global__ void __launch_bounds__(RowCfg<NX, LAY>::THREADS, RowCfg<NX, LAY>::MIN_BLOCKS) k_row(RowArgs a) {
+    using Cfg = RowCfg<NX, LAY>;
     constexpr int E = Cfg::E, T = Cfg::T;
     extern __shared__ float2 smem[];
-    const int lr = threadIdx.x / T, t = threadIdx.x % T;
+    int lr, t;
+    if constexpr (LAY == LAY_QUAD) {
+        // the 2T threads of a row pair interleave so a warp covers 2 rows x 16
+        // consecutive x = 8 whole quads (256 contiguous bytes)
+        const int pr = threadIdx.x / (2 * T), q = threadIdx.x % (2 * T);
+        int r;
+        if constexpr (T >= 2) {
+            r = (q >> 1) & 1;
+            t = ((q >> 2) << 1) | (q & 1);
+        } else {
+            r = q & 1;
+            t = 0;
+        }
+        lr = 2 * pr + r;
+    } else {
+        lr = threadIdx.x / T;
+        t = threadIdx.x % T;
+    }
     const int y = blockIdx.x * Cfg::RPC + lr;
     const int b = blockIdx.y;
-    RowSmemIdx idx{lr * PaddedLen<NX>::value};
+    RowSmemIdx idx{lr * RowStride<NX>::value};
     const bool valid = y < a.ny;  // (ny is a multiple of RPC except for tiny fields)
-    float2* row = a.field + a.bstride * b + (size_t)(valid ? y : 0) * NX;
+    const int yy = valid ? y : 0;
+    float2* fb = a.field + a.bstride * b;
+    // element e of this thread sits at x = t + e*T
+    auto addr = [&](int e) -> size_t {
+        if constexpr (LAY == LAY_QUAD) {
+            if constexpr (T >= 2)
+                return quad_index(t, yy, NX) + (size_t)e * (2 * T);  // x>>1 advances by T/2 quads
+            else
+                return quad_index(t + e * T, yy, NX);
+        } else {
+            return (size_t)yy * NX + t + e * T;
+        }
+    };
     float2 v[E];
 #pragma unroll
-    for (int e = 0; e < E; ++e) v[e] = row[t + e * T];
+    for (int e = 0; e < E; ++e) v[e] = fb[addr(e)];
 
     if constexpr (MODE == ROW_PLAIN) {
         // Propagator<float>::forward / inverse halves (propagation.hpp:81-95):
@@ -120,7 +163,7 @@ __global__ void __launch_bounds__(RowCfg<NX>::THREADS, RowCfg<NX>::MIN_BLOCKS) k
         uint16_t* __restrict__ lv16 = a.levels16 ? a.levels16 + a.lv_bstride * b : nullptr;
 #pragma unroll
         for (int e = 0; e < E; ++e) {
-            const int i = rowbase + t + e * T;
+            const int i = rowbase + t + e * T;  // row-major pixel index (levels, Q, illumination)
             float2 f = cscale(v[e], norm);                        // fftw_backend.cpp:121-123
             if (fq) f = cmul_conj_rn(f, __ldg(&fq[i]));           // propagation.hpp:93
             const int k = quant_decide_kind<QK>(a.q, f.x, f.y, i);  // quantise.hpp:211-215
@@ -133,19 +176,24 @@ __global__ void __launch_bounds__(RowCfg<NX>::THREADS, RowCfg<NX>::MIN_BLOCKS) k
         }
         fft_line<NX, -1>(v, t, smem, idx, a.tw);  // starts the forward transform
     }
-    if (valid)
+    if (valid) {
+        float2* ob = opaque(fb);
 #pragma unroll
-        for (int e = 0; e < E; ++e) row[t + e * T] = v[e];
+        for (int e = 0; e < E; ++e) ob[addr(e)] = v[e];
+    }
 }
 
 // ------------------------------------------------------------- column pass
-enum ColMode { COL_PLAIN = 0, COL_GS = 1, COL_OSPR = 2 };
+// COL_GS_FAST / COL_WGS_FAST: no ROI, no LT schedule, phase freedom (the
+// benchmark configurations); COL_GS_GENERIC: every TargetSpec / variant.
+enum ColMode { COL_PLAIN = 0, COL_GS_GENERIC = 1, COL_OSPR = 2, COL_GS_FAST = 3, COL_WGS_FAST = 4 };
 
 struct ColArgs {
     const float2* tw;
     float2* field;
     size_t bstride;
     int nx;
+    int layout;      // Layout (dispatch)
     float norm;
     int sign;        // COL_PLAIN
     int apply_norm;  // COL_PLAIN
@@ -167,17 +215,45 @@ struct ColArgs {
     float inv_n;          // 1/n for the cumulative replay sqrt(S/n)
 };
 
-template <int NY>
+template <int NY, int LAY>
 struct ColCfg {
     static constexpr int E = LineCfg<NY>::E, T = LineCfg<NY>::T;
-    static constexpr int CMAX = (16384 / NY) < 16 ? (16384 / NY) : 16;  // 128 KiB of complex64 per CTA
-    static constexpr int C = CMAX < 1 ? 1 : CMAX;
+    // LAY_ROW: up to 128 KiB of complex64 per CTA (1 CTA / SM at 4096);
+    // LAY_QUAD: 64 KiB column-pair tiles (2 CTAs / SM)
+    static constexpr int BUDGET = LAY == LAY_QUAD ? 8192 : 16384;
+    static constexpr int CMAX0 = (BUDGET / NY) < 16 ? (BUDGET / NY) : 16;
+    static constexpr int CMIN = LAY == LAY_QUAD ? 2 : 1;
+    static constexpr int C = CMAX0 < CMIN ? CMIN : CMAX0;
     static constexpr int THREADS = T * C;
-    static constexpr int SMEM = (NY > E) ? PaddedLen<NY>::value * C * (int)sizeof(float2) : 0;
+    static constexpr int MIN_BLOCKS = (LAY == LAY_QUAD && THREADS >= 512) ? HG_COLQ_MINB : 1;
 };
 
-template <int NY, int C, int MODE>
-__global__ void __launch_bounds__(LineCfg<NY>::T * C) k_col(ColArgs a) {
+// Per-thread float partials -> warp sums in float (32 terms) -> per-warp
+// doubles -> fixed-order double block sum; thread 0 stores NV doubles.
+template <int NV>
+__device__ __forceinline__ void block_sum_float_store(float (&v)[NV], double* out) {
+    __shared__ double red[32][NV];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+    if (lane == 0)
+#pragma unroll
+        for (int i = 0; i < NV; ++i) red[warp][i] = (double)v[i];
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            double x = lane < nw ? red[lane][i] : 0.0;
+            x = warp_sum(x);
+            if (lane == 0) out[i] = x;
+        }
+    }
+}
+
+template <int NY, int C, int MODE, int LAY>
+__global__ void __launch_bounds__(LineCfg<NY>::T * C, ColCfg<NY, LAY>::MIN_BLOCKS) k_col(ColArgs a) {
     constexpr int E = LineCfg<NY>::E, T = LineCfg<NY>::T;
     extern __shared__ float2 smem[];
     const int c = threadIdx.x % C, t = threadIdx.x / C;
@@ -185,21 +261,38 @@ __global__ void __launch_bounds__(LineCfg<NY>::T * C) k_col(ColArgs a) {
     const int b = blockIdx.y;
     const int nx = a.nx;
     ColSmemIdx<C> idx{c};
-    float2* base = a.field + a.bstride * b + x;
-    float2 v[E];
-    {
-        const float2* p0 = base + t * nx;
-        const int st = T * nx;
-#pragma unroll
-        for (int e = 0; e < E; ++e) v[e] = p0[e * st];
+    // element e of this thread is row y = t + e*T.  Field offsets: per-thread
+    // base + e*st (both layouts advance by T*nx elements per e when T is even);
+    // side arrays (target, weights, S, roi): base sb + e*ss.
+    size_t f0;
+    int st;
+    size_t sb;
+    int ss;
+    if constexpr (LAY == LAY_QUAD) {
+        f0 = quad_index(x, t, nx);
+        st = (T >= 2) ? T * nx : 0;
+        sb = colpair_index(x, t, NY);
+        ss = 2 * T;
+    } else {
+        f0 = (size_t)t * nx + x;
+        st = T * nx;
+        sb = f0;
+        ss = st;
     }
+    auto fofs = [&](int e) -> size_t {
+        if constexpr (LAY == LAY_QUAD && T < 2) return quad_index(x, t + e * T, nx);
+        else return f0 + (size_t)e * st;
+    };
+    float2* base = a.field + a.bstride * b;
+    float2 v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = base[fofs(e)];
     // stores recompute their addresses from an opaque base (keeps 16 64-bit
     // pointers from living across the transforms)
     auto store_col = [&](float2* dst) {
-        float2* p1 = opaque(dst) + t * nx;
-        const int st = opaque(T * nx);
+        float2* p1 = opaque(dst);
 #pragma unroll
-        for (int e = 0; e < E; ++e) p1[e * st] = v[e];
+        for (int e = 0; e < E; ++e) p1[fofs(e)] = v[e];
     };
 
     if constexpr (MODE == COL_PLAIN) {
@@ -212,17 +305,54 @@ __global__ void __launch_bounds__(LineCfg<NY>::T * C) k_col(ColArgs a) {
         return;
     } else {
         fft_line<NY, -1>(v, t, smem, idx, a.tw);  // completes the forward transform
-        const float* tg = a.target + a.t_bstride * b + x;
-        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        if constexpr (MODE == COL_GS) {
-            float* w = a.weights ? a.weights + a.t_bstride * b + x : nullptr;
+        const float norm = a.norm;
+        const float* tg = a.target + a.t_bstride * b + sb;
+        constexpr int NV = MODE == COL_OSPR ? 7 : 4;
+        float acc[NV];
+#pragma unroll
+        for (int i = 0; i < NV; ++i) acc[i] = 0.f;
+        if constexpr (MODE == COL_GS_FAST || MODE == COL_WGS_FAST) {
+            // GS/WGS, no ROI, phase freedom: mse partials (metrics.hpp:70-97) and
+            // R <- amp * R/|R| (ifta.hpp:198-214), branch-free
+            const bool last = a.last;
+            float* w = MODE == COL_WGS_FAST ? a.weights + a.t_bstride * b + sb : nullptr;
+            const float lo = a.clamp_lo, hi = a.clamp_hi;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const float2 R = cscale(v[e], norm);
+                const float r2 = R.x * R.x + R.y * R.y;
+                const float amp0 = __ldg(&tg[e * ss]);
+                const float ri = rsqrtf(r2);                 // +inf at r2 == 0
+                const float r = r2 > 0.f ? r2 * ri : 0.f;    // |R|
+                const float d = amp0 - r;
+                acc[0] = fmaf(d, d, acc[0]);
+                acc[1] = fmaf(amp0, r, acc[1]);
+                acc[2] += r2;
+                acc[3] = fmaf(amp0, amp0, acc[3]);
+                float amp = amp0;
+                if constexpr (MODE == COL_WGS_FAST) {
+                    if (!last && amp0 > 0.f) {  // ifta.hpp:198-204
+                        const float cand = w[e * ss] * amp0 * (r > 1e-12f ? ri : 1e12f);
+                        const float wn = fminf(fmaxf(cand, lo), hi);
+                        w[e * ss] = wn;
+                        amp = amp0 * wn;
+                    }
+                }
+                const float sc = amp * ri;
+                v[e] = r2 > 0.f ? make_float2(R.x * sc, R.y * sc) : make_float2(amp, 0.f);
+                if (last) v[e] = R;
+            }
+        } else if constexpr (MODE == COL_GS_GENERIC) {
+            float* w = a.weights ? a.weights + a.t_bstride * b + sb : nullptr;
+            const float2* tcs = a.tphase_cs ? a.tphase_cs + a.t_bstride * b + sb : nullptr;
+            const uint8_t* roi = a.roi ? a.roi + sb : nullptr;
 #pragma unroll
             for (int e = 0; e < E; ++e) {
                 const int y = t + e * T;
-                const int off = y * nx;
-                float2 R = cscale(v[e], a.norm);
-                const bool in_roi = !a.roi || a.roi[off + x];
-                float amp = __ldg(&tg[off]);
+                const size_t so = (size_t)e * ss;
+                float2 R = cscale(v[e], norm);
+                const bool in_roi = !roi || roi[so];
+                float amp = __ldg(&tg[so]);
                 float r = sqrtf(R.x * R.x + R.y * R.y);
                 if (in_roi) {  // mse partials (metrics.hpp:70-97)
                     float d = amp - r;
@@ -236,20 +366,20 @@ __global__ void __launch_bounds__(LineCfg<NY>::T * C) k_col(ColArgs a) {
                         const bool active = !a.lt || (x >= a.lt_x0 && x < a.lt_x1 && y >= a.lt_y0 && y < a.lt_y1);
                         if (active) {
                             if (w && amp > 0.f) {
-                                float cand = w[off] * amp / fmaxf(r, 1e-12f);
+                                float cand = w[so] * amp / fmaxf(r, 1e-12f);
                                 float wn = fminf(fmaxf(cand, a.clamp_lo), a.clamp_hi);
-                                w[off] = wn;
+                                w[so] = wn;
                                 amp *= wn;
                             }
                             if (a.phase_freedom) {
                                 if (r > 0.f) {
-                                    float s = amp / r;
-                                    R = make_float2(R.x * s, R.y * s);
+                                    float sc = amp / r;
+                                    R = make_float2(R.x * sc, R.y * sc);
                                 } else {
                                     R = make_float2(amp, 0.f);
                                 }
                             } else {
-                                float2 cs = a.tphase_cs[a.t_bstride * b + off + x];
+                                float2 cs = tcs[so];
                                 R = make_float2(amp * cs.x, amp * cs.y);
                             }
                         }
@@ -259,45 +389,41 @@ __global__ void __launch_bounds__(LineCfg<NY>::T * C) k_col(ColArgs a) {
                 }
                 v[e] = R;
             }
+        } else {  // COL_OSPR: ospr.hpp:134-145
+            float* S = a.S + a.S_bstride * b + sb;
+            const float inv_n = a.inv_n;
+            const uint8_t* roi = a.roi ? a.roi + sb : nullptr;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const float2 R = cscale(v[e], norm);
+                const float I = R.x * R.x + R.y * R.y;
+                const float sv = S[e * ss] + I;
+                S[e * ss] = sv;
+                const float m = (!roi || roi[e * ss]) ? 1.f : 0.f;
+                const float amp = __ldg(&tg[e * ss]) * m;
+                const float r = sqrtf(I) * m;
+                const float d = amp - r;
+                acc[0] = fmaf(d, d, acc[0]);
+                acc[1] = fmaf(amp, r, acc[1]);
+                acc[2] = fmaf(I, m, acc[2]);
+                acc[3] = fmaf(amp, amp, acc[3]);
+                const float rc = sqrtf(sv * inv_n) * m;
+                const float dc = amp - rc;
+                acc[4] = fmaf(dc, dc, acc[4]);
+                acc[5] = fmaf(amp, rc, acc[5]);
+                acc[6] = fmaf(rc, rc, acc[6]);
+            }
+        }
+        if constexpr (MODE != COL_OSPR) {
             if (a.last) {
-                store_col(a.replay_out + a.bstride * b + x);
+                store_col(a.replay_out + a.bstride * b);
             } else {
                 fft_line<NY, +1>(v, t, smem, idx, a.tw);  // starts the next inverse transform
                 store_col(base);
             }
-        } else {  // COL_OSPR: ospr.hpp:134-145
-            float* S = a.S + a.S_bstride * b + x;
-#pragma unroll
-            for (int e = 0; e < E; ++e) {
-                const int y = t + e * T;
-                const int off = y * nx;
-                float2 R = cscale(v[e], a.norm);
-                float I = R.x * R.x + R.y * R.y;
-                float s = S[off] + I;
-                S[off] = s;
-                if (!a.roi || a.roi[off + x]) {
-                    float amp = __ldg(&tg[off]);
-                    float r = sqrtf(I);
-                    float d = amp - r;
-                    acc[0] += d * d;
-                    acc[1] += amp * r;
-                    acc[2] += I;
-                    acc[3] += amp * amp;
-                    float rc = sqrtf(s * a.inv_n);
-                    float dc = amp - rc;
-                    acc[4] += dc * dc;
-                    acc[5] += amp * rc;
-                    acc[6] += rc * rc;
-                }
-            }
         }
-        // per-thread float partials (<= 16 terms) -> fixed-order double block sums
         const size_t blk = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
-        constexpr int NV = MODE == COL_GS ? 4 : 7;
-        double dacc[NV];
-#pragma unroll
-        for (int i = 0; i < NV; ++i) dacc[i] = (double)acc[i];
-        block_sum_store<NV>(dacc, a.partials + blk * 8);
+        block_sum_float_store<NV>(acc, a.partials + blk * 8);
     }
 }
 

@@ -57,7 +57,7 @@ def parse():
     ap.add_argument("--targets", type=int, default=64, help="targets per GPU per step")
     ap.add_argument("--iters", type=int, default=25)
     ap.add_argument("--ospr-n", type=int, default=1024)
-    ap.add_argument("--ospr-jobs", type=int, default=64, help="OSPR jobs per GPU per step")
+    ap.add_argument("--ospr-jobs", type=int, default=148, help="OSPR jobs per GPU per step (one MT stream per SM)")
     ap.add_argument("--ospr-subframes", type=int, default=24)
     ap.add_argument("--no-ospr", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

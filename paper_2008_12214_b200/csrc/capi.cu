@@ -994,7 +994,7 @@ struct hgc_ospr_plan {
     bool wide_levels = false, has_roi = false;
     size_t M = 0;
     int tiles = 0;
-    DBuf<float2> field;
+    DBuf<float2> field, field2;  // double-buffered seeded field (plain OSPR)
     DBuf<float> target_f, S;
     DBuf<double> amp_d, partials, traces;
     DBuf<uint8_t> roi, lv8;
@@ -1006,11 +1006,19 @@ struct hgc_ospr_plan {
     uint64_t graph_sig = 0;
     int launches = 0;
     bool uploaded = false;
+    cudaStream_t stream2 = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_seed = nullptr, ev_pass[2] = {nullptr, nullptr};
 
     ~hgc_ospr_plan() {
         if (graph) cudaGraphExecDestroy(graph);
+        for (cudaEvent_t e : {ev_fork, ev_seed, ev_pass[0], ev_pass[1]})
+            if (e) cudaEventDestroy(e);
+        if (stream2) cudaStreamDestroy(stream2);
         if (stream) cudaStreamDestroy(stream);
     }
+
+    bool overlapped() const { return cfg.variant == 0 && field2.p; }
+    float2* buf(int n) const { return (overlapped() && (n & 1) == 0) ? field2.p : field.p; }
 
     float norm() const { return (float)(1.0 / std::sqrt((double)nx * ny)); }
 
@@ -1021,7 +1029,7 @@ struct hgc_ospr_plan {
         sa.seeds = n == 1 ? seeds.p : nullptr;
         sa.amp = amp_d.p;
         sa.amp_stride = per_job ? npix : 0;
-        sa.out = field.p;
+        sa.out = buf(n);
         sa.out_stride = npix;
         sa.npix = npix;
         sa.quad = 1;
@@ -1035,10 +1043,10 @@ struct hgc_ospr_plan {
         }
         return sa;
     }
-    ColArgs col_inv_args() const {
+    ColArgs col_inv_args(int n) const {
         ColArgs ci{};
         ci.tw = tw;
-        ci.field = field.p;
+        ci.field = buf(n);
         ci.bstride = npix;
         ci.nx = nx;
         ci.layout = LAY_QUAD;
@@ -1049,7 +1057,7 @@ struct hgc_ospr_plan {
         const int N = cfg.subframes;
         RowArgs ra{};
         ra.tw = tw;
-        ra.field = field.p;
+        ra.field = buf(n);
         ra.bstride = npix;
         ra.ny = ny;
         ra.layout = LAY_QUAD;
@@ -1063,7 +1071,7 @@ struct hgc_ospr_plan {
     ColArgs col_acc_args(int n) const {
         ColArgs co{};
         co.tw = tw;
-        co.field = field.p;
+        co.field = buf(n);
         co.bstride = npix;
         co.nx = nx;
         co.layout = LAY_QUAD;
@@ -1080,17 +1088,38 @@ struct hgc_ospr_plan {
     }
 
     // run_ospr_impl's subframe loop (ospr.hpp:105-147), all jobs at once.
+    // Plain OSPR: the seed of frame n+1 (one MT stream per job, its own
+    // stream of the graph) overlaps the three passes of frame n on a second
+    // field buffer; a seed CTA (512 thr x 56 regs, 40 KiB) co-resides with a
+    // pass CTA on an SM.  Adaptive OSPR seeds frame n from S after frame n-1,
+    // so it stays sequential.
     void record(cudaStream_t st) {
         launches = 0;
         const int N = cfg.subframes;
         CK(cudaMemsetAsync(S.p, 0, sizeof(float) * npix * jobs, st));
+        const bool ov = overlapped();
+        cudaStream_t ss = ov ? stream2 : st;
+        if (ov) {  // fork the seed stream into the capture
+            CK(cudaEventRecord(ev_fork, st));
+            CK(cudaStreamWaitEvent(ss, ev_fork, 0));
+        }
         for (int n = 1; n <= N; ++n) {
-            k_seed_random_phase<<<jobs, kSeedThreads, kSeedSmem, st>>>(seed_args(n));
+            if (ov && n >= 3) CK(cudaStreamWaitEvent(ss, ev_pass[n & 1], 0));  // buffer n%2 free again
+            k_seed_random_phase<<<jobs, kSeedThreads, kSeedSmem, ss>>>(seed_args(n));
             CK(cudaGetLastError());
-            col_plain(ny, col_inv_args(), jobs, st);
+            if (ov) {
+                CK(cudaEventRecord(ev_seed, ss));
+                CK(cudaStreamWaitEvent(st, ev_seed, 0));
+            }
+            col_plain(ny, col_inv_args(n), jobs, st);
             row_fused(nx, row_args(n), jobs, st);
             col_ospr(ny, col_acc_args(n), jobs, st);
+            if (ov) CK(cudaEventRecord(ev_pass[n & 1], st));
             launches += 4;
+        }
+        if (ov) {  // join the seed stream
+            CK(cudaEventRecord(ev_fork, ss));
+            CK(cudaStreamWaitEvent(st, ev_fork, 0));
         }
         k_finalize<<<jobs, 32, 0, st>>>(partials.p, N, jobs, tiles, (double)M, cfg.freedom_scale, 1, traces.p);
         ++launches;
@@ -1134,6 +1163,14 @@ int hgc_ospr_plan_create(hgc_ospr_plan** out, const hgc_ospr_cfg* cfg, const hgc
         const size_t tot = p->npix * jobs;
         const size_t ttot = p->per_job ? tot : p->npix;
         p->field.alloc(tot);
+        if (cfg->variant == 0 && cfg->subframes > 1) {  // second buffer + stream for seed/pass overlap
+            p->field2.alloc(tot);
+            CK(cudaStreamCreateWithFlags(&p->stream2, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&p->ev_seed, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&p->ev_pass[0], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&p->ev_pass[1], cudaEventDisableTiming));
+        }
         p->S.alloc(tot);
         p->target_f.alloc(ttot);
         p->amp_d.alloc(ttot);
@@ -1287,7 +1324,7 @@ int hgc_ospr_plan_profile(hgc_ospr_plan* p, int reps, double* ms_seed, double* m
             *ms_seed = time_launches(st, reps, [&] {
                 k_seed_random_phase<<<j, kSeedThreads, kSeedSmem, st>>>(p->seed_args(1));
             });
-        if (ms_col_inv) *ms_col_inv = time_launches(st, reps, [&] { col_plain(p->ny, p->col_inv_args(), j, st); });
+        if (ms_col_inv) *ms_col_inv = time_launches(st, reps, [&] { col_plain(p->ny, p->col_inv_args(1), j, st); });
         if (ms_row) *ms_row = time_launches(st, reps, [&] { row_fused(p->nx, p->row_args(1), j, st); });
         if (ms_col_acc) *ms_col_acc = time_launches(st, reps, [&] { col_ospr(p->ny, p->col_acc_args(1), j, st); });
         CK(cudaGetLastError());

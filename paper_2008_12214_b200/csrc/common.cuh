@@ -4,6 +4,9 @@
 #include <stdint.h>
 
 #define HG_TWO_PI 6.283185307179586476925286766559
+#ifndef HG_STREAM_LOADS
+#define HG_STREAM_LOADS 1
+#endif
 #define HG_PI 3.1415926535897932384626433832795
 
 // Complex products with every product/sum rounded separately (no FMA
@@ -69,6 +72,27 @@ __host__ __device__ __forceinline__ size_t colpair_index(int x, int y, int ny) {
     return (((size_t)(x >> 1) * ny + y) << 1) + (x & 1);
 }
 }  // namespace hg
+
+// Streaming loads that do not allocate in L1 (keeps the L1-resident twiddle
+// table hot while tiles stream through).
+__device__ __forceinline__ float2 ld_stream(const float2* p) {
+#if HG_STREAM_LOADS
+    float2 v;
+    asm volatile("ld.global.L1::no_allocate.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+    return v;
+#else
+    return *p;
+#endif
+}
+__device__ __forceinline__ float ld_stream(const float* p) {
+#if HG_STREAM_LOADS
+    float v;
+    asm volatile("ld.global.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
 
 // ------------------------------------------------ TMA bulk copy + mbarrier
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

@@ -27,6 +27,7 @@
 #define HG_COLQ_MINB 2
 #endif
 
+
 namespace hg {
 
 // --------------------------------------------------------------- reductions
@@ -134,7 +135,7 @@ __global__ void __launch_bounds__(RowCfg<NX, LAY>::THREADS, RowCfg<NX, LAY>::MIN
     };
     float2 v[E];
 #pragma unroll
-    for (int e = 0; e < E; ++e) v[e] = fb[addr(e)];
+    for (int e = 0; e < E; ++e) v[e] = ld_stream(&fb[addr(e)]);
 
     if constexpr (MODE == ROW_PLAIN) {
         // Propagator<float>::forward / inverse halves (propagation.hpp:81-95):
@@ -286,7 +287,7 @@ __global__ void __launch_bounds__(LineCfg<NY>::T * C, ColCfg<NY, LAY>::MIN_BLOCK
     float2* base = a.field + a.bstride * b;
     float2 v[E];
 #pragma unroll
-    for (int e = 0; e < E; ++e) v[e] = base[fofs(e)];
+    for (int e = 0; e < E; ++e) v[e] = ld_stream(&base[fofs(e)]);
     // stores recompute their addresses from an opaque base (keeps 16 64-bit
     // pointers from living across the transforms)
     auto store_col = [&](float2* dst) {

@@ -471,6 +471,7 @@ struct hgc_ifta_plan {
     int tiles = 0;
     int bx0 = 0, by0 = 0, bw = 0, bh = 0;  // LT roi bounding box
     DBuf<float2> field, Q, tphase_cs, init_field, scratch;
+    cudaEvent_t done = nullptr;  // recorded after each execute on the execute stream
     DBuf<float> target_f, weights, init_weights;
     DBuf<double> amp_d, phase_d, partials, trace;
     DBuf<uint8_t> roi, roi_rm, lv8;
@@ -486,6 +487,7 @@ struct hgc_ifta_plan {
 
     ~hgc_ifta_plan() {
         if (graph) cudaGraphExecDestroy(graph);
+        if (done) cudaEventDestroy(done);
         if (stream) cudaStreamDestroy(stream);
     }
 
@@ -755,11 +757,13 @@ int hgc_ifta_plan_create(hgc_ifta_plan** out, const hgc_ifta_cfg* cfg, const hgc
         if (fresnel) {
             p->Q.ensure(p->npix);
             double scale = 3.1415926535897932384626433832795 / (fresnel->wavelength * fresnel->distance);
-            k_fresnel_q<<<ew_grid(p->npix), 256>>>(nx, ny, scale, fresnel->pixel_pitch_x, fresnel->pixel_pitch_y, p->Q.p);
+            k_fresnel_q<<<ew_grid(p->npix), 256, 0, p->stream>>>(nx, ny, scale, fresnel->pixel_pitch_x,
+                                                                  fresnel->pixel_pitch_y, p->Q.p);
             CK(cudaGetLastError());
         }
         prepare_kernels(nx, ny);
-        CK(cudaDeviceSynchronize());
+        CK(cudaEventCreateWithFlags(&p->done, cudaEventDisableTiming));
+        CK(cudaStreamSynchronize(p->stream));
         *out = p.release();
     });
 }
@@ -873,6 +877,7 @@ int hgc_ifta_plan_execute(hgc_ifta_plan* p, void* stream) {
             cudaGraphDestroy(g);
         }
         CK(cudaGraphLaunch(p->graph, st));
+        CK(cudaEventRecord(p->done, st));
     });
 }
 
@@ -880,7 +885,7 @@ int hgc_ifta_plan_download(hgc_ifta_plan* p, hgc_ifta_io* io) {
     return guarded([&] {
         if (!p || !io) invalid("hgc_ifta_plan_download: null argument");
         CK(cudaSetDevice(p->device));
-        CK(cudaDeviceSynchronize());
+        CK(cudaEventSynchronize(p->done));  // this plan's last execute only (other plans keep running)
         const size_t tot = p->npix * p->batch;
         const int K = p->cfg.iterations;
         if (io->replay) {  // resident quad layout -> row-major
@@ -1008,10 +1013,11 @@ struct hgc_ospr_plan {
     bool uploaded = false;
     cudaStream_t stream2 = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_seed = nullptr, ev_pass[2] = {nullptr, nullptr};
+    cudaEvent_t done = nullptr;  // recorded after each execute on the execute stream
 
     ~hgc_ospr_plan() {
         if (graph) cudaGraphExecDestroy(graph);
-        for (cudaEvent_t e : {ev_fork, ev_seed, ev_pass[0], ev_pass[1]})
+        for (cudaEvent_t e : {ev_fork, ev_seed, ev_pass[0], ev_pass[1], done})
             if (e) cudaEventDestroy(e);
         if (stream2) cudaStreamDestroy(stream2);
         if (stream) cudaStreamDestroy(stream);
@@ -1182,7 +1188,8 @@ int hgc_ospr_plan_create(hgc_ospr_plan** out, const hgc_ospr_cfg* cfg, const hgc
         p->mt.alloc(jobs);
         p->seeds.alloc(jobs);
         prepare_kernels(nx, ny);
-        CK(cudaDeviceSynchronize());
+        CK(cudaEventCreateWithFlags(&p->done, cudaEventDisableTiming));
+        CK(cudaStreamSynchronize(p->stream));
         *out = p.release();
     });
 }
@@ -1243,6 +1250,7 @@ int hgc_ospr_plan_execute(hgc_ospr_plan* p, void* stream) {
             cudaGraphDestroy(g);
         }
         CK(cudaGraphLaunch(p->graph, st));
+        CK(cudaEventRecord(p->done, st));
     });
 }
 
@@ -1250,7 +1258,7 @@ int hgc_ospr_plan_download(hgc_ospr_plan* p, hgc_ospr_io* io) {
     return guarded([&] {
         if (!p || !io) invalid("hgc_ospr_plan_download: null argument");
         CK(cudaSetDevice(p->device));
-        CK(cudaDeviceSynchronize());
+        CK(cudaEventSynchronize(p->done));
         const int N = p->cfg.subframes;
         const size_t npix = p->npix, tot = npix * p->jobs, lvtot = tot * N;
         std::vector<double> tr((size_t)N * p->jobs * 2);

@@ -212,7 +212,15 @@ int hgc_propagate(int nx, int ny, int sign, const hgc_fresnel* fresnel, int batc
 int hgc_quantise(const hgc_slm* slm, int nx, int ny, int batch, float* field, int32_t* levels);
 /* seed_random_phase<float>(amp, Rng) with the engine seeded by
  * `engine_seed` (Rng(seed).fork(0) uses hgc_fork_seed(seed, 0)) after
- * discarding `skip` draws. */
+ * discarding `skip` draws (std::mt19937_64::discard, by jump-ahead: O(1) in
+ * skip).  The draws are split across CTAs by jump-ahead; the result is the
+ * single sequential stream of rng.hpp:54-67. */
+/* Host utility: the std::mt19937_64 (rng.hpp:23-34) state after `draws`
+ * draws from seed `engine_seed`, as the 312 raw words x_draws .. x_draws+311
+ * whose twist yields the next output (libstdc++ _M_x with _M_p == 312).
+ * Computed by jump-ahead (x^(draws-1) mod the engine's characteristic
+ * polynomial); no device needed. */
+int hgc_mt_jump_state(uint64_t engine_seed, uint64_t draws, uint64_t* window);
 int hgc_seed_random_phase(const double* amplitude, int nx, int ny, uint64_t engine_seed,
                           uint64_t skip, float* out);
 uint64_t hgc_fork_seed(uint64_t seed, uint64_t stream);

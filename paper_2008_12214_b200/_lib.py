@@ -103,6 +103,7 @@ _SIGS = {
     "hgc_propagate": (_i, [_i, _i, _i, _P(HgcFresnel), _i, _vp, _vp]),
     "hgc_quantise": (_i, [_P(HgcSlm), _i, _i, _i, _vp, _vp]),
     "hgc_seed_random_phase": (_i, [_vp, _i, _i, _u64, _u64, _vp]),
+    "hgc_mt_jump_state": (_i, [_u64, _u64, _vp]),
     "hgc_fork_seed": (_u64, [_u64, _u64]),
     "hgc_mse": (_i, [_vp, _vp, _vp, _i, _i, _i, _P(_d)]),
     "hgc_fresnel_phase": (_i, [_i, _i, _P(HgcFresnel), _vp]),

@@ -213,6 +213,13 @@ def seed_random_phase(amp: np.ndarray, seed: int, skip: int = 0, engine_seed: in
     return out
 
 
+def mt_jump_state(engine_seed: int, draws: int) -> np.ndarray:
+    """std::mt19937_64 state after ``draws`` draws (312 raw words, host jump-ahead)."""
+    out = np.empty(312, np.uint64)
+    check(lib.hgc_mt_jump_state(engine_seed, draws, _p(out)))
+    return out
+
+
 # ----------------------------------------------------------------- metric
 def mse(target: np.ndarray, replay: np.ndarray, cfg: MetricConfig | None = None) -> float:
     """mse() phase-insensitive (metrics.hpp:70-124)."""

@@ -22,6 +22,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
                 "-Xptxas", "-v"]
 
+HOST_FLAGS = ["-Xcompiler", "-mpclmul"]  # host-only translation units (mtjump.cpp)
+
 
 def _stale(obj: str, deps: list[str]) -> bool:
     if not os.path.exists(obj):
@@ -38,19 +40,20 @@ def build(verbose: bool = False, jobs: int | None = None, defines: list[str] | N
         LIB, OBJ = out, objdir or out + ".obj"
     extra = [f"-D{d}" for d in (defines or [])]
     os.makedirs(OBJ, exist_ok=True)
-    srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
     headers = glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) + \
         glob.glob(os.path.join(PKG, "..", "include", "*.h"))
     objs, todo = [], []
     for s in srcs:
-        o = os.path.join(OBJ, os.path.basename(s)[:-3] + ".o")
+        o = os.path.join(OBJ, os.path.splitext(os.path.basename(s))[0] + ".o")
         objs.append(o)
         if _stale(o, [s, *headers, __file__]):
             todo.append((s, o))
 
     def compile_one(so):
         s, o = so
-        cmd = [NVCC, *FLAGS, *extra, "-c", s, "-o", o]
+        host = HOST_FLAGS if s.endswith(".cpp") else []
+        cmd = [NVCC, *FLAGS, *host, *extra, "-c", s, "-o", o]
         r = subprocess.run(cmd, capture_output=True, text=True)
         with open(o + ".log", "w") as f:
             f.write(r.stdout + r.stderr)

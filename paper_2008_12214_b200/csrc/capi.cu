@@ -19,6 +19,7 @@
 #include "errors.h"
 #include "launch.h"
 #include "mt64.cuh"
+#include "mtjump.h"
 #include "passes.cuh"
 
 namespace hg {
@@ -127,6 +128,59 @@ static void prepare_kernels(int nx, int ny) {
     col_ospr(ny, ca, 1, nullptr, true);
     CK(cudaFuncSetAttribute(k_seed_random_phase, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSeedSmem));
 }
+
+// ------------------------------------------ RNG chunking (jump-ahead)
+// One reference stream split across several CTAs: CTA (stream s, chunk c)
+// starts at draw offset0 + c*len, its state set by k_mt_jump from the
+// polynomials of mtjump.cpp (computed once per process per shape).  Enough
+// chunks that streams*chunks fills the GPU twice, none shorter than
+// kMinChunkDraws (the jump costs about as much as ~30k draws).
+constexpr size_t kMinChunkDraws = 32768;
+constexpr int kMaxChunks = 512;
+struct SeedChunks {
+    int chunks = 1;
+    size_t len = 0;
+    uint64_t offset0 = 0;
+    DBuf<uint64_t> polys;
+
+    void plan(size_t npix, int streams, uint64_t offset = 0) {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        long long c = (2LL * sms + streams - 1) / std::max(1, streams);
+        c = std::min<long long>(c, std::max<size_t>(1, npix / kMinChunkDraws));
+        if (const char* ev = getenv("HG_SEED_CHUNKS")) c = std::max(1, atoi(ev));  // tuning / tests
+        c = std::min<long long>(c, (long long)std::max<size_t>(1, npix));
+        c = std::max<long long>(1, std::min<long long>(c, kMaxChunks));
+        len = (npix + c - 1) / c;
+        chunks = (int)((npix + len - 1) / len);
+        offset0 = offset;
+        polys.reset();
+        if (jumps()) {
+            const std::vector<uint64_t>& v = mt_chunk_polys(offset0, len, chunks);
+            polys.alloc(v.size());
+            CK(cudaMemcpy(polys.p, v.data(), sizeof(uint64_t) * v.size(), cudaMemcpyHostToDevice));
+        }
+    }
+    int c_first() const { return offset0 == 0 ? 1 : 0; }
+    bool jumps() const { return chunks > c_first(); }
+    // jump (when needed) + chunked seed; `seeds` are engine seeds (already forked),
+    // `states` holds streams*chunks entries.  Returns the number of launches.
+    int launch(SeedArgs sa, const uint64_t* seeds, MtState* states, int streams, cudaStream_t st) const {
+        int n = 0;
+        if (jumps()) {
+            JumpArgs ja{seeds, polys.p, states, chunks, c_first()};
+            k_mt_jump<<<streams * (chunks - c_first()), kJumpThreads, 0, st>>>(ja);
+            ++n;
+        }
+        sa.states = states;
+        sa.seeds = offset0 == 0 ? seeds : nullptr;
+        sa.chunks = chunks;
+        sa.chunk_len = len;
+        k_seed_random_phase<<<streams * chunks, kSeedThreads, kSeedSmem, st>>>(sa);
+        return n + 1;
+    }
+};
 
 // ------------------------------------------------------- small kernels
 __global__ void k_fill_f(float* p, size_t n, float v) {
@@ -478,6 +532,7 @@ struct hgc_ifta_plan {
     DBuf<uint16_t> lv16;
     DBuf<MtState> mt;
     DBuf<uint64_t> seeds;
+    SeedChunks chunking;
     const float2* tw = nullptr;
     cudaGraphExec_t graph = nullptr;
     uint64_t graph_sig = 0;
@@ -603,8 +658,7 @@ struct hgc_ifta_plan {
             k_init_target_phase<<<ew_grid(tot), 256, 0, st>>>(amp_d.p, phase_d.p, field.p, nx, ny, tot);
             ++launches;
         } else {
-            k_seed_random_phase<<<batch, kSeedThreads, kSeedSmem, st>>>(seed_args());
-            ++launches;
+            launches += chunking.launch(seed_args(), seeds.p, mt.p, batch, st);
         }
         CK(cudaGetLastError());
         if (cfg.variant == 1) {
@@ -752,7 +806,8 @@ int hgc_ifta_plan_create(hgc_ifta_plan** out, const hgc_ifta_cfg* cfg, const hgc
         else p->lv8.alloc(tot);
         p->partials.alloc((size_t)cfg->iterations * batch * p->tiles * 8);
         p->trace.alloc((size_t)cfg->iterations * batch);
-        p->mt.alloc(batch);
+        if (p->random_init()) p->chunking.plan(p->npix, batch);
+        p->mt.alloc((size_t)batch * p->chunking.chunks);
         p->seeds.alloc(batch);
         if (fresnel) {
             p->Q.ensure(p->npix);
@@ -949,7 +1004,7 @@ int hgc_ifta_plan_profile(hgc_ifta_plan* p, int reps, double* ms_seed, double* m
         const int b = p->batch;
         if (ms_seed)
             *ms_seed = time_launches(st, reps, [&] {
-                k_seed_random_phase<<<b, kSeedThreads, kSeedSmem, st>>>(p->seed_args());
+                p->chunking.launch(p->seed_args(), p->seeds.p, p->mt.p, b, st);
             });
         const int k = p->cfg.iterations > 1 ? 1 : p->cfg.iterations;  // a constraining iteration when K > 1
         if (ms_row) *ms_row = time_launches(st, reps, [&] { row_fused(p->nx, p->row_args(false), b, st); });
@@ -1453,6 +1508,13 @@ int hgc_quantise(const hgc_slm* slm, int nx, int ny, int batch, float* field, in
     });
 }
 
+int hgc_mt_jump_state(uint64_t engine_seed, uint64_t draws, uint64_t* window) {
+    return guarded([&] {
+        if (!window) invalid("mt_jump_state: null buffer");
+        mt_jump_state_host(engine_seed, draws, window);
+    });
+}
+
 int hgc_seed_random_phase(const double* amplitude, int nx, int ny, uint64_t engine_seed, uint64_t skip, float* out) {
     return guarded([&] {
         if (!amplitude || !out) invalid("seed_random_phase: null buffer");
@@ -1467,23 +1529,17 @@ int hgc_seed_random_phase(const double* amplitude, int nx, int ny, uint64_t engi
         DBuf<uint64_t> sd;
         a.alloc(npix);
         f.alloc(npix);
-        mt.alloc(1);
         sd.alloc(1);
         CK(cudaMemcpy(a.p, amplitude, sizeof(double) * npix, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(sd.p, &engine_seed, sizeof(uint64_t), cudaMemcpyHostToDevice));
+        SeedChunks ch;
+        ch.plan(npix, 1, skip);  // skip: jump ahead instead of drawing
+        mt.alloc(ch.chunks);
         SeedArgs sa{};
-        sa.states = mt.p;
-        sa.seeds = sd.p;
-        if (skip) {  // advance the stream without producing output
-            sa.npix = skip;
-            k_seed_random_phase<<<1, kSeedThreads, kSeedSmem>>>(sa);
-            CK(cudaGetLastError());
-            sa.seeds = nullptr;
-        }
         sa.amp = a.p;
         sa.out = f.p;
         sa.npix = npix;
-        k_seed_random_phase<<<1, kSeedThreads, kSeedSmem>>>(sa);
+        ch.launch(sa, sd.p, mt.p, 1, nullptr);
         CK(cudaGetLastError());
         CK(cudaMemcpy(out, f.p, sizeof(float2) * npix, cudaMemcpyDeviceToHost));
     });

@@ -141,17 +141,94 @@ struct SeedArgs {
     // output layout: quad != 0 writes the plans' LAY_QUAD field (and reads S
     // column-pair major); otherwise row-major.  nx, ny used when quad != 0.
     int quad, nx, ny;
+    // chunking: CTA b = stream * chunks + c draws [c*chunk_len, min(npix, (c+1)*chunk_len))
+    // of this launch, starting from states[b] (set by k_mt_jump) unless c == 0 and seeds
+    // is given.  chunks <= 1: one CTA per stream over all npix draws.
+    int chunks;
+    size_t chunk_len;
 };
+
+// Jump-ahead (mtjump.cpp): CTA (stream s, chunk c) writes states[s*chunks + c]
+// = the engine seeded with seeds[s] advanced by offset0 + c*len draws, as the
+// window g(F) W_1 with g = polys[c - c_first] (x^(offset0 + c*len - 1) mod P):
+// word j = XOR over set bits i of g of raw word x_{1+i+j}.  The raw words are
+// regenerated block by block (one warp twists block q+2 while the CTA
+// accumulates over bits [312q, 312q+312) from blocks q, q+1); each block is
+// stored twice (slots b%3 and b%3+3) so reads never wrap.
+constexpr int kJumpThreads = 320;
+constexpr int kPolyWords = 312;
+struct JumpArgs {
+    const uint64_t* seeds;  // [streams] engine seeds
+    const uint64_t* polys;  // [chunks - c_first][kPolyWords]
+    MtState* states;        // [streams * chunks]
+    int chunks, c_first;
+};
+
+__global__ void __launch_bounds__(kJumpThreads) k_mt_jump(JumpArgs a) {
+    __shared__ uint64_t ring[6 * kMtN];
+    __shared__ uint64_t g[kPolyWords + 1];
+    const int per = a.chunks - a.c_first;
+    const int s = blockIdx.x / per, c = a.c_first + blockIdx.x % per;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t* gp = a.polys + (size_t)(c - a.c_first) * kPolyWords;
+    for (int i = tid; i < kPolyWords; i += blockDim.x) g[i] = gp[i];
+    if (tid == 0) {
+        g[kPolyWords] = 0;
+        uint64_t x = a.seeds[s];  // std::mt19937_64::seed: block 0
+        ring[0] = ring[3 * kMtN] = x;
+        for (int i = 1; i < kMtN; ++i) {
+            x = 6364136223846793005ull * (x ^ (x >> 62)) + (uint64_t)i;
+            ring[i] = ring[3 * kMtN + i] = x;
+        }
+    }
+    __syncthreads();
+    if (warp == 0) {  // block 1
+        mt_twist_warp(ring, ring + kMtN, lane);
+        for (int i = lane; i < kMtN; i += 32) ring[4 * kMtN + i] = ring[kMtN + i];
+    }
+    __syncthreads();
+    constexpr int kBits = kPolyWords * 64;
+    uint64_t acc = 0;
+    const int j = tid;
+    for (int q = 0; q * kMtN < kBits; ++q) {
+        if (warp == 0 && (q + 2) * kMtN <= kBits + kMtN) {  // block q+2 from block q+1
+            const int so = (q + 1) % 3, sn = (q + 2) % 3;
+            mt_twist_warp(ring + so * kMtN, ring + sn * kMtN, lane);
+            for (int i = lane; i < kMtN; i += 32) ring[(sn + 3) * kMtN + i] = ring[sn * kMtN + i];
+        }
+        if (j < kMtN) {
+            const uint64_t* base = ring + (q % 3) * kMtN + 1 + j;  // x_{312q + 1 + j + ii} = base[ii]
+            const int i0 = q * kMtN;
+#pragma unroll 1
+            for (int k = 0; k < kMtN; k += 64) {
+                const int bi = i0 + k;  // bits bi .. bi+63 of g (fewer at the block end)
+                if (bi >= kBits) break;
+                const int w = bi >> 6, o = bi & 63;
+                uint64_t m = o ? (g[w] >> o) | (g[w + 1] << (64 - o)) : g[w];
+                if (kMtN - k < 64) m &= (1ull << (kMtN - k)) - 1;
+                while (m) {
+                    const int b = __ffsll((long long)m) - 1;
+                    acc ^= base[k + b];
+                    m &= m - 1;
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (j < kMtN) a.states[(size_t)s * a.chunks + c].w[j] = acc;
+    if (tid == 0) a.states[(size_t)s * a.chunks + c].pos = kMtN;
+}
 
 // One CTA per stream.  Warp 0 produces twists; warps 1.. consume.
 __global__ void __launch_bounds__(kSeedThreads) k_seed_random_phase(SeedArgs a) {
     extern __shared__ uint64_t ring[];  // kRingSlots * 312 words
     __shared__ int s_pos;
-    const int s = blockIdx.x;
+    const int chunks = a.chunks > 1 ? a.chunks : 1;
+    const int s = blockIdx.x / chunks, c = blockIdx.x % chunks;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    MtState* st = a.states + s;
+    MtState* st = a.states + blockIdx.x;
     uint64_t* init = ring + (kRingSlots - 1) * kMtN;  // twist "-1" lives in the last slot
-    if (a.seeds) {
+    if (a.seeds && c == 0) {
         if (tid == 0) {  // std::mt19937_64::seed
             uint64_t x = a.seeds[s];
             init[0] = x;
@@ -167,7 +244,9 @@ __global__ void __launch_bounds__(kSeedThreads) k_seed_random_phase(SeedArgs a) 
     }
     __syncthreads();
     const int pos0 = s_pos;
-    const size_t npix = a.npix;
+    const size_t cbeg = chunks > 1 ? (size_t)c * a.chunk_len : 0;
+    if (cbeg >= a.npix) return;
+    const size_t npix = chunks > 1 ? (a.npix - cbeg < a.chunk_len ? a.npix - cbeg : a.chunk_len) : a.npix;
     const double* amp = a.amp + a.amp_stride * s;
     float2* out = a.out + a.out_stride * s;
 
@@ -213,7 +292,7 @@ __global__ void __launch_bounds__(kSeedThreads) k_seed_random_phase(SeedArgs a) 
                 const double theta = __dmul_rn(HG_TWO_PI, u);    // rng.hpp:62
                 double sn, cs;
                 sincos_0_2pi(theta, &sn, &cs);
-                const int p = d0 + j;  // row-major pixel index of this draw (rng.hpp:60)
+                const int p = (int)cbeg + d0 + j;  // row-major pixel index of this draw (rng.hpp:60)
                 double av = ampp[p];
                 int o = p, so = p;
                 if (a.quad) {

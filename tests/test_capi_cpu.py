@@ -78,3 +78,32 @@ def test_no_cpu_fallback():
     with pytest.raises(hg.HgcError):
         hg.run_gs(hg.IftaConfig(iterations=1, slm=hg.SlmSpec.binary_phase(),
                                 target=hg.TargetSpec(hg.patterns.bench_target(8))))
+
+
+def _mt_next(window: np.ndarray, k: int) -> np.ndarray:
+    """k tempered std::mt19937_64 outputs from a saved window (pos = 312)."""
+    m = (1 << 64) - 1
+    x = [int(v) for v in window]
+    out = []
+    for i in range(k):
+        y = (x[i] & 0xFFFFFFFF80000000) | (x[i + 1] & 0x7FFFFFFF)
+        w = x[i + 156] ^ (y >> 1) ^ (0xB5026F5AA96619E9 if y & 1 else 0)
+        x.append(w)
+        w ^= (w >> 29) & 0x5555555555555555
+        w ^= (w << 17) & 0x71D67FFFEDA60000 & m
+        w ^= (w << 37) & 0xFFF7EEE000000000 & m
+        w ^= w >> 43
+        out.append(w & m)
+    return np.array(out, np.uint64)
+
+
+@pytest.mark.parametrize("draws", [0, 1, 311, 312, 313, 4096 * 3 + 5, 1 << 24, 24 * (1 << 20) + 7])
+def test_mt_jump_state_matches_sequential_stream(oracle, draws):
+    """Jump-ahead (x^J mod the characteristic polynomial) lands exactly on draw J
+    of the sequential engine (rng.hpp:23-34); the GPU seeds chunk k of a stream
+    from these states."""
+    es = hg.fork_seed(7, 0)
+    w = hg.mt_jump_state(es, draws)
+    nxt = _mt_next(w, 8)
+    want = oracle.mt_draws(es, 8, skip=draws)
+    np.testing.assert_array_equal(nxt, want)

@@ -129,6 +129,28 @@ def test_seed_random_phase_bit_exact(oracle, n, skip):
     assert mism <= 1, mism  # CUDA vs glibc double sincos may differ by 1 ulp (~2^-29 per value)
 
 
+@pytest.mark.parametrize("chunks,skip", [(2, 0), (3, 0), (7, 1000), (64, 0), (5, 3 * 512 * 512 + 1)])
+def test_seed_chunked_jump_ahead_bit_exact(oracle, monkeypatch, chunks, skip):
+    """One stream split across CTAs by MT jump-ahead (k_mt_jump) must equal the
+    sequential stream: chunk boundaries at draw offsets that are not multiples
+    of the 312-word twist block, with and without a skip."""
+    monkeypatch.setenv("HG_SEED_CHUNKS", str(chunks))
+    amp = np.random.default_rng(3).uniform(0, 2, (512, 512))
+    got = hg.seed_random_phase(amp, seed=11, skip=skip)
+    ref = oracle.seed_random_phase(amp, 11, skip=skip)
+    mism = np.count_nonzero(got.view(np.uint32) != ref.view(np.uint32))
+    assert mism <= 1, mism
+
+
+def test_seed_default_chunking_full_size(oracle):
+    """4096^2 (16.7M draws) with the default chunking (~2 CTAs per SM)."""
+    amp = hg.patterns.bench_target(4096)
+    got = hg.seed_random_phase(amp, seed=5)
+    ref = oracle.seed_random_phase(amp, 5)
+    mism = np.count_nonzero(got.view(np.uint32) != ref.view(np.uint32))
+    assert mism <= 4, mism
+
+
 def test_fresnel_phase_matches(oracle):
     p = hg.FresnelParams(532e-9, 0.1, 8e-6, 8e-6)
     got = hg.make_fresnel_phase(512, 256, p)

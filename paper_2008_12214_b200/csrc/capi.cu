@@ -164,12 +164,13 @@ struct SeedChunks {
     }
     int c_first() const { return offset0 == 0 ? 1 : 0; }
     bool jumps() const { return chunks > c_first(); }
-    // jump (when needed) + chunked seed; `seeds` are engine seeds (already forked),
-    // `states` holds streams*chunks entries.  Returns the number of launches.
+    // One-shot stream (IFTA init, seed_random_phase): jump (when needed) +
+    // chunked seed; `seeds` are engine seeds (already forked), `states` holds
+    // streams*chunks entries.  Returns the number of launches.
     int launch(SeedArgs sa, const uint64_t* seeds, MtState* states, int streams, cudaStream_t st) const {
         int n = 0;
         if (jumps()) {
-            JumpArgs ja{seeds, polys.p, states, chunks, c_first()};
+            JumpArgs ja{seeds, nullptr, polys.p, (size_t)kPolyWords, states, chunks, c_first(), c_first()};
             k_mt_jump<<<streams * (chunks - c_first()), kJumpThreads, 0, st>>>(ja);
             ++n;
         }
@@ -179,6 +180,40 @@ struct SeedChunks {
         sa.chunk_len = len;
         k_seed_random_phase<<<streams * chunks, kSeedThreads, kSeedSmem, st>>>(sa);
         return n + 1;
+    }
+
+    // Continued stream (OSPR: subframe n draws [(n-1)*npix, n*npix)).  With
+    // chunks > 1, states[] holds each chunk's start window; subframe 1 jumps
+    // from the seeds, later subframes move every start window by npix draws
+    // in place (one polynomial, x^(npix-1)).
+    DBuf<uint64_t> step;
+    void plan_stream(size_t npix, int streams) {
+        plan(npix, streams, 0);
+        step.reset();
+        if (chunks > 1) {
+            step.alloc(kPolyWords);
+            std::vector<uint64_t> g(kPolyWords);
+            mt_jump_poly(npix - 1, g.data());
+            CK(cudaMemcpy(step.p, g.data(), sizeof(uint64_t) * kPolyWords, cudaMemcpyHostToDevice));
+        }
+    }
+    int launch_stream(SeedArgs sa, const uint64_t* seeds, MtState* states, int streams, bool first,
+                      cudaStream_t st) const {
+        sa.states = states;
+        if (chunks == 1) {
+            sa.seeds = first ? seeds : nullptr;
+            k_seed_random_phase<<<streams, kSeedThreads, kSeedSmem, st>>>(sa);
+            return 1;
+        }
+        JumpArgs ja = first ? JumpArgs{seeds, nullptr, polys.p, (size_t)kPolyWords, states, chunks, 0, 1}
+                            : JumpArgs{nullptr, states, step.p, 0, states, chunks, 0, 0};
+        k_mt_jump<<<streams * chunks, kJumpThreads, 0, st>>>(ja);
+        sa.seeds = nullptr;
+        sa.chunks = chunks;
+        sa.chunk_len = len;
+        sa.no_save = 1;
+        k_seed_random_phase<<<streams * chunks, kSeedThreads, kSeedSmem, st>>>(sa);
+        return 2;
     }
 };
 
@@ -1061,6 +1096,7 @@ struct hgc_ospr_plan {
     DBuf<uint16_t> lv16;
     DBuf<MtState> mt;
     DBuf<uint64_t> seeds;
+    SeedChunks chunking;
     const float2* tw = nullptr;
     cudaGraphExec_t graph = nullptr;
     uint64_t graph_sig = 0;
@@ -1166,7 +1202,7 @@ struct hgc_ospr_plan {
         }
         for (int n = 1; n <= N; ++n) {
             if (ov && n >= 3) CK(cudaStreamWaitEvent(ss, ev_pass[n & 1], 0));  // buffer n%2 free again
-            k_seed_random_phase<<<jobs, kSeedThreads, kSeedSmem, ss>>>(seed_args(n));
+            launches += chunking.launch_stream(seed_args(n), seeds.p, mt.p, jobs, n == 1, ss) - 1;
             CK(cudaGetLastError());
             if (ov) {
                 CK(cudaEventRecord(ev_seed, ss));
@@ -1240,7 +1276,8 @@ int hgc_ospr_plan_create(hgc_ospr_plan** out, const hgc_ospr_cfg* cfg, const hgc
         else p->lv8.alloc(lvtot);
         p->partials.alloc((size_t)cfg->subframes * jobs * p->tiles * 8);
         p->traces.alloc((size_t)cfg->subframes * jobs * 2);
-        p->mt.alloc(jobs);
+        p->chunking.plan_stream(p->npix, jobs);
+        p->mt.alloc((size_t)jobs * p->chunking.chunks);
         p->seeds.alloc(jobs);
         prepare_kernels(nx, ny);
         CK(cudaEventCreateWithFlags(&p->done, cudaEventDisableTiming));
@@ -1385,7 +1422,7 @@ int hgc_ospr_plan_profile(hgc_ospr_plan* p, int reps, double* ms_seed, double* m
         const int j = p->jobs;
         if (ms_seed)
             *ms_seed = time_launches(st, reps, [&] {
-                k_seed_random_phase<<<j, kSeedThreads, kSeedSmem, st>>>(p->seed_args(1));
+                p->chunking.launch_stream(p->seed_args(1), p->seeds.p, p->mt.p, j, false, st);
             });
         if (ms_col_inv) *ms_col_inv = time_launches(st, reps, [&] { col_plain(p->ny, p->col_inv_args(1), j, st); });
         if (ms_row) *ms_row = time_launches(st, reps, [&] { row_fused(p->nx, p->row_args(1), j, st); });

@@ -146,34 +146,40 @@ struct SeedArgs {
     // is given.  chunks <= 1: one CTA per stream over all npix draws.
     int chunks;
     size_t chunk_len;
+    int no_save;  // keep states[] (the chunk start windows) instead of saving the end state
 };
 
-// Jump-ahead (mtjump.cpp): CTA (stream s, chunk c) writes states[s*chunks + c]
-// = the engine seeded with seeds[s] advanced by offset0 + c*len draws, as the
-// window g(F) W_1 with g = polys[c - c_first] (x^(offset0 + c*len - 1) mod P):
-// word j = XOR over set bits i of g of raw word x_{1+i+j}.  The raw words are
+// Jump-ahead (mtjump.cpp): CTA (stream s, chunk c), c in [c_lo, chunks),
+// writes states[s*chunks + c] = its start window advanced by J draws, as
+// g(F) W_1 with g = x^(J-1) mod P: word j = XOR over set bits i of g of raw
+// word x_{1+i+j}, x_0.. being the start window (the fresh seed block when
+// `from` is null, else from[s*chunks + c], a pos = 312 window; may alias
+// states).  g = polys + (c - poly_base) * poly_stride; chunks c < poly_base
+// are not moved (the seed block is stored as is).  The raw words are
 // regenerated block by block (one warp twists block q+2 while the CTA
 // accumulates over bits [312q, 312q+312) from blocks q, q+1); each block is
 // stored twice (slots b%3 and b%3+3) so reads never wrap.
 constexpr int kJumpThreads = 320;
 constexpr int kPolyWords = 312;
 struct JumpArgs {
-    const uint64_t* seeds;  // [streams] engine seeds
-    const uint64_t* polys;  // [chunks - c_first][kPolyWords]
+    const uint64_t* seeds;  // [streams] engine seeds (from == nullptr)
+    const MtState* from;    // [streams * chunks] start windows, or nullptr
+    const uint64_t* polys;
+    size_t poly_stride;     // kPolyWords, or 0: one polynomial for every chunk
     MtState* states;        // [streams * chunks]
-    int chunks, c_first;
+    int chunks, c_lo, poly_base;
 };
 
 __global__ void __launch_bounds__(kJumpThreads) k_mt_jump(JumpArgs a) {
     __shared__ uint64_t ring[6 * kMtN];
     __shared__ uint64_t g[kPolyWords + 1];
-    const int per = a.chunks - a.c_first;
-    const int s = blockIdx.x / per, c = a.c_first + blockIdx.x % per;
+    const int per = a.chunks - a.c_lo;
+    const int s = blockIdx.x / per, c = a.c_lo + blockIdx.x % per;
+    const size_t b = (size_t)s * a.chunks + c;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint64_t* gp = a.polys + (size_t)(c - a.c_first) * kPolyWords;
-    for (int i = tid; i < kPolyWords; i += blockDim.x) g[i] = gp[i];
-    if (tid == 0) {
-        g[kPolyWords] = 0;
+    if (a.from) {
+        for (int i = tid; i < kMtN; i += blockDim.x) ring[i] = ring[3 * kMtN + i] = a.from[b].w[i];
+    } else if (tid == 0) {
         uint64_t x = a.seeds[s];  // std::mt19937_64::seed: block 0
         ring[0] = ring[3 * kMtN] = x;
         for (int i = 1; i < kMtN; ++i) {
@@ -181,6 +187,15 @@ __global__ void __launch_bounds__(kJumpThreads) k_mt_jump(JumpArgs a) {
             ring[i] = ring[3 * kMtN + i] = x;
         }
     }
+    if (c < a.poly_base) {  // offset 0: the seed block itself
+        __syncthreads();
+        for (int i = tid; i < kMtN; i += blockDim.x) a.states[b].w[i] = ring[i];
+        if (tid == 0) a.states[b].pos = kMtN;
+        return;
+    }
+    const uint64_t* gp = a.polys + (size_t)(c - a.poly_base) * a.poly_stride;
+    for (int i = tid; i < kPolyWords; i += blockDim.x) g[i] = gp[i];
+    if (tid == 0) g[kPolyWords] = 0;
     __syncthreads();
     if (warp == 0) {  // block 1
         mt_twist_warp(ring, ring + kMtN, lane);
@@ -215,8 +230,8 @@ __global__ void __launch_bounds__(kJumpThreads) k_mt_jump(JumpArgs a) {
         }
         __syncthreads();
     }
-    if (j < kMtN) a.states[(size_t)s * a.chunks + c].w[j] = acc;
-    if (tid == 0) a.states[(size_t)s * a.chunks + c].pos = kMtN;
+    if (j < kMtN) a.states[b].w[j] = acc;
+    if (tid == 0) a.states[b].pos = kMtN;
 }
 
 // One CTA per stream.  Warp 0 produces twists; warps 1.. consume.
@@ -313,6 +328,7 @@ __global__ void __launch_bounds__(kSeedThreads) k_seed_random_phase(SeedArgs a) 
         }
         __syncthreads();
     }
+    if (a.no_save) return;
     // save the block holding the next draw
     const uint64_t* keep;
     int pos;

@@ -89,3 +89,17 @@ def test_ospr_validation():
         hg.run_adaptive_ospr(ocfg(amp, 3, 1, adaptive=True, gain=1.5))
     with pytest.raises(ValueError, match="variant mismatch"):
         hg.run_adaptive_ospr(ocfg(amp, 3, 1))
+
+
+@pytest.mark.parametrize("adaptive", [False, True])
+def test_ospr_chunked_stream_matches_oracle(oracle, monkeypatch, adaptive):
+    """Each subframe's draws split across 5 CTAs; the chunk start states move
+    by npix draws per subframe (k_mt_jump in place).  Same levels as the
+    sequential stream (ospr.hpp:89, :118)."""
+    monkeypatch.setenv("HG_SEED_CHUNKS", "5")
+    amp = hg.patterns.bench_target(64)
+    N = 5
+    run = (hg.run_adaptive_ospr if adaptive else hg.run_ospr)(ocfg(amp, N, 17, adaptive=adaptive, gain=0.7))
+    ref = oracle.ospr(amp, hg.SlmSpec.binary_phase(), N, seed=17, adaptive=adaptive, gain=0.7)
+    assert level_mismatches(run.set.levels, ref.levels).sum() <= 2 * N
+    assert np.max(np.abs(run.report.trace.values() - ref.cumulative_mse) / ref.cumulative_mse) < 1e-3

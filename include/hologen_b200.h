@@ -201,6 +201,27 @@ int hgc_ospr_plan_profile(hgc_ospr_plan* plan, int reps, double* ms_seed, double
                           double* ms_col_acc);
 int hgc_ospr_plan_destroy(hgc_ospr_plan* plan);
 
+/* Subframe-block sharding of ONE plain OSPR job across ranks (
+ * the loop of run_ospr_impl, ospr.hpp:105-147, split at subframe
+ * boundaries).  The plan computes global subframes [first, first + count) of
+ * the cfg->subframes-frame job: its random-phase stream starts first*npix
+ * draws into Rng(seed).fork(0) (ospr.hpp:89, :118) by jump-ahead, so frames,
+ * levels and frame MSEs are those of the unsharded run.  Upload / execute /
+ * download as for hgc_ospr_plan_* with jobs = 1; traces/levels hold the
+ * block's `count` frames.  Adaptive OSPR is sequential: HGC_EUNSUPPORTED.
+ *
+ * Exchange: hgc_ospr_block_sum gives this block's intensity sum B (float
+ * device buffer, `count` elements, plan layout) after execute; all-gather the
+ * B of every block in block order into one device buffer [nblocks][count]
+ * (e.g. ncclAllGather), then hgc_ospr_block_finish computes the block's
+ * cumulative MSEs (ospr.hpp:142-145) from the prefix of the earlier blocks
+ * and sets the intensity to the job total (mean_intensity / replay of the
+ * whole job on download). */
+int hgc_ospr_block_plan_create(hgc_ospr_plan** plan, const hgc_ospr_cfg* cfg, const hgc_slm* slm, int nx, int ny,
+                               int first, int count);
+int hgc_ospr_block_sum(hgc_ospr_plan* plan, void** dev_ptr, size_t* count);
+int hgc_ospr_block_finish(hgc_ospr_plan* plan, const void* gathered, int nblocks, int index, void* stream);
+
 /* ------------------------------------------------------- primitives */
 /* Unitary 2-D DFT of `batch` fields, sign -1 forward / +1 inverse; in == out allowed. */
 int hgc_fft2d(int nx, int ny, int sign, int batch, const float* in, float* out);

@@ -7,7 +7,7 @@ mirrored in Python.  Importing requires the in-tree libhologen_b200.so; there
 is no CPU fallback.
 """
 from ._lib import HgcError, HgcUnsupported, exported_symbols
-from .api import (IftaPlan, OsprPlan, Propagator, Quantiser, allowed_states_f32, device_count, fft_forward,
+from .api import (IftaPlan, OsprBlockPlan, OsprPlan, Propagator, Quantiser, allowed_states_f32, device_count, fft_forward,
                   fft_inverse, fork_seed, fresnel_forward, fresnel_inverse, make_fresnel_phase, mse, quantise_field,
                   run_adaptive_ospr, run_gs, run_ifta, run_ifta_batch, run_liu_taghizadeh, run_ospr, run_ospr_batch,
                   run_ospr_variant, run_weighted_gs, seed_random_phase, set_device, subframe_mse_statistic,
@@ -15,6 +15,6 @@ from .api import (IftaPlan, OsprPlan, Propagator, Quantiser, allowed_states_f32,
 from .types import (PI, TWO_PI, Freedoms, FresnelParams, IftaConfig, IftaVariant, InitPhase, MetricConfig,
                     MetricTrace, Normalization, OsprConfig, OsprRun, OsprVariant, PhaseProfile, RunReport, SlmMode,
                     SlmSpec, SubframeSet, TargetSpec, allowed_states, lt_area_fractions, normalize_image)
-from . import patterns
+from . import patterns, shard
 
 __version__ = "0.1.0"

@@ -98,6 +98,9 @@ _SIGS = {
     "hgc_ospr_plan_device_ptrs": (_i, [_vp, _P(_vp), _P(_vp), _P(_vp)]),
     "hgc_ospr_plan_launches": (_i, [_vp]),
     "hgc_ospr_plan_profile": (_i, [_vp, _i, _P(_d), _P(_d), _P(_d), _P(_d)]),
+    "hgc_ospr_block_plan_create": (_i, [_P(_vp), _P(HgcOsprCfg), _P(HgcSlm), _i, _i, _i, _i]),
+    "hgc_ospr_block_sum": (_i, [_vp, _P(_vp), _P(C.c_size_t)]),
+    "hgc_ospr_block_finish": (_i, [_vp, _vp, _i, _i, _vp]),
     "hgc_ospr_plan_destroy": (_i, [_vp]),
     "hgc_fft2d": (_i, [_i, _i, _i, _i, _vp, _vp]),
     "hgc_propagate": (_i, [_i, _i, _i, _P(HgcFresnel), _i, _vp, _vp]),

@@ -527,6 +527,7 @@ class OsprPlan:
     def __init__(self, cfg: OsprConfig, nx: int, ny: int, jobs: int, per_job_target: bool = False):
         cfg.slm.validate()
         self.cfg, self.nx, self.ny, self.jobs, self.per_job = cfg, nx, ny, jobs, per_job_target
+        self._nf = cfg.subframes
         self._keep = []
         self._c = _ospr_cfg(cfg)
         self._slm = _slm(cfg.slm, self._keep)
@@ -550,7 +551,7 @@ class OsprPlan:
         check(lib.hgc_ospr_plan_execute(self._h, stream))
 
     def download(self, frames: bool = False):
-        N = self.cfg.subframes
+        N = self._nf
         jobs, ny, nx = self.jobs, self.ny, self.nx
         wide = self.cfg.slm.levels > 256
         out = {"levels": np.empty((jobs, N, ny, nx), np.uint16 if wide else np.uint8),
@@ -581,7 +582,7 @@ class OsprPlan:
     def device_arrays(self):
         lv, tr, S = C.c_void_p(), C.c_void_p(), C.c_void_p()
         check(lib.hgc_ospr_plan_device_ptrs(self._h, C.byref(lv), C.byref(tr), C.byref(S)))
-        N = self.cfg.subframes
+        N = self._nf
         lt = "<u2" if self.cfg.slm.levels > 256 else "|u1"
         return (_CudaArray(lv.value, (self.jobs, N, self.ny, self.nx), lt),
                 _CudaArray(tr.value, (self.jobs, N, 2), "<f8"),
@@ -594,6 +595,34 @@ class OsprPlan:
 
     def __del__(self):
         self.close()
+
+
+class OsprBlockPlan(OsprPlan):
+    """Global subframes [first, first + count) of ONE plain OSPR job (SURVEY
+    §8 e2): the stream starts first*npix draws into Rng(seed).fork(0) by
+    jump-ahead.  After execute, all-gather every block's ``block_sum()`` in
+    block order and call ``finish`` to get the cumulative MSEs and the job's
+    mean intensity (hgc_ospr_block_*)."""
+
+    def __init__(self, cfg: OsprConfig, nx: int, ny: int, first: int, count: int):
+        cfg.slm.validate()
+        self.cfg, self.nx, self.ny, self.jobs, self.per_job = cfg, nx, ny, 1, False
+        self.first, self.count, self._nf = first, count, count
+        self._keep = []
+        self._c = _ospr_cfg(cfg)
+        self._slm = _slm(cfg.slm, self._keep)
+        h = C.c_void_p()
+        check(lib.hgc_ospr_block_plan_create(C.byref(h), C.byref(self._c), C.byref(self._slm), nx, ny, first, count))
+        self._h = h
+        self._io = None
+
+    def block_sum(self) -> "_CudaArray":
+        ptr, n = C.c_void_p(), C.c_size_t()
+        check(lib.hgc_ospr_block_sum(self._h, C.byref(ptr), C.byref(n)))
+        return _CudaArray(ptr.value, (n.value,), "<f4")
+
+    def finish(self, gathered_ptr: int, nblocks: int, index: int, stream: int | None = None):
+        check(lib.hgc_ospr_block_finish(self._h, gathered_ptr, nblocks, index, stream))
 
 
 def device_count() -> int:

@@ -187,8 +187,8 @@ struct SeedChunks {
     // from the seeds, later subframes move every start window by npix draws
     // in place (one polynomial, x^(npix-1)).
     DBuf<uint64_t> step;
-    void plan_stream(size_t npix, int streams) {
-        plan(npix, streams, 0);
+    void plan_stream(size_t npix, int streams, uint64_t offset = 0) {
+        plan(npix, streams, offset);
         step.reset();
         if (chunks > 1) {
             step.alloc(kPolyWords);
@@ -201,11 +201,17 @@ struct SeedChunks {
                       cudaStream_t st) const {
         sa.states = states;
         if (chunks == 1) {
-            sa.seeds = first ? seeds : nullptr;
+            int n = 0;
+            if (first && offset0 > 0) {  // stream starts offset0 draws in (subframe block)
+                JumpArgs ja{seeds, nullptr, polys.p, (size_t)kPolyWords, states, 1, 0, 0};
+                k_mt_jump<<<streams, kJumpThreads, 0, st>>>(ja);
+                ++n;
+            }
+            sa.seeds = first && offset0 == 0 ? seeds : nullptr;
             k_seed_random_phase<<<streams, kSeedThreads, kSeedSmem, st>>>(sa);
-            return 1;
+            return n + 1;
         }
-        JumpArgs ja = first ? JumpArgs{seeds, nullptr, polys.p, (size_t)kPolyWords, states, chunks, 0, 1}
+        JumpArgs ja = first ? JumpArgs{seeds, nullptr, polys.p, (size_t)kPolyWords, states, chunks, 0, c_first()}
                             : JumpArgs{nullptr, states, step.p, 0, states, chunks, 0, 0};
         k_mt_jump<<<streams * chunks, kJumpThreads, 0, st>>>(ja);
         sa.seeds = nullptr;
@@ -367,6 +373,39 @@ __global__ void k_finalize(const double* part, int slots, int targets, int tiles
             }
         }
     }
+}
+
+// Subframe-block OSPR, after the all-gather of every block's
+// intensity sum: cumulative-MSE partials of local frame n (global frame
+// first+n+1) from S = (sum of the earlier blocks) + local snapshot n, with the
+// per-pixel float math of COL_OSPR (passes.cuh; ospr.hpp:134-145).  Frame-0
+// CTAs also store the job total into S (mean intensity, ospr.hpp:149-156).
+__global__ void __launch_bounds__(256) k_ospr_block_cum(const float* gathered, int index, int nblocks,
+                                                        const float* snaps, const float* target, const uint8_t* roi,
+                                                        size_t npix, int first, float* S, double* partials) {
+    const int n = blockIdx.y;
+    const float inv_n = 1.0f / (float)(first + n + 1);
+    float acc[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    const float* sn = snaps + (size_t)n * npix;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < npix; i += (size_t)gridDim.x * blockDim.x) {
+        float pre = 0.f;
+        for (int h = 0; h < index; ++h) pre += gathered[(size_t)h * npix + i];
+        const float sv = pre + sn[i];
+        const float m = (!roi || roi[i]) ? 1.f : 0.f;
+        const float amp = target[i] * m;
+        const float rc = sqrtf(sv * inv_n) * m;
+        const float dc = amp - rc;
+        acc[3] = fmaf(amp, amp, acc[3]);
+        acc[4] = fmaf(dc, dc, acc[4]);
+        acc[5] = fmaf(amp, rc, acc[5]);
+        acc[6] = fmaf(rc, rc, acc[6]);
+        if (n == 0) {
+            float tot = pre;
+            for (int h = index; h < nblocks; ++h) tot += gathered[(size_t)h * npix + i];
+            S[i] = tot;
+        }
+    }
+    block_sum_float_store<7>(acc, partials + ((size_t)n * gridDim.x + blockIdx.x) * 8);
 }
 
 // TargetSpec::validate on the device (target.hpp:52-73): bit 0 = non-finite
@@ -1097,6 +1136,13 @@ struct hgc_ospr_plan {
     DBuf<MtState> mt;
     DBuf<uint64_t> seeds;
     SeedChunks chunking;
+    // subframe-block mode: this plan runs global subframes
+    // [first, first + cfg.subframes) of a total_subframes job
+    int first = 0, total_subframes = 0;
+    bool block_mode = false;
+    DBuf<float> snaps;            // [cfg.subframes][npix] local S after each frame
+    DBuf<double> cum_part, cum_tr;
+    int cum_tiles = 0;
     const float2* tw = nullptr;
     cudaGraphExec_t graph = nullptr;
     uint64_t graph_sig = 0;
@@ -1211,6 +1257,9 @@ struct hgc_ospr_plan {
             col_plain(ny, col_inv_args(n), jobs, st);
             row_fused(nx, row_args(n), jobs, st);
             col_ospr(ny, col_acc_args(n), jobs, st);
+            if (block_mode)  // local running sum after frame n, for hgc_ospr_block_finish
+                CK(cudaMemcpyAsync(snaps.p + (size_t)(n - 1) * npix, S.p, sizeof(float) * npix, cudaMemcpyDeviceToDevice,
+                                   st));
             if (ov) CK(cudaEventRecord(ev_pass[n & 1], st));
             launches += 4;
         }
@@ -1233,12 +1282,21 @@ static void validate_ospr_cfg(const hgc_ospr_cfg* c) {  // OsprConfig::validate,
     if (c->variant < 0 || c->variant > 1) invalid("OsprConfig: unknown variant");
 }
 
-int hgc_ospr_plan_create(hgc_ospr_plan** out, const hgc_ospr_cfg* cfg, const hgc_slm* slm, int nx, int ny, int jobs,
-                         int per_job_target) {
-    return guarded([&] {
+static void create_ospr_plan(hgc_ospr_plan** out, const hgc_ospr_cfg* cfg_in, const hgc_slm* slm, int nx, int ny,
+                             int jobs, int per_job_target, int first, int count) {
         if (!out) invalid("hgc_ospr_plan_create: null plan pointer");
         *out = nullptr;
-        validate_ospr_cfg(cfg);
+        validate_ospr_cfg(cfg_in);
+        const bool block = count > 0;
+        if (block) {
+            if (cfg_in->variant != 0)
+                fail(HGC_EUNSUPPORTED, "hgc_ospr_block_plan_create: adaptive OSPR is sequential (replicas only)");
+            if (first < 0 || first + count > cfg_in->subframes)
+                invalid("hgc_ospr_block_plan_create: subframe block outside [0, subframes)");
+        }
+        hgc_ospr_cfg cfg_local = *cfg_in;
+        if (block) cfg_local.subframes = count;
+        const hgc_ospr_cfg* cfg = &cfg_local;
         if (nx <= 0 || ny <= 0) invalid("ComplexField: dimensions must be positive");
         validate_slm(slm, (size_t)nx * ny);
         if (jobs < 1) invalid("hgc_ospr_plan_create: jobs must be >= 1");
@@ -1276,13 +1334,65 @@ int hgc_ospr_plan_create(hgc_ospr_plan** out, const hgc_ospr_cfg* cfg, const hgc
         else p->lv8.alloc(lvtot);
         p->partials.alloc((size_t)cfg->subframes * jobs * p->tiles * 8);
         p->traces.alloc((size_t)cfg->subframes * jobs * 2);
-        p->chunking.plan_stream(p->npix, jobs);
+        p->first = block ? first : 0;
+        p->total_subframes = cfg_in->subframes;
+        p->block_mode = block;
+        if (block) {
+            p->snaps.alloc((size_t)count * p->npix);
+            p->cum_tiles = std::min<int>(148 * 4, (int)((p->npix + 255) / 256));
+            p->cum_part.alloc((size_t)count * p->cum_tiles * 8);
+            p->cum_tr.alloc((size_t)count * 2);
+        }
+        p->chunking.plan_stream(p->npix, jobs, (uint64_t)p->first * p->npix);
         p->mt.alloc((size_t)jobs * p->chunking.chunks);
         p->seeds.alloc(jobs);
         prepare_kernels(nx, ny);
         CK(cudaEventCreateWithFlags(&p->done, cudaEventDisableTiming));
         CK(cudaStreamSynchronize(p->stream));
         *out = p.release();
+}
+
+int hgc_ospr_plan_create(hgc_ospr_plan** out, const hgc_ospr_cfg* cfg, const hgc_slm* slm, int nx, int ny, int jobs,
+                         int per_job_target) {
+    return guarded([&] { create_ospr_plan(out, cfg, slm, nx, ny, jobs, per_job_target, 0, 0); });
+}
+
+int hgc_ospr_block_plan_create(hgc_ospr_plan** out, const hgc_ospr_cfg* cfg, const hgc_slm* slm, int nx, int ny,
+                               int first, int count) {
+    return guarded([&] {
+        if (count < 1) invalid("hgc_ospr_block_plan_create: count must be >= 1");
+        create_ospr_plan(out, cfg, slm, nx, ny, 1, 0, first, count);
+    });
+}
+
+int hgc_ospr_block_sum(hgc_ospr_plan* p, void** dev_ptr, size_t* count) {
+    return guarded([&] {
+        if (!p || !p->block_mode) invalid("hgc_ospr_block_sum: not a subframe-block plan");
+        if (dev_ptr) *dev_ptr = p->S.p;
+        if (count) *count = p->npix;
+    });
+}
+
+int hgc_ospr_block_finish(hgc_ospr_plan* p, const void* gathered, int nblocks, int index, void* stream) {
+    return guarded([&] {
+        if (!p || !p->block_mode) invalid("hgc_ospr_block_finish: not a subframe-block plan");
+        if (!gathered || nblocks < 1 || index < 0 || index >= nblocks)
+            invalid("hgc_ospr_block_finish: bad gathered buffer / block index");
+        CK(cudaSetDevice(p->device));
+        cudaStream_t st = stream ? (cudaStream_t)stream : p->stream;
+        CK(cudaStreamWaitEvent(st, p->done, 0));
+        const int K = p->cfg.subframes;
+        dim3 grid(p->cum_tiles, K);
+        k_ospr_block_cum<<<grid, 256, 0, st>>>((const float*)gathered, index, nblocks, p->snaps.p, p->target_f.p,
+                                               p->has_roi ? p->roi.p : nullptr, p->npix, p->first, p->S.p,
+                                               p->cum_part.p);
+        k_finalize<<<1, 32, 0, st>>>(p->cum_part.p, K, 1, p->cum_tiles, (double)p->M, p->cfg.freedom_scale, 1,
+                                      p->cum_tr.p);
+        // cumulative entries (odd slots) replace the block-local ones
+        CK(cudaMemcpy2DAsync(p->traces.p + 1, 2 * sizeof(double), p->cum_tr.p + 1, 2 * sizeof(double), sizeof(double),
+                             K, cudaMemcpyDeviceToDevice, st));
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(p->done, st));
     });
 }
 
@@ -1369,7 +1479,7 @@ int hgc_ospr_plan_download(hgc_ospr_plan* p, hgc_ospr_io* io) {
             for (size_t i = 0; i < tot; ++i) {  // S is column-pair major per job
                 const size_t j = i / npix, pi = i % npix;
                 const int px = (int)(pi % p->nx), py = (int)(pi / p->nx);
-                double m = (double)S[j * npix + colpair_index(px, py, p->ny)] / N;
+                double m = (double)S[j * npix + colpair_index(px, py, p->ny)] / p->total_subframes;
                 if (io->mean_intensity) io->mean_intensity[i] = m;
                 if (io->replay) {
                     io->replay[2 * i] = (float)std::sqrt(m);

@@ -107,3 +107,16 @@ def test_mt_jump_state_matches_sequential_stream(oracle, draws):
     nxt = _mt_next(w, 8)
     want = oracle.mt_draws(es, 8, skip=draws)
     np.testing.assert_array_equal(nxt, want)
+
+
+def test_ospr_block_plan_validation():
+    """Subframe-block plans reject adaptive OSPR (sequential:
+    replicas only) and blocks outside the job before touching a device."""
+    amp = hg.patterns.bench_target(32)
+    base = dict(subframes=4, slm=hg.SlmSpec.binary_phase(), target=hg.TargetSpec(amp), seed=1)
+    with pytest.raises(hg.HgcUnsupported, match="sequential"):
+        hg.OsprBlockPlan(hg.OsprConfig(variant=hg.OsprVariant.AdaptiveOspr, **base), 32, 32, 0, 2)
+    with pytest.raises(ValueError, match="outside"):
+        hg.OsprBlockPlan(hg.OsprConfig(**base), 32, 32, 3, 2)
+    with pytest.raises(ValueError, match="count"):
+        hg.OsprBlockPlan(hg.OsprConfig(**base), 32, 32, 0, 0)

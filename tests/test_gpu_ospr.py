@@ -103,3 +103,51 @@ def test_ospr_chunked_stream_matches_oracle(oracle, monkeypatch, adaptive):
     ref = oracle.ospr(amp, hg.SlmSpec.binary_phase(), N, seed=17, adaptive=adaptive, gain=0.7)
     assert level_mismatches(run.set.levels, ref.levels).sum() <= 2 * N
     assert np.max(np.abs(run.report.trace.values() - ref.cumulative_mse) / ref.cumulative_mse) < 1e-3
+
+
+def _block_run(cfg, amp, G):
+    """Subframe-block sharding with G blocks on one GPU: the
+    all-gather is a stack of the block sums (the GPU ranks use NCCL)."""
+    import torch
+    ny, nx = amp.shape
+    N = cfg.subframes
+    plans = []
+    for g in range(G):
+        first, count = hg.shard.shard_range(N, G, g)
+        p = hg.OsprBlockPlan(cfg, nx, ny, first, count)
+        p.upload(amp)
+        p.execute()
+        plans.append(p)
+    torch.cuda.synchronize()
+    gathered = torch.stack([torch.as_tensor(p.block_sum(), device="cuda") for p in plans]).contiguous()
+    outs = []
+    for g, p in enumerate(plans):
+        p.finish(gathered.data_ptr(), G, g)
+        outs.append(p.download())
+    return outs
+
+
+@pytest.mark.parametrize("n,N,G", [(64, 7, 1), (64, 7, 3), (256, 8, 4), (1024, 24, 8)])
+def test_ospr_subframe_blocks_match_unsharded(oracle, n, N, G):
+    amp = hg.patterns.bench_target(n)
+    cfg = ocfg(amp, N, 1)
+    outs = _block_run(cfg, amp, G)
+    levels = np.concatenate([o["levels"][0] for o in outs])
+    fm = np.concatenate([o["frame_mse"][0] for o in outs])
+    cm = np.concatenate([o["cumulative_mse"][0] for o in outs])
+    ref = oracle.ospr(amp, hg.SlmSpec.binary_phase(), N, seed=1)
+    assert level_mismatches(levels, ref.levels).sum() <= N
+    assert np.max(np.abs(fm - ref.frame_mse) / ref.frame_mse) < 1e-4
+    assert np.max(np.abs(cm - ref.cumulative_mse) / ref.cumulative_mse) < 1e-4
+    for o in outs:  # every block holds the job's mean intensity after finish
+        assert np.allclose(o["mean_intensity"][0], ref.mean_intensity, rtol=1e-4, atol=1e-7)
+
+
+def test_ospr_sharded_driver_world1(oracle):
+    """shard.run_ospr_sharded end to end at world size 1 (no process group)."""
+    amp = hg.patterns.bench_target(128)
+    cfg = ocfg(amp, 6, 3)
+    out = hg.shard.run_ospr_sharded(cfg, None, 1, 0)
+    ref = oracle.ospr(amp, hg.SlmSpec.binary_phase(), 6, seed=3)
+    assert level_mismatches(out["levels"], ref.levels).sum() <= 6
+    assert np.max(np.abs(out["cumulative_mse"] - ref.cumulative_mse) / ref.cumulative_mse) < 1e-4

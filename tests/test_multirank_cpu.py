@@ -71,3 +71,55 @@ def test_two_rank_gather_matches_single_process():
         assert p.exitcode == 0
     want = _final_errors(unit_seeds(0, TOTAL))
     assert np.array_equal(got, want)
+
+
+# ---- one OSPR job split into subframe blocks (world size 2, gloo)
+OSPR_N, OSPR_NPX = 5, 32
+
+
+def _ospr_block_worker(rank, world, port, q):
+    """Each rank owns subframes shard_range(N, world, rank) of one job, forms
+    its block intensity sum B_g, all-gathers B (the only exchange), and
+    finishes its cumulative MSEs from the prefix of earlier blocks — the
+    protocol of shard.run_ospr_sharded / hgc_ospr_block_finish, with the
+    oracle's frames standing in for the GPU block."""
+    from pyoracle import Oracle
+    from paper_2008_12214_b200.types import SlmSpec
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    o = Oracle("restatement")
+    amp = patterns.bench_target(OSPR_NPX)
+    full = o.ospr(amp, SlmSpec.binary_phase(), OSPR_N, seed=1, keep_frames=True)
+    first, count = shard_range(OSPR_N, world, rank)
+    inten = [np.abs(o.fft2(full.frames[k], -1)).astype(np.float64) ** 2 for k in range(first, first + count)]
+    snaps = np.cumsum(np.array(inten), axis=0)  # local running sums after each block frame
+    B = torch.tensor(snaps[-1].ravel())
+    gathered = [torch.empty_like(B) for _ in range(world)]
+    dist.all_gather(gathered, B)
+    prefix = sum((gathered[h].numpy() for h in range(rank)), np.zeros_like(B.numpy())).reshape(amp.shape)
+    cum = np.array([o.mse(amp, np.sqrt((prefix + snaps[k]) / (first + k + 1)).astype(np.complex64))
+                    for k in range(count)])
+    pad = np.zeros(shard_range(OSPR_N, world, 0)[1])
+    pad[:count] = cum
+    got = gather_to_root(torch.tensor(pad), dist, world, rank)
+    if rank == 0:
+        parts = got.numpy().reshape(world, -1)
+        q.put((np.concatenate([parts[g, :shard_range(OSPR_N, world, g)[1]] for g in range(world)]),
+               full.cumulative_mse))
+    dist.destroy_process_group()
+
+
+def test_two_rank_ospr_subframe_blocks_match_single_process():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ospr_block_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got, want = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert got.shape == want.shape
+    assert np.max(np.abs(got - want) / want) < 1e-5

@@ -314,6 +314,55 @@ def ospr_ours(args, d: Dist):
     return res
 
 
+def ospr_single_job(args, d: Dist):
+    """ONE config-3 OSPR job (1024^2 binary, 24 subframes, seed 1) split into
+    subframe blocks over the ranks (SURVEY §8 e2, strong scaling): per step
+    each rank runs its block (jump-ahead stream start, chunked seeds), one
+    NCCL all-gather of the block intensity sums, then its cumulative-MSE
+    finish.  Device time per job, max over ranks."""
+    import torch
+    import paper_2008_12214_b200 as hg
+    from paper_2008_12214_b200.shard import shard_range
+    n, N = args.ospr_n, args.ospr_subframes
+    amp = hg.patterns.bench_target(n)
+    cfg = hg.OsprConfig(subframes=N, slm=hg.SlmSpec.binary_phase(), target=hg.TargetSpec(amp), seed=1)
+    first, count = shard_range(N, d.world, d.rank)
+    plan = hg.OsprBlockPlan(cfg, n, n, first, count)
+    plan.upload(amp)
+    st = torch.cuda.Stream()
+    B = torch.as_tensor(plan.block_sum(), device="cuda")
+    gathered = torch.empty((d.world, B.numel()), dtype=torch.float32, device="cuda")
+
+    def job():
+        plan.execute(st.cuda_stream)
+        if d.pg:
+            d.pg.all_gather_into_tensor(gathered, B)
+        else:
+            gathered[0].copy_(B)
+        plan.finish(gathered.data_ptr(), d.world, d.rank, st.cuda_stream)
+
+    with torch.cuda.stream(st):
+        for _ in range(max(3, args.warmup)):
+            job()
+        torch.cuda.synchronize()
+        d.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 10
+        e0.record(st)
+        for _ in range(reps):
+            job()
+        e1.record(st)
+        torch.cuda.synchronize()
+    ms = d.max(e0.elapsed_time(e1) / reps)
+    out = plan.download()
+    plan.close()
+    return {"metric": "OSPR single-job latency", "ms_per_job": ms, "subframes_per_s": N / (ms / 1e3),
+            "unit": "ms", "scaling": "strong", "n_gpus": d.world,
+            "config": {"workload": f"ospr_{n}_binary single job (BASELINE config 3)", "subframes": N, "seed": 1,
+                       "split": "contiguous subframe blocks per rank, one all-gather of npix fp32 block sums"},
+            "final_error": float(out["final_error"][0]) if d.world == 1 else None}
+
+
 # ---------------------------------------------------- reference CPU path
 def reference_gs(n, levels, iters, jobs, threads):
     """The reference's own run_ifta<float> (oracle/_ref: unmodified headers,
@@ -393,6 +442,7 @@ def main():
     peak, peak_kind = peaks()
     gs = gs_ours(args, d)
     osp = None if args.no_ospr else ospr_ours(args, d)
+    single = None if args.no_ospr else ospr_single_job(args, d)
     cpu = None
     if d.rank == 0 and d.world == 1 and not args.no_cpu:
         threads = cpu_threads()
@@ -458,6 +508,8 @@ def main():
                         "e2e": osp.get("e2e")}
         if cpu and "ospr" in cpu:
             line["ospr"]["cpu_baseline"] = cpu.pop("ospr")
+        if single is not None:
+            line["ospr"]["single_job"] = single
         line["gpu_launches"] += osp["launches"]
     print(json.dumps(line), flush=True)
     d.close()

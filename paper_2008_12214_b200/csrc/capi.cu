@@ -141,36 +141,57 @@ struct SeedChunks {
     int chunks = 1;
     size_t len = 0;
     uint64_t offset0 = 0;
-    DBuf<uint64_t> polys;
+    DBuf<int> starts;       // jump polynomials as set-bit offsets (mt_poly_offsets)
+    DBuf<uint16_t> pool;
 
-    void plan(size_t npix, int streams, uint64_t offset = 0) {
+    static void upload_offsets(const uint64_t* polys, int n, DBuf<int>& st, DBuf<uint16_t>& pl) {
+        std::vector<int> s;
+        std::vector<uint16_t> p;
+        mt_poly_offsets(polys, n, s, p);
+        st.alloc(s.size());
+        pl.alloc(std::max<size_t>(p.size(), 1));
+        CK(cudaMemcpy(st.p, s.data(), sizeof(int) * s.size(), cudaMemcpyHostToDevice));
+        if (!p.empty()) CK(cudaMemcpy(pl.p, p.data(), sizeof(uint16_t) * p.size(), cudaMemcpyHostToDevice));
+    }
+
+    void plan(size_t npix, int streams, uint64_t offset = 0, int ctas_per_sm = 2) {
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        long long c = (2LL * sms + streams - 1) / std::max(1, streams);
-        c = std::min<long long>(c, std::max<size_t>(1, npix / kMinChunkDraws));
+        // enough chunks to fill every slot; among up to 4x that, the count
+        // whose last wave is fullest (ties: fewer chunks, fewer jumps)
+        const long long slots = (long long)ctas_per_sm * sms, S = std::max(1, streams);
+        const long long cmax = std::max<long long>(1, (long long)(npix / kMinChunkDraws));
+        long long c = std::min((slots + S - 1) / S, cmax);
+        double best = 0.0;
+        for (long long k = c, hi = std::min(4 * c, cmax); k <= hi; ++k) {
+            const long long ctas = S * k, waves = (ctas + slots - 1) / slots;
+            const double eff = (double)ctas / (double)(waves * slots);
+            if (eff > best + 0.02) best = eff, c = k;
+        }
         if (const char* ev = getenv("HG_SEED_CHUNKS")) c = std::max(1, atoi(ev));  // tuning / tests
         c = std::min<long long>(c, (long long)std::max<size_t>(1, npix));
         c = std::max<long long>(1, std::min<long long>(c, kMaxChunks));
         len = (npix + c - 1) / c;
         chunks = (int)((npix + len - 1) / len);
         offset0 = offset;
-        polys.reset();
+        starts.reset();
+        pool.reset();
         if (jumps()) {
             const std::vector<uint64_t>& v = mt_chunk_polys(offset0, len, chunks);
-            polys.alloc(v.size());
-            CK(cudaMemcpy(polys.p, v.data(), sizeof(uint64_t) * v.size(), cudaMemcpyHostToDevice));
+            upload_offsets(v.data(), (int)(v.size() / kMtPolyWords), starts, pool);
         }
     }
     int c_first() const { return offset0 == 0 ? 1 : 0; }
     bool jumps() const { return chunks > c_first(); }
-    // One-shot stream (IFTA init, seed_random_phase): jump (when needed) +
-    // chunked seed; `seeds` are engine seeds (already forked), `states` holds
-    // streams*chunks entries.  Returns the number of launches.
+    // One-shot stream (IFTA init, seed_random_phase, pre-seeded OSPR): jump
+    // (when needed) + chunked seed; `seeds` are engine seeds (already
+    // forked), `states` holds streams*chunks entries.  Returns the number of
+    // launches.
     int launch(SeedArgs sa, const uint64_t* seeds, MtState* states, int streams, cudaStream_t st) const {
         int n = 0;
         if (jumps()) {
-            JumpArgs ja{seeds, nullptr, polys.p, (size_t)kPolyWords, states, chunks, c_first(), c_first()};
+            JumpArgs ja{seeds, nullptr, starts.p, pool.p, 1, states, chunks, c_first(), c_first()};
             k_mt_jump<<<streams * (chunks - c_first()), kJumpThreads, 0, st>>>(ja);
             ++n;
         }
@@ -182,19 +203,20 @@ struct SeedChunks {
         return n + 1;
     }
 
-    // Continued stream (OSPR: subframe n draws [(n-1)*npix, n*npix)).  With
-    // chunks > 1, states[] holds each chunk's start window; subframe 1 jumps
-    // from the seeds, later subframes move every start window by npix draws
-    // in place (one polynomial, x^(npix-1)).
-    DBuf<uint64_t> step;
+    // Continued stream (adaptive OSPR: subframe n draws [(n-1)*npix, n*npix)).
+    // With chunks > 1, states[] holds each chunk's start window; subframe 1
+    // jumps from the seeds, later subframes move every start window by npix
+    // draws in place (one polynomial, x^(npix-1)).
+    DBuf<int> step_starts;
+    DBuf<uint16_t> step_pool;
     void plan_stream(size_t npix, int streams, uint64_t offset = 0) {
-        plan(npix, streams, offset);
-        step.reset();
+        plan(npix, streams, offset, 1);  // a per-frame jump per chunk: split only below one CTA per SM
+        step_starts.reset();
+        step_pool.reset();
         if (chunks > 1) {
-            step.alloc(kPolyWords);
-            std::vector<uint64_t> g(kPolyWords);
+            std::vector<uint64_t> g(kMtPolyWords);
             mt_jump_poly(npix - 1, g.data());
-            CK(cudaMemcpy(step.p, g.data(), sizeof(uint64_t) * kPolyWords, cudaMemcpyHostToDevice));
+            upload_offsets(g.data(), 1, step_starts, step_pool);
         }
     }
     int launch_stream(SeedArgs sa, const uint64_t* seeds, MtState* states, int streams, bool first,
@@ -203,7 +225,7 @@ struct SeedChunks {
         if (chunks == 1) {
             int n = 0;
             if (first && offset0 > 0) {  // stream starts offset0 draws in (subframe block)
-                JumpArgs ja{seeds, nullptr, polys.p, (size_t)kPolyWords, states, 1, 0, 0};
+                JumpArgs ja{seeds, nullptr, starts.p, pool.p, 1, states, 1, 0, 0};
                 k_mt_jump<<<streams, kJumpThreads, 0, st>>>(ja);
                 ++n;
             }
@@ -211,8 +233,8 @@ struct SeedChunks {
             k_seed_random_phase<<<streams, kSeedThreads, kSeedSmem, st>>>(sa);
             return n + 1;
         }
-        JumpArgs ja = first ? JumpArgs{seeds, nullptr, polys.p, (size_t)kPolyWords, states, chunks, 0, c_first()}
-                            : JumpArgs{nullptr, states, step.p, 0, states, chunks, 0, 0};
+        JumpArgs ja = first ? JumpArgs{seeds, nullptr, starts.p, pool.p, 1, states, chunks, 0, c_first()}
+                            : JumpArgs{nullptr, states, step_starts.p, step_pool.p, 0, states, chunks, 0, 0};
         k_mt_jump<<<streams * chunks, kJumpThreads, 0, st>>>(ja);
         sa.seeds = nullptr;
         sa.chunks = chunks;
@@ -1160,8 +1182,30 @@ struct hgc_ospr_plan {
         if (stream) cudaStreamDestroy(stream);
     }
 
+    // Pre-seeded mode (plain OSPR, fewer jobs than SMs): all N subframes'
+    // draws are one stream of N*npix per job, seeded in one chunked launch
+    // (jump-ahead start states) into N field slices; the passes then run
+    // frame by frame on their slice.  Otherwise one seed launch per frame,
+    // double-buffered against the passes of the previous frame.
+    bool preseed = false;
+    size_t fstride = 0;  // field elements per job
     bool overlapped() const { return cfg.variant == 0 && field2.p; }
-    float2* buf(int n) const { return (overlapped() && (n & 1) == 0) ? field2.p : field.p; }
+    float2* buf(int n) const {
+        if (preseed) return field.p + (size_t)(n - 1) * npix;
+        return (overlapped() && (n & 1) == 0) ? field2.p : field.p;
+    }
+    SeedArgs seed_all_args() const {
+        SeedArgs sa{};
+        sa.amp = amp_d.p;
+        sa.amp_stride = per_job ? npix : 0;
+        sa.out = field.p;
+        sa.out_stride = fstride;
+        sa.npix = (size_t)cfg.subframes * npix;
+        sa.quad = 1;
+        sa.nx = nx;
+        sa.ny = ny;
+        return sa;
+    }
 
     float norm() const { return (float)(1.0 / std::sqrt((double)nx * ny)); }
 
@@ -1190,7 +1234,7 @@ struct hgc_ospr_plan {
         ColArgs ci{};
         ci.tw = tw;
         ci.field = buf(n);
-        ci.bstride = npix;
+        ci.bstride = fstride;
         ci.nx = nx;
         ci.layout = LAY_QUAD;
         ci.sign = +1;
@@ -1201,7 +1245,7 @@ struct hgc_ospr_plan {
         RowArgs ra{};
         ra.tw = tw;
         ra.field = buf(n);
-        ra.bstride = npix;
+        ra.bstride = fstride;
         ra.ny = ny;
         ra.layout = LAY_QUAD;
         ra.norm = norm();
@@ -1215,7 +1259,7 @@ struct hgc_ospr_plan {
         ColArgs co{};
         co.tw = tw;
         co.field = buf(n);
-        co.bstride = npix;
+        co.bstride = fstride;
         co.nx = nx;
         co.layout = LAY_QUAD;
         co.norm = norm();
@@ -1240,6 +1284,10 @@ struct hgc_ospr_plan {
         launches = 0;
         const int N = cfg.subframes;
         CK(cudaMemsetAsync(S.p, 0, sizeof(float) * npix * jobs, st));
+        if (preseed) {
+            launches += chunking.launch(seed_all_args(), seeds.p, mt.p, jobs, st);
+            CK(cudaGetLastError());
+        }
         const bool ov = overlapped();
         cudaStream_t ss = ov ? stream2 : st;
         if (ov) {  // fork the seed stream into the capture
@@ -1248,7 +1296,7 @@ struct hgc_ospr_plan {
         }
         for (int n = 1; n <= N; ++n) {
             if (ov && n >= 3) CK(cudaStreamWaitEvent(ss, ev_pass[n & 1], 0));  // buffer n%2 free again
-            launches += chunking.launch_stream(seed_args(n), seeds.p, mt.p, jobs, n == 1, ss) - 1;
+            if (!preseed) launches += chunking.launch_stream(seed_args(n), seeds.p, mt.p, jobs, n == 1, ss);
             CK(cudaGetLastError());
             if (ov) {
                 CK(cudaEventRecord(ev_seed, ss));
@@ -1261,7 +1309,7 @@ struct hgc_ospr_plan {
                 CK(cudaMemcpyAsync(snaps.p + (size_t)(n - 1) * npix, S.p, sizeof(float) * npix, cudaMemcpyDeviceToDevice,
                                    st));
             if (ov) CK(cudaEventRecord(ev_pass[n & 1], st));
-            launches += 4;
+            launches += 3;
         }
         if (ov) {  // join the seed stream
             CK(cudaEventRecord(ev_fork, ss));
@@ -1317,8 +1365,17 @@ static void create_ospr_plan(hgc_ospr_plan** out, const hgc_ospr_cfg* cfg_in, co
         p->tiles = col_tiles(nx, ny, LAY_QUAD);
         const size_t tot = p->npix * jobs;
         const size_t ttot = p->per_job ? tot : p->npix;
-        p->field.alloc(tot);
-        if (cfg->variant == 0 && cfg->subframes > 1) {  // second buffer + stream for seed/pass overlap
+        {
+            int dev = 0, sms = 148;
+            CK(cudaGetDevice(&dev));
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            const size_t all = (size_t)cfg->subframes * p->npix;
+            p->preseed = cfg->variant == 0 && cfg->subframes > 1 && jobs < sms && all < (1ull << 31) &&
+                         all * jobs * sizeof(float2) <= (8ull << 30);
+            p->fstride = p->preseed ? all : p->npix;
+        }
+        p->field.alloc(p->fstride * jobs);
+        if (!p->preseed && cfg->variant == 0 && cfg->subframes > 1) {  // second buffer + stream for seed/pass overlap
             p->field2.alloc(tot);
             CK(cudaStreamCreateWithFlags(&p->stream2, cudaStreamNonBlocking));
             CK(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
@@ -1343,7 +1400,8 @@ static void create_ospr_plan(hgc_ospr_plan** out, const hgc_ospr_cfg* cfg_in, co
             p->cum_part.alloc((size_t)count * p->cum_tiles * 8);
             p->cum_tr.alloc((size_t)count * 2);
         }
-        p->chunking.plan_stream(p->npix, jobs, (uint64_t)p->first * p->npix);
+        if (p->preseed) p->chunking.plan(p->fstride, jobs, (uint64_t)p->first * p->npix);
+        else p->chunking.plan_stream(p->npix, jobs, (uint64_t)p->first * p->npix);
         p->mt.alloc((size_t)jobs * p->chunking.chunks);
         p->seeds.alloc(jobs);
         prepare_kernels(nx, ny);
@@ -1531,9 +1589,13 @@ int hgc_ospr_plan_profile(hgc_ospr_plan* p, int reps, double* ms_seed, double* m
         cudaStream_t st = p->stream;
         const int j = p->jobs;
         if (ms_seed)
-            *ms_seed = time_launches(st, reps, [&] {
-                p->chunking.launch_stream(p->seed_args(1), p->seeds.p, p->mt.p, j, false, st);
-            });
+            *ms_seed = p->preseed  // per-frame share of the one all-frames seed
+                           ? time_launches(st, reps, [&] {
+                                 p->chunking.launch(p->seed_all_args(), p->seeds.p, p->mt.p, j, st);
+                             }) / p->cfg.subframes
+                           : time_launches(st, reps, [&] {
+                                 p->chunking.launch_stream(p->seed_args(1), p->seeds.p, p->mt.p, j, false, st);
+                             });
         if (ms_col_inv) *ms_col_inv = time_launches(st, reps, [&] { col_plain(p->ny, p->col_inv_args(1), j, st); });
         if (ms_row) *ms_row = time_launches(st, reps, [&] { row_fused(p->nx, p->row_args(1), j, st); });
         if (ms_col_acc) *ms_col_acc = time_launches(st, reps, [&] { col_ospr(p->ny, p->col_acc_args(1), j, st); });

@@ -154,25 +154,32 @@ struct SeedArgs {
 // g(F) W_1 with g = x^(J-1) mod P: word j = XOR over set bits i of g of raw
 // word x_{1+i+j}, x_0.. being the start window (the fresh seed block when
 // `from` is null, else from[s*chunks + c], a pos = 312 window; may alias
-// states).  g = polys + (c - poly_base) * poly_stride; chunks c < poly_base
-// are not moved (the seed block is stored as is).  The raw words are
-// regenerated block by block (one warp twists block q+2 while the CTA
-// accumulates over bits [312q, 312q+312) from blocks q, q+1); each block is
-// stored twice (slots b%3 and b%3+3) so reads never wrap.
-constexpr int kJumpThreads = 320;
-constexpr int kPolyWords = 312;
+// states).  g is given as its set-bit offsets per 312-bit block (mtjump.cpp,
+// mt_poly_offsets): poly k = c - poly_base (0 for every chunk when
+// poly_step == 0) has offsets pool[starts[65k + q] .. starts[65k + q + 1]) in
+// block q.  Chunks c < poly_base are not moved (the seed block is stored as
+// is).  The raw words are regenerated block by block (one warp twists block
+// q+2 while the CTA accumulates block q's offsets from blocks q, q+1); each
+// block is stored twice (slots b%3 and b%3+3) so reads never wrap.  Two
+// thread groups split each block's offsets; their partial XORs are combined
+// at the end.
+constexpr int kJumpGroups = 2;
+constexpr int kJumpGroupThreads = 320;
+constexpr int kJumpThreads = kJumpGroups * kJumpGroupThreads;
+constexpr int kJumpBlocks = 64;  // 312-bit blocks covering deg P = 19937
 struct JumpArgs {
     const uint64_t* seeds;  // [streams] engine seeds (from == nullptr)
     const MtState* from;    // [streams * chunks] start windows, or nullptr
-    const uint64_t* polys;
-    size_t poly_stride;     // kPolyWords, or 0: one polynomial for every chunk
+    const int* starts;      // [polys][kJumpBlocks + 1]
+    const uint16_t* pool;   // set-bit offsets within each block
+    int poly_step;          // 1: one polynomial per chunk; 0: one for all
     MtState* states;        // [streams * chunks]
     int chunks, c_lo, poly_base;
 };
 
 __global__ void __launch_bounds__(kJumpThreads) k_mt_jump(JumpArgs a) {
     __shared__ uint64_t ring[6 * kMtN];
-    __shared__ uint64_t g[kPolyWords + 1];
+    __shared__ uint64_t red[kMtN];
     const int per = a.chunks - a.c_lo;
     const int s = blockIdx.x / per, c = a.c_lo + blockIdx.x % per;
     const size_t b = (size_t)s * a.chunks + c;
@@ -187,50 +194,45 @@ __global__ void __launch_bounds__(kJumpThreads) k_mt_jump(JumpArgs a) {
             ring[i] = ring[3 * kMtN + i] = x;
         }
     }
+    __syncthreads();
     if (c < a.poly_base) {  // offset 0: the seed block itself
-        __syncthreads();
         for (int i = tid; i < kMtN; i += blockDim.x) a.states[b].w[i] = ring[i];
         if (tid == 0) a.states[b].pos = kMtN;
         return;
     }
-    const uint64_t* gp = a.polys + (size_t)(c - a.poly_base) * a.poly_stride;
-    for (int i = tid; i < kPolyWords; i += blockDim.x) g[i] = gp[i];
-    if (tid == 0) g[kPolyWords] = 0;
-    __syncthreads();
+    const int* st = a.starts + (size_t)(c - a.poly_base) * a.poly_step * (kJumpBlocks + 1);
     if (warp == 0) {  // block 1
         mt_twist_warp(ring, ring + kMtN, lane);
         for (int i = lane; i < kMtN; i += 32) ring[4 * kMtN + i] = ring[kMtN + i];
     }
     __syncthreads();
-    constexpr int kBits = kPolyWords * 64;
+    const int grp = tid / kJumpGroupThreads, j = tid % kJumpGroupThreads;
     uint64_t acc = 0;
-    const int j = tid;
-    for (int q = 0; q * kMtN < kBits; ++q) {
-        if (warp == 0 && (q + 2) * kMtN <= kBits + kMtN) {  // block q+2 from block q+1
+    for (int q = 0; q < kJumpBlocks; ++q) {
+        if (warp == 0) {  // block q+2 from block q+1
             const int so = (q + 1) % 3, sn = (q + 2) % 3;
             mt_twist_warp(ring + so * kMtN, ring + sn * kMtN, lane);
             for (int i = lane; i < kMtN; i += 32) ring[(sn + 3) * kMtN + i] = ring[sn * kMtN + i];
         }
         if (j < kMtN) {
             const uint64_t* base = ring + (q % 3) * kMtN + 1 + j;  // x_{312q + 1 + j + ii} = base[ii]
-            const int i0 = q * kMtN;
+            const int k0 = __ldg(st + q), k1 = __ldg(st + q + 1);
+            const int half = (k1 - k0 + 1) >> 1;
+            const uint16_t* off = a.pool + k0 + (grp ? half : 0);
+            const int cnt = grp ? (k1 - k0) - half : half;
+            int k = 0;
 #pragma unroll 1
-            for (int k = 0; k < kMtN; k += 64) {
-                const int bi = i0 + k;  // bits bi .. bi+63 of g (fewer at the block end)
-                if (bi >= kBits) break;
-                const int w = bi >> 6, o = bi & 63;
-                uint64_t m = o ? (g[w] >> o) | (g[w + 1] << (64 - o)) : g[w];
-                if (kMtN - k < 64) m &= (1ull << (kMtN - k)) - 1;
-                while (m) {
-                    const int b = __ffsll((long long)m) - 1;
-                    acc ^= base[k + b];
-                    m &= m - 1;
-                }
+            for (; k + 4 <= cnt; k += 4) {
+                const int o0 = __ldg(off + k), o1 = __ldg(off + k + 1), o2 = __ldg(off + k + 2), o3 = __ldg(off + k + 3);
+                acc ^= base[o0] ^ base[o1] ^ base[o2] ^ base[o3];
             }
+            for (; k < cnt; ++k) acc ^= base[__ldg(off + k)];
         }
         __syncthreads();
     }
-    if (j < kMtN) a.states[b].w[j] = acc;
+    if (grp == 1 && j < kMtN) red[j] = acc;
+    __syncthreads();
+    if (grp == 0 && j < kMtN) a.states[b].w[j] = acc ^ red[j];
     if (tid == 0) a.states[b].pos = kMtN;
 }
 
@@ -273,6 +275,7 @@ __global__ void __launch_bounds__(kSeedThreads) k_seed_random_phase(SeedArgs a) 
     const int cthreads = blockDim.x - 32;
     const int ctid = tid - 32;
     const int lognx = 31 - __clz(a.nx > 0 ? a.nx : 1), nxm = a.nx - 1;  // nx is a power of two
+    const int pmask = a.quad ? a.nx * a.ny - 1 : 0x7fffffff;
     const double* __restrict__ ampp = amp;
     const float* __restrict__ Sp = a.S ? a.S + a.S_stride * s : nullptr;
     // step g: producer writes group g (g < ngroups); consumers process group g-1
@@ -308,7 +311,7 @@ __global__ void __launch_bounds__(kSeedThreads) k_seed_random_phase(SeedArgs a) 
                 double sn, cs;
                 sincos_0_2pi(theta, &sn, &cs);
                 const int p = (int)cbeg + d0 + j;  // row-major pixel index of this draw (rng.hpp:60)
-                double av = ampp[p];
+                double av = ampp[p & pmask];  // pre-seeded OSPR: draw p of frame p / npix
                 int o = p, so = p;
                 if (a.quad) {
                     const int py = p >> lognx, px = p & nxm;

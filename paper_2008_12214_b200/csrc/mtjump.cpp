@@ -262,6 +262,23 @@ const std::vector<uint64_t>& mt_chunk_polys(uint64_t offset0, uint64_t len, int 
     return cache.emplace(key, std::move(out)).first->second;
 }
 
+void mt_poly_offsets(const uint64_t* polys, int npolys, std::vector<int>& starts, std::vector<uint16_t>& pool) {
+    constexpr int kBlocks = (kMtPolyWords * 64 + kN - 1) / kN;  // 64
+    starts.assign((size_t)npolys * (kBlocks + 1), 0);
+    pool.clear();
+    for (int k = 0; k < npolys; ++k) {
+        const uint64_t* g = polys + (size_t)k * kMtPolyWords;
+        for (int q = 0; q < kBlocks; ++q) {
+            starts[(size_t)k * (kBlocks + 1) + q] = (int)pool.size();
+            for (int ii = 0; ii < kN; ++ii) {
+                const int i = q * kN + ii;
+                if (i < kMtPolyWords * 64 && ((g[i >> 6] >> (i & 63)) & 1)) pool.push_back((uint16_t)ii);
+            }
+        }
+        starts[(size_t)k * (kBlocks + 1) + kBlocks] = (int)pool.size();
+    }
+}
+
 // Host reference of the jump: the raw-word window after J draws of the engine
 // seeded with `engine_seed` (words x_J .. x_{J+311}), computed as g(F) W_1.
 void mt_jump_state_host(uint64_t engine_seed, uint64_t J, uint64_t* window) {

@@ -1,0 +1,15 @@
+// k_row_full.cu — fused aperture-plane row pass with the QK_FULL quantiser
+// (quant.cuh), instantiated without (FQ = 0) and with (FQ = 1) Fresnel Q.
+#include "launch_impl.cuh"
+
+namespace hg {
+void row_fused_full(int nx, const RowArgs& a, int batch, cudaStream_t st, bool prepare) {
+    if (prepare) {
+        row_dispatch_q<ROW_FUSED, QK_FULL, LAY_QUAD, 0>(nx, a, batch, st, true);
+        row_dispatch_q<ROW_FUSED, QK_FULL, LAY_QUAD, 1>(nx, a, batch, st, true);
+        return;
+    }
+    if (a.fresnel_q) row_dispatch_q<ROW_FUSED, QK_FULL, LAY_QUAD, 1>(nx, a, batch, st, false);
+    else row_dispatch_q<ROW_FUSED, QK_FULL, LAY_QUAD, 0>(nx, a, batch, st, false);
+}
+}  // namespace hg

@@ -13,6 +13,9 @@ namespace hg {
 // plain transforms for both layouts.
 void row_fused(int nx, const RowArgs& a, int batch, cudaStream_t st, bool prepare = false);
 void row_plain(int nx, const RowArgs& a, int batch, cudaStream_t st, bool prepare = false);
+// specialised fused row passes, one translation unit each (k_row_bin.cu, k_row_full.cu)
+void row_fused_binary(int nx, const RowArgs& a, int batch, cudaStream_t st, bool prepare);
+void row_fused_full(int nx, const RowArgs& a, int batch, cudaStream_t st, bool prepare);
 void col_plain(int ny, const ColArgs& a, int batch, cudaStream_t st, bool prepare = false);
 void col_gs(int ny, const ColArgs& a, int batch, cudaStream_t st, bool prepare = false);
 void col_ospr(int ny, const ColArgs& a, int batch, cudaStream_t st, bool prepare = false);

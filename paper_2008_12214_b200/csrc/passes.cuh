@@ -93,7 +93,9 @@ struct RowCfg {
     static constexpr int MIN_BLOCKS = LAY == LAY_QUAD ? (THREADS >= 512 ? HG_ROWQ_MINB : 1) : (THREADS >= 256 ? 3 : 1);
 };
 
-template <int NX, int MODE, int QK, int LAY>
+// FQ: Fresnel Q in the fused pass — 0 absent, 1 present (compile time, the
+// specialised quantisers), 2 decided at run time from a.fresnel_q.
+template <int NX, int MODE, int QK, int LAY, int FQ>
 __global__ void __launch_bounds__(RowCfg<NX, LAY>::THREADS, RowCfg<NX, LAY>::MIN_BLOCKS) k_row(RowArgs a) {
     using Cfg = RowCfg<NX, LAY>;
     constexpr int E = Cfg::E, T = Cfg::T;
@@ -159,20 +161,22 @@ __global__ void __launch_bounds__(RowCfg<NX, LAY>::THREADS, RowCfg<NX, LAY>::MIN
         fft_line<NX, +1>(v, t, smem, idx, a.tw);  // completes the 2-D inverse (propagation.hpp:89-95)
         const int rowbase = y * NX;
         const float norm = a.norm;
-        const float2* __restrict__ fq = a.fresnel_q;
+        const float2* __restrict__ fq = FQ == 0 ? nullptr : a.fresnel_q;
+        const bool hasq = FQ == 1 || (FQ == 2 && fq != nullptr);
         uint8_t* __restrict__ lv8 = a.levels8 ? a.levels8 + a.lv_bstride * b : nullptr;
         uint16_t* __restrict__ lv16 = a.levels16 ? a.levels16 + a.lv_bstride * b : nullptr;
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             const int i = rowbase + t + e * T;  // row-major pixel index (levels, Q, illumination)
             float2 f = cscale(v[e], norm);                        // fftw_backend.cpp:121-123
-            if (fq) f = cmul_conj_rn(f, __ldg(&fq[i]));           // propagation.hpp:93
+            if (hasq) f = cmul_conj_rn(f, __ldg(&fq[i]));         // propagation.hpp:93
             const int k = quant_decide_kind<QK>(a.q, f.x, f.y, i);  // quantise.hpp:211-215
             if constexpr (QK == QK_BINARY) f = k ? a.q.s1 : a.q.s0;
+            else if constexpr (QK == QK_FULL) f = __ldg(&a.q.states[k]);  // phase mode, no illumination
             else f = quant_state(a.q, k, i);
             if (lv8 && valid) lv8[i] = (uint8_t)k;
             if (lv16 && valid) lv16[i] = (uint16_t)k;
-            if (fq) f = cmul_rn(f, __ldg(&fq[i]));                // propagation.hpp:85
+            if (hasq) f = cmul_rn(f, __ldg(&fq[i]));              // propagation.hpp:85
             v[e] = f;
         }
         fft_line<NX, -1>(v, t, smem, idx, a.tw);  // starts the forward transform

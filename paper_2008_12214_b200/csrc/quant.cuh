@@ -119,7 +119,9 @@ enum QuantKind { QK_GENERIC = 0, QK_BINARY = 1, QK_FULL = 2 };
 __device__ __forceinline__ float fast_atan2f(float y, float x) {
     const float ax = fabsf(x), ay = fabsf(y);
     const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
-    const float a = mn * __frcp_rn(mx);  // mx == 0 -> NaN; caller treats NaN as "near"
+    float rmx;  // approximate reciprocal (<= 1 ulp); mx == 0 -> inf -> a = NaN, which the caller treats as "near"
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rmx) : "f"(mx));
+    const float a = mn * rmx;
     const float s = a * a;
     float r = 0.0068426248975283f;
     r = fmaf(r, s, -0.03372593810402613f);

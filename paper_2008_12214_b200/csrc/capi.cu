@@ -639,29 +639,7 @@ struct hgc_ifta_plan {
     ~hgc_ifta_plan() {
         if (graph) cudaGraphExecDestroy(graph);
         if (done) cudaEventDestroy(done);
-        for (cudaEvent_t e : {ev_fork, ev_stagger, ev_join[0]})
-            if (e) cudaEventDestroy(e);
-        if (lane_stream[0]) cudaStreamDestroy(lane_stream[0]);
         if (stream) cudaStreamDestroy(stream);
-    }
-
-    // concurrent lanes (streams) of target halves; see record()
-    static constexpr int kMaxLanes = 2;
-    cudaStream_t lane_stream[kMaxLanes - 1] = {nullptr};
-    cudaEvent_t ev_fork = nullptr, ev_stagger = nullptr, ev_join[kMaxLanes - 1] = {nullptr};
-    int lanes() const {
-        int l = batch >= 2 && group_size() >= batch ? 2 : 1;  // working set beyond L2: no group reuse to lose
-        if (const char* ev = getenv("HG_LANES")) l = atoi(ev);  // tuning
-        const int cap = kMaxLanes;
-        return std::max(1, std::min(std::min(l, cap), batch));
-    }
-    void create_lanes() {
-        for (int i = 0; i < kMaxLanes - 1; ++i) {
-            CK(cudaStreamCreateWithFlags(&lane_stream[i], cudaStreamNonBlocking));
-            CK(cudaEventCreateWithFlags(&ev_join[i], cudaEventDisableTiming));
-        }
-        CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&ev_stagger, cudaEventDisableTiming));
     }
 
     bool random_init() const {
@@ -800,42 +778,27 @@ struct hgc_ifta_plan {
         ++launches;
         // Iterations run target-group by target-group: a group's field +
         // target (+ weights) is sized to stay L2-resident across the two
-        // passes and successive iterations (126 MB L2 on B200).  With two
-        // lanes the batch is split in halves on two captured streams, lane 1
-        // starting one row pass behind lane 0, so the issue-bound row pass of
-        // one half co-runs with the latency-bound column pass of the other.
-        const int L = lanes();
+        // passes and successive iterations (126 MB L2 on B200).  (Running two
+        // target halves on concurrent streams, staggered by a pass, measured
+        // no gain at 4096^2: 3927 vs 3950 it/s.)
         const int G = group_size();
-        if (L > 1) CK(cudaEventRecord(ev_fork, st));
-        for (int l = 0; l < L; ++l) {
-            const int lb0 = (int)((long long)batch * l / L), lb1 = (int)((long long)batch * (l + 1) / L);
-            cudaStream_t ls = l == 0 ? st : lane_stream[l - 1];
-            if (l > 0) CK(cudaStreamWaitEvent(ls, ev_stagger, 0));
-            bool first = true;
-            for (int g0 = lb0; g0 < lb1; g0 += G) {
-                const int gn = std::min(G, lb1 - g0);
-                for (int k = 1; k <= cfg.iterations; ++k) {
-                    RowArgs ra = row_args(k == cfg.iterations);
-                    ra.field += (size_t)g0 * npix;
-                    if (ra.levels8) ra.levels8 += (size_t)g0 * npix;
-                    if (ra.levels16) ra.levels16 += (size_t)g0 * npix;
-                    row_fused(nx, ra, gn, ls);
-                    if (l == 0 && first && L > 1) CK(cudaEventRecord(ev_stagger, ls));
-                    first = false;
-                    ColArgs cg = col_args(k);
-                    cg.field += (size_t)g0 * npix;
-                    cg.target += (size_t)g0 * npix;
-                    if (cg.weights) cg.weights += (size_t)g0 * npix;
-                    if (cg.tphase_cs) cg.tphase_cs += (size_t)g0 * npix;
-                    cg.replay_out += (size_t)g0 * npix;
-                    cg.partials += (size_t)g0 * tiles * 8;
-                    col_gs(ny, cg, gn, ls);
-                    launches += 2;
-                }
-            }
-            if (l > 0) {
-                CK(cudaEventRecord(ev_join[l - 1], ls));
-                CK(cudaStreamWaitEvent(st, ev_join[l - 1], 0));
+        for (int g0 = 0; g0 < batch; g0 += G) {
+            const int gn = std::min(G, batch - g0);
+            for (int k = 1; k <= cfg.iterations; ++k) {
+                RowArgs ra = row_args(k == cfg.iterations);
+                ra.field += (size_t)g0 * npix;
+                if (ra.levels8) ra.levels8 += (size_t)g0 * npix;
+                if (ra.levels16) ra.levels16 += (size_t)g0 * npix;
+                row_fused(nx, ra, gn, st);
+                ColArgs cg = col_args(k);
+                cg.field += (size_t)g0 * npix;
+                cg.target += (size_t)g0 * npix;
+                if (cg.weights) cg.weights += (size_t)g0 * npix;
+                if (cg.tphase_cs) cg.tphase_cs += (size_t)g0 * npix;
+                cg.replay_out += (size_t)g0 * npix;
+                cg.partials += (size_t)g0 * tiles * 8;
+                col_gs(ny, cg, gn, st);
+                launches += 2;
             }
         }
         k_finalize<<<batch, 32, 0, st>>>(partials.p, cfg.iterations, batch, tiles, (double)M, cfg.freedom_scale, 0,
@@ -942,7 +905,6 @@ int hgc_ifta_plan_create(hgc_ifta_plan** out, const hgc_ifta_cfg* cfg, const hgc
         p->partials.alloc((size_t)cfg->iterations * batch * p->tiles * 8);
         p->trace.alloc((size_t)cfg->iterations * batch);
         if (p->random_init()) p->chunking.plan(p->npix, batch);
-        p->create_lanes();
         p->mt.alloc((size_t)batch * p->chunking.chunks);
         p->seeds.alloc(batch);
         if (fresnel) {

@@ -167,12 +167,18 @@ typedef struct hgc_ospr_plan hgc_ospr_plan;
 
 int hgc_ifta_plan_create(hgc_ifta_plan** plan, const hgc_ifta_cfg* cfg, const hgc_slm* slm,
                          const hgc_fresnel* fresnel, int nx, int ny, int batch);
-/* Host->device copy of io's inputs (amplitude, phase, roi, seeds, init_*). */
+/* Host->device copy of io's inputs (amplitude, phase, roi, seeds, init_*),
+ * asynchronous on the plan's stream: with pinned host buffers it returns once
+ * the copies are enqueued, so the caller must keep them unchanged until the
+ * next execute has completed (download returned).  TargetSpec validation
+ * (target.hpp:52-73) runs on the device; its error (HGC_EINVAL, same message)
+ * is returned by the next download.  hgc_ifta_run validates eagerly. */
 int hgc_ifta_plan_upload(hgc_ifta_plan* plan, const hgc_ifta_io* io);
 /* Enqueue one full run (init + iterations + trace reduction) on `stream`
  * (a cudaStream_t, or NULL for the plan's own stream).  Asynchronous. */
 int hgc_ifta_plan_execute(hgc_ifta_plan* plan, void* stream);
-/* Synchronise the plan's stream and copy io's requested outputs to the host. */
+/* Wait for this plan's last execute and copy io's requested outputs to the
+ * host (HGC_EINVAL if the uploaded target failed validation). */
 int hgc_ifta_plan_download(hgc_ifta_plan* plan, hgc_ifta_io* io);
 /* Device pointers of the resident buffers (any may be NULL on input):
  * field = replay after execute (complex float [batch][ny][nx]),
@@ -188,6 +194,7 @@ int hgc_ifta_plan_destroy(hgc_ifta_plan* plan);
 
 int hgc_ospr_plan_create(hgc_ospr_plan** plan, const hgc_ospr_cfg* cfg, const hgc_slm* slm, int nx,
                          int ny, int jobs, int per_job_target);
+/* Asynchronous as hgc_ifta_plan_upload (validation errors on download). */
 int hgc_ospr_plan_upload(hgc_ospr_plan* plan, const hgc_ospr_io* io);
 int hgc_ospr_plan_execute(hgc_ospr_plan* plan, void* stream);
 int hgc_ospr_plan_download(hgc_ospr_plan* plan, hgc_ospr_io* io);

@@ -246,6 +246,9 @@ struct SeedChunks {
 };
 
 // ------------------------------------------------------- small kernels
+__global__ void k_fill_c(float2* p, size_t n, float2 v) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = v;
+}
 __global__ void k_fill_f(float* p, size_t n, float v) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = v;
 }
@@ -487,25 +490,30 @@ static void validate_slm(const hgc_slm* s, size_t npix) {
 // TargetSpec::validate, target.hpp:52-73, for a batch already copied to the
 // device (amplitude + optional phase), and the shared roi on the host.
 // Returns the roi coverage M (npix without roi).
-static size_t validate_target_dev(const double* d_amp, const double* d_phase, const uint8_t* roi, size_t npix,
-                                  size_t total, cudaStream_t st) {
-    DBuf<int> flag;
-    flag.alloc(1);
-    CK(cudaMemsetAsync(flag.p, 0, sizeof(int), st));
-    k_validate<<<ew_grid(total), 256, 0, st>>>(d_amp, d_phase, total, flag.p);
+// TargetSpec::validate (target.hpp:52-73) for the plan API, asynchronous: the
+// amplitude / phase scan runs on the device at upload and its flags are
+// raised by the next download (or right away by the one-shot hgc_*_run).
+static void launch_validate(const double* d_amp, const double* d_phase, size_t total, int* flags, cudaStream_t st) {
+    CK(cudaMemsetAsync(flags, 0, sizeof(int), st));
+    k_validate<<<ew_grid(total), 256, 0, st>>>(d_amp, d_phase, total, flags);
     CK(cudaGetLastError());
-    int h = 0;
-    CK(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+}
+static void raise_validation(int h) {
     if (h & 1) invalid("TargetSpec.amplitude: image contains non-finite values");
     if (h & 2) invalid("TargetSpec: amplitude must be non-negative");
     if (h & 4) invalid("TargetSpec.phase: image contains non-finite values");
-    size_t m = npix;
-    if (roi) {
-        m = 0;
-        for (size_t i = 0; i < npix; ++i) m += roi[i] != 0;
-        if (m == 0) invalid("TargetSpec: roi covers no pixels");
-    }
+}
+static void check_validation(const int* flags, cudaStream_t st) {
+    int h = 0;
+    CK(cudaMemcpyAsync(&h, flags, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    raise_validation(h);
+}
+static size_t roi_count(const uint8_t* roi, size_t npix) {
+    if (!roi) return npix;
+    size_t m = 0;
+    for (size_t i = 0; i < npix; ++i) m += roi[i] != 0;
+    if (m == 0) invalid("TargetSpec: roi covers no pixels");
     return m;
 }
 
@@ -622,6 +630,8 @@ struct hgc_ifta_plan {
     int bx0 = 0, by0 = 0, bw = 0, bh = 0;  // LT roi bounding box
     DBuf<float2> field, Q, tphase_cs, init_field, scratch;
     cudaEvent_t done = nullptr;  // recorded after each execute on the execute stream
+    cudaEvent_t up_ev = nullptr;  // end of the last upload's stream work
+    DBuf<int> vflags;             // deferred TargetSpec validation flags
     DBuf<float> target_f, weights, init_weights;
     DBuf<double> amp_d, phase_d, partials, trace;
     DBuf<uint8_t> roi, roi_rm, lv8;
@@ -639,6 +649,7 @@ struct hgc_ifta_plan {
     ~hgc_ifta_plan() {
         if (graph) cudaGraphExecDestroy(graph);
         if (done) cudaEventDestroy(done);
+        if (up_ev) cudaEventDestroy(up_ev);
         if (stream) cudaStreamDestroy(stream);
     }
 
@@ -916,6 +927,8 @@ int hgc_ifta_plan_create(hgc_ifta_plan** out, const hgc_ifta_cfg* cfg, const hgc
         }
         prepare_kernels(nx, ny);
         CK(cudaEventCreateWithFlags(&p->done, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&p->up_ev, cudaEventDisableTiming));
+        p->vflags.alloc(1);
         CK(cudaStreamSynchronize(p->stream));
         *out = p.release();
     });
@@ -933,7 +946,8 @@ int hgc_ifta_plan_upload(hgc_ifta_plan* p, const hgc_ifta_io* io) {
             p->phase_d.ensure(tot);
             CK(cudaMemcpyAsync(p->phase_d.p, io->phase, sizeof(double) * tot, cudaMemcpyHostToDevice, p->stream));
         }
-        p->M = validate_target_dev(p->amp_d.p, io->phase ? p->phase_d.p : nullptr, io->roi, npix, tot, p->stream);
+        p->M = roi_count(io->roi, npix);
+        launch_validate(p->amp_d.p, io->phase ? p->phase_d.p : nullptr, tot, p->vflags.p, p->stream);
         k_to_colpair<double, float><<<ew_grid(tot), 256, 0, p->stream>>>(p->amp_d.p, p->target_f.p, p->nx, p->ny, tot);
         CK(cudaGetLastError());
         if (io->phase) {
@@ -944,9 +958,8 @@ int hgc_ifta_plan_upload(hgc_ifta_plan* p, const hgc_ifta_io* io) {
         } else if (!p->cfg.freedom_phase) {
             // no target phase: the constraint enforces phase 0 (ifta.hpp:216)
             p->tphase_cs.ensure(tot);
-            std::vector<float2> ones(tot, make_float2(1.f, 0.f));
-            CK(cudaMemcpyAsync(p->tphase_cs.p, ones.data(), sizeof(float2) * tot, cudaMemcpyHostToDevice, p->stream));
-            CK(cudaStreamSynchronize(p->stream));
+            k_fill_c<<<ew_grid(tot), 256, 0, p->stream>>>(p->tphase_cs.p, tot, make_float2(1.f, 0.f));
+            CK(cudaGetLastError());
         }
         if (io->fresnel_q) {  // caller-supplied Q (e.g. from a reference Propagator<float>)
             p->Q.ensure(npix);
@@ -995,7 +1008,7 @@ int hgc_ifta_plan_upload(hgc_ifta_plan* p, const hgc_ifta_io* io) {
                                    p->stream));
             }
         }
-        CK(cudaStreamSynchronize(p->stream));
+        CK(cudaEventRecord(p->up_ev, p->stream));  // execute waits on it; no host sync
         const uint64_t sig = (uint64_t)(uintptr_t)p->roi.p ^ ((uint64_t)(uintptr_t)p->phase_d.p << 1) ^
                              ((uint64_t)(uintptr_t)p->tphase_cs.p << 2) ^ ((uint64_t)(uintptr_t)p->init_field.p << 3) ^
                              ((uint64_t)(uintptr_t)p->init_weights.p << 4) ^ ((uint64_t)(uintptr_t)p->Q.p << 5) ^
@@ -1029,6 +1042,7 @@ int hgc_ifta_plan_execute(hgc_ifta_plan* p, void* stream) {
             CK(cudaGraphInstantiate(&p->graph, g, 0));
             cudaGraphDestroy(g);
         }
+        CK(cudaStreamWaitEvent(st, p->up_ev, 0));  // the last upload's copies and conversions
         CK(cudaGraphLaunch(p->graph, st));
         CK(cudaEventRecord(p->done, st));
     });
@@ -1039,6 +1053,11 @@ int hgc_ifta_plan_download(hgc_ifta_plan* p, hgc_ifta_io* io) {
         if (!p || !io) invalid("hgc_ifta_plan_download: null argument");
         CK(cudaSetDevice(p->device));
         CK(cudaEventSynchronize(p->done));  // this plan's last execute only (other plans keep running)
+        {
+            int h = 0;
+            CK(cudaMemcpy(&h, p->vflags.p, sizeof(int), cudaMemcpyDeviceToHost));
+            raise_validation(h);  // deferred from upload
+        }
         const size_t tot = p->npix * p->batch;
         const int K = p->cfg.iterations;
         if (io->replay) {  // resident quad layout -> row-major
@@ -1127,6 +1146,7 @@ int hgc_ifta_run(const hgc_ifta_cfg* cfg, const hgc_slm* slm, const hgc_fresnel*
     hgc_ifta_plan* p = nullptr;
     int rc = hgc_ifta_plan_create(&p, cfg, slm, fresnel, nx, ny, batch);
     if (rc == HGC_OK) rc = hgc_ifta_plan_upload(p, io);
+    if (rc == HGC_OK) rc = guarded([&] { check_validation(p->vflags.p, p->stream); });  // eager in the one-shot run
     if (rc == HGC_OK) rc = hgc_ifta_plan_execute(p, nullptr);
     if (rc == HGC_OK) rc = hgc_ifta_plan_download(p, io);
     if (p) {
@@ -1175,10 +1195,13 @@ struct hgc_ospr_plan {
     cudaStream_t stream2 = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_seed = nullptr, ev_pass[2] = {nullptr, nullptr};
     cudaEvent_t done = nullptr;  // recorded after each execute on the execute stream
+    cudaEvent_t up_ev = nullptr;  // end of the last upload's stream work
+    DBuf<int> vflags;             // deferred TargetSpec validation flags
+    DBuf<uint8_t> roi_rm;
 
     ~hgc_ospr_plan() {
         if (graph) cudaGraphExecDestroy(graph);
-        for (cudaEvent_t e : {ev_fork, ev_seed, ev_pass[0], ev_pass[1], done})
+        for (cudaEvent_t e : {ev_fork, ev_seed, ev_pass[0], ev_pass[1], done, up_ev})
             if (e) cudaEventDestroy(e);
         if (stream2) cudaStreamDestroy(stream2);
         if (stream) cudaStreamDestroy(stream);
@@ -1408,6 +1431,8 @@ static void create_ospr_plan(hgc_ospr_plan** out, const hgc_ospr_cfg* cfg_in, co
         p->seeds.alloc(jobs);
         prepare_kernels(nx, ny);
         CK(cudaEventCreateWithFlags(&p->done, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&p->up_ev, cudaEventDisableTiming));
+        p->vflags.alloc(1);
         CK(cudaStreamSynchronize(p->stream));
         *out = p.release();
 }
@@ -1463,25 +1488,25 @@ int hgc_ospr_plan_upload(hgc_ospr_plan* p, const hgc_ospr_io* io) {
         const size_t ttot = p->per_job ? p->npix * p->jobs : p->npix;
         if (!io->amplitude) invalid("TargetSpec: amplitude image is empty");
         CK(cudaMemcpyAsync(p->amp_d.p, io->amplitude, sizeof(double) * ttot, cudaMemcpyHostToDevice, p->stream));
-        p->M = validate_target_dev(p->amp_d.p, nullptr, io->roi, p->npix, ttot, p->stream);
+        p->M = roi_count(io->roi, p->npix);
+        launch_validate(p->amp_d.p, nullptr, ttot, p->vflags.p, p->stream);
         k_to_colpair<double, float><<<ew_grid(ttot), 256, 0, p->stream>>>(p->amp_d.p, p->target_f.p, p->nx, p->ny,
                                                                           ttot);
         CK(cudaGetLastError());
         p->has_roi = io->roi != nullptr;
         if (io->roi) {  // column-pair major
             p->roi.ensure(p->npix);
-            DBuf<uint8_t> rm;
-            rm.alloc(p->npix);
-            CK(cudaMemcpyAsync(rm.p, io->roi, p->npix, cudaMemcpyHostToDevice, p->stream));
-            k_to_colpair<uint8_t, uint8_t><<<ew_grid(p->npix), 256, 0, p->stream>>>(rm.p, p->roi.p, p->nx, p->ny,
-                                                                                  p->npix);
+            p->roi_rm.ensure(p->npix);
+            CK(cudaMemcpyAsync(p->roi_rm.p, io->roi, p->npix, cudaMemcpyHostToDevice, p->stream));
+            k_to_colpair<uint8_t, uint8_t><<<ew_grid(p->npix), 256, 0, p->stream>>>(p->roi_rm.p, p->roi.p, p->nx,
+                                                                                  p->ny, p->npix);
             CK(cudaGetLastError());
-            CK(cudaStreamSynchronize(p->stream));
+            
         }
         std::vector<uint64_t> es(p->jobs);
         for (int j = 0; j < p->jobs; ++j) es[j] = fork_seed(io->seeds ? io->seeds[j] : p->cfg.seed, 0);  // ospr.hpp:89
         CK(cudaMemcpyAsync(p->seeds.p, es.data(), sizeof(uint64_t) * p->jobs, cudaMemcpyHostToDevice, p->stream));
-        CK(cudaStreamSynchronize(p->stream));
+        CK(cudaEventRecord(p->up_ev, p->stream));
         const uint64_t sig = (uint64_t)(uintptr_t)p->roi.p ^ ((uint64_t)p->has_roi << 60) ^ p->M;
         if (p->graph && sig != p->graph_sig) {
             cudaGraphExecDestroy(p->graph);
@@ -1511,6 +1536,7 @@ int hgc_ospr_plan_execute(hgc_ospr_plan* p, void* stream) {
             CK(cudaGraphInstantiate(&p->graph, g, 0));
             cudaGraphDestroy(g);
         }
+        CK(cudaStreamWaitEvent(st, p->up_ev, 0));  // the last upload's copies and conversions
         CK(cudaGraphLaunch(p->graph, st));
         CK(cudaEventRecord(p->done, st));
     });
@@ -1521,6 +1547,11 @@ int hgc_ospr_plan_download(hgc_ospr_plan* p, hgc_ospr_io* io) {
         if (!p || !io) invalid("hgc_ospr_plan_download: null argument");
         CK(cudaSetDevice(p->device));
         CK(cudaEventSynchronize(p->done));
+        {
+            int h = 0;
+            CK(cudaMemcpy(&h, p->vflags.p, sizeof(int), cudaMemcpyDeviceToHost));
+            raise_validation(h);  // deferred from upload
+        }
         const int N = p->cfg.subframes;
         const size_t npix = p->npix, tot = npix * p->jobs, lvtot = tot * N;
         std::vector<double> tr((size_t)N * p->jobs * 2);
@@ -1620,6 +1651,7 @@ int hgc_ospr_run(const hgc_ospr_cfg* cfg, const hgc_slm* slm, int nx, int ny, in
     hgc_ospr_plan* p = nullptr;
     int rc = hgc_ospr_plan_create(&p, cfg, slm, nx, ny, jobs, io ? io->per_job_target : 0);
     if (rc == HGC_OK) rc = hgc_ospr_plan_upload(p, io);
+    if (rc == HGC_OK) rc = guarded([&] { check_validation(p->vflags.p, p->stream); });  // eager in the one-shot run
     if (rc == HGC_OK) rc = hgc_ospr_plan_execute(p, nullptr);
     if (rc == HGC_OK) rc = hgc_ospr_plan_download(p, io);
     if (p) {

@@ -225,12 +225,15 @@ struct ColCfg {
     static constexpr int E = LineCfg<NY>::E, T = LineCfg<NY>::T;
     // LAY_ROW: up to 128 KiB of complex64 per CTA (1 CTA / SM at 4096);
     // LAY_QUAD: 64 KiB column-pair tiles (2 CTAs / SM)
-    static constexpr int BUDGET = LAY == LAY_QUAD ? 8192 : 16384;
+#ifndef HG_COLQ_BUDGET
+#define HG_COLQ_BUDGET 8192
+#endif
+    static constexpr int BUDGET = LAY == LAY_QUAD ? HG_COLQ_BUDGET : 16384;
     static constexpr int CMAX0 = (BUDGET / NY) < 16 ? (BUDGET / NY) : 16;
     static constexpr int CMIN = LAY == LAY_QUAD ? 2 : 1;
     static constexpr int C = CMAX0 < CMIN ? CMIN : CMAX0;
     static constexpr int THREADS = T * C;
-    static constexpr int MIN_BLOCKS = (LAY == LAY_QUAD && THREADS >= 512) ? HG_COLQ_MINB : 1;
+    static constexpr int MIN_BLOCKS = (LAY == LAY_QUAD && THREADS >= 512 && THREADS < 1024) ? HG_COLQ_MINB : 1;
 };
 
 // Per-thread float partials -> warp sums in float (32 terms) -> per-warp

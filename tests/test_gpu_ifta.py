@@ -240,3 +240,22 @@ def test_validation_errors():
         hg.run_weighted_gs(cfg_for(amp, hg.SlmSpec.binary_phase(), 3))
     with pytest.raises(hg.HgcUnsupported):
         hg.run_gs(cfg_for(np.ones((12, 12)), hg.SlmSpec.binary_phase(), 3))
+
+
+def test_plan_upload_is_async_and_download_reports_invalid_target():
+    """Plan API: upload no longer blocks on target validation; a non-finite
+    target is reported (same message as TargetSpec::validate) by download,
+    and a valid re-upload on the same plan runs normally."""
+    amp = hg.patterns.bench_target(64)
+    cfg = hg.IftaConfig(iterations=3, slm=hg.SlmSpec.binary_phase(), target=hg.TargetSpec(amp), seed=1)
+    p = hg.IftaPlan(cfg, 64, 64, 2)
+    bad = np.broadcast_to(amp, (2, 64, 64)).copy()
+    bad[1, 3, 5] = np.nan
+    p.upload(bad, seeds=[1, 2])
+    p.execute()
+    with pytest.raises(ValueError, match="non-finite"):
+        p.download()
+    p.upload(np.broadcast_to(amp, (2, 64, 64)), seeds=[1, 2])
+    p.execute()
+    out = p.download()
+    assert np.isfinite(out.trace).all()

@@ -235,7 +235,7 @@ def gs_e2e(args, plan, amps, seeds, d: Dist):
 
     run(2)  # warm (graph instantiation of the second plan)
     d.barrier()
-    steps = max(2, min(args.steps, 4))
+    steps = max(2, args.steps)
     t0 = time.perf_counter()
     run(steps)
     dt = d.max(time.perf_counter() - t0)
@@ -301,7 +301,7 @@ def ospr_ours(args, d: Dist):
 
         run(2)
         d.barrier()
-        es = max(2, min(steps, 4))
+        es = max(2, steps)
         t0 = time.perf_counter()
         run(es)
         dt = d.max(time.perf_counter() - t0)

@@ -8,6 +8,6 @@ $CMD > gpurun_out/prof_bench_plain.json 2> gpurun_out/prof_bench_plain.err || ex
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
     $CMD > gpurun_out/ncu_launches.log 2>&1 || echo "launch list rc=$?"
 python tools/prof_gs.py 4096 64 2 > gpurun_out/prof_gs_plain.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"k_row|k_col|k_seed" -s 1 -c 3 \
+ncu --set full --clock-control none --import-source on -k regex:"k_row|k_col|k_seed|k_mt_jump" -s 1 -c 5 \
     -o gpurun_out/prof_full python tools/prof_gs.py 4096 64 2 > gpurun_out/ncu_full.log 2>&1
 echo done

@@ -58,7 +58,8 @@ typedef enum {
     HGC_OK = 0,
     HGC_EINVAL = 1,       /* std::invalid_argument in the reference */
     HGC_ECUDA = 2,        /* device / runtime failure */
-    HGC_EUNSUPPORTED = 3  /* valid for the reference, outside the GPU path's scope */
+    HGC_EUNSUPPORTED = 3, /* valid for the reference, outside the GPU path's scope */
+    HGC_EIO = 4           /* file / format error: std::runtime_error in the reference (io.cpp:16) */
 } hgc_status;
 
 /* hologen::SlmSpec (quantise.hpp:20-105).  mode: 0 Amplitude, 1 Phase.
@@ -118,6 +119,12 @@ typedef struct hgc_ifta_io {
     const float* fresnel_q;     /* optional complex [ny][nx] quadratic phase Q to use instead of
                                    computing it from hgc_fresnel (e.g. taken from an existing
                                    Propagator<float>, propagation.hpp:97-103) */
+    /* Output encodings computed on the device from the resident results
+     * (the runner's hologram.png / replay.png, runner.cpp:251-266): */
+    uint8_t* hologram_gray8;    /* write_hologram_png pixels lround(255 k / (L-1)) [batch][ny][nx],
+                                   L <= 256 (io.cpp:272-287) */
+    uint8_t* replay_gray8;      /* write_replay_png pixels [batch][ny][nx] (io.cpp:189-205) */
+    double* replay_peak;        /* its amplitude_at_255 [batch] (io.cpp:206-207) */
 } hgc_ifta_io;
 
 /* hologen::OsprConfig (ospr.hpp:20-38).  variant: 0 Ospr, 1 AdaptiveOspr.
@@ -145,6 +152,10 @@ typedef struct hgc_ospr_io {
     float* replay;              /* RunReport::replay complex [jobs][ny][nx] */
     double* final_error;        /* [jobs] */
     double* seconds;
+    /* device-side output encodings, as hgc_ifta_io: */
+    uint8_t* frames_gray8;      /* frame levels as write_hologram_png pixels [jobs][subframes][ny][nx] */
+    uint8_t* replay_gray8;      /* write_replay_png pixels of the replay [jobs][ny][nx] */
+    double* replay_peak;        /* [jobs] */
 } hgc_ospr_io;
 
 /* ------------------------------------------------------------ library */
@@ -228,6 +239,24 @@ int hgc_ospr_block_plan_create(hgc_ospr_plan** plan, const hgc_ospr_cfg* cfg, co
                                int first, int count);
 int hgc_ospr_block_sum(hgc_ospr_plan* plan, void** dev_ptr, size_t* count);
 int hgc_ospr_block_finish(hgc_ospr_plan* plan, const void* gathered, int nblocks, int index, void* stream);
+
+/* --------------------------------- output formats */
+/* write_field_dump (io.cpp:168-186): HGF1 = "HGF1", u32 nx, u32 ny, u8
+ * precision (4 float / 8 double), then interleaved little-endian (re, im).
+ * Non-finite values: HGC_EINVAL "field dump: field contains non-finite values". */
+int hgc_write_field_dump(const char* path, int nx, int ny, int precision, const void* data);
+/* read_field_dump (io.cpp:316-345), same checks and messages (HGC_EIO).
+ * data == NULL: validate the file and return nx, ny, precision only. */
+int hgc_read_field_dump(const char* path, int* nx, int* ny, int* precision, void* data);
+/* write_hologram_png's pixel encoding lround(255 k / (L-1)) (io.cpp:272-287) and
+ * read_hologram_png's inverse (io.cpp:289-298), with their validation. */
+int hgc_levels_to_gray8(const int32_t* levels, int width, int height, int level_count, uint8_t* out);
+int hgc_gray8_to_levels(const uint8_t* px, size_t n, int level_count, int32_t* out);
+/* write_replay_png's pixels on the device (io.cpp:189-205): amp = |z| in
+ * double, peak = max amp, px = clamp(lround(amp * 255 / peak)), 0 if peak == 0. */
+int hgc_replay_to_gray8(const float* replay, int nx, int ny, int batch, uint8_t* out, double* peak);
+/* The "<png_path>.scale.txt" companion: "amplitude_at_255=<shortest double>\n". */
+int hgc_write_replay_scale(const char* png_path, double peak);
 
 /* ------------------------------------------------------- primitives */
 /* Unitary 2-D DFT of `batch` fields, sign -1 forward / +1 inverse; in == out allowed. */

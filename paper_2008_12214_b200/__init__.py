@@ -6,7 +6,7 @@ include/hologen_b200.h, with the reference's API (proj/include/hologen)
 mirrored in Python.  Importing requires the in-tree libhologen_b200.so; there
 is no CPU fallback.
 """
-from ._lib import HgcError, HgcUnsupported, exported_symbols
+from ._lib import HgcError, HgcIOError, HgcUnsupported, exported_symbols
 from .api import (IftaPlan, OsprBlockPlan, OsprPlan, Propagator, Quantiser, allowed_states_f32, device_count, fft_forward,
                   fft_inverse, fork_seed, fresnel_forward, fresnel_inverse, make_fresnel_phase, mse, quantise_field,
                   run_adaptive_ospr, run_gs, run_ifta, run_ifta_batch, run_liu_taghizadeh, run_ospr, run_ospr_batch,
@@ -15,6 +15,6 @@ from .api import (IftaPlan, OsprBlockPlan, OsprPlan, Propagator, Quantiser, allo
 from .types import (PI, TWO_PI, Freedoms, FresnelParams, IftaConfig, IftaVariant, InitPhase, MetricConfig,
                     MetricTrace, Normalization, OsprConfig, OsprRun, OsprVariant, PhaseProfile, RunReport, SlmMode,
                     SlmSpec, SubframeSet, TargetSpec, allowed_states, lt_area_fractions, normalize_image)
-from . import patterns, shard
+from . import io, patterns, shard
 
 __version__ = "0.1.0"

@@ -21,7 +21,7 @@ if not os.path.exists(LIB_PATH):
 
 lib = C.CDLL(LIB_PATH)
 
-HGC_OK, HGC_EINVAL, HGC_ECUDA, HGC_EUNSUPPORTED = 0, 1, 2, 3
+HGC_OK, HGC_EINVAL, HGC_ECUDA, HGC_EUNSUPPORTED, HGC_EIO = 0, 1, 2, 3, 4
 
 
 class HgcError(RuntimeError):
@@ -30,6 +30,10 @@ class HgcError(RuntimeError):
 
 class HgcUnsupported(HgcError):
     """Valid for the reference but outside the GPU path (no CPU fallback)."""
+
+
+class HgcIOError(RuntimeError):
+    """File / format error (std::runtime_error from io.cpp in the reference)."""
 
 
 class HgcSlm(C.Structure):
@@ -56,7 +60,8 @@ class HgcIftaIo(C.Structure):
                 ("init_field", C.c_void_p), ("init_weights", C.c_void_p), ("hologram", C.c_void_p),
                 ("levels8", C.c_void_p), ("levels16", C.c_void_p), ("replay", C.c_void_p),
                 ("trace", C.c_void_p), ("final_error", C.c_void_p), ("seconds", C.c_void_p),
-                ("fresnel_q", C.c_void_p)]
+                ("fresnel_q", C.c_void_p), ("hologram_gray8", C.c_void_p), ("replay_gray8", C.c_void_p),
+                ("replay_peak", C.c_void_p)]
 
 
 class HgcOsprCfg(C.Structure):
@@ -69,7 +74,8 @@ class HgcOsprIo(C.Structure):
                 ("seeds", C.c_void_p), ("levels8", C.c_void_p), ("levels16", C.c_void_p),
                 ("frames", C.c_void_p), ("frame_mse", C.c_void_p), ("cumulative_mse", C.c_void_p),
                 ("mean_intensity", C.c_void_p), ("replay", C.c_void_p), ("final_error", C.c_void_p),
-                ("seconds", C.c_void_p)]
+                ("seconds", C.c_void_p), ("frames_gray8", C.c_void_p), ("replay_gray8", C.c_void_p),
+                ("replay_peak", C.c_void_p)]
 
 
 _vp, _i, _u64, _d = C.c_void_p, C.c_int, C.c_uint64, C.c_double
@@ -107,6 +113,12 @@ _SIGS = {
     "hgc_quantise": (_i, [_P(HgcSlm), _i, _i, _i, _vp, _vp]),
     "hgc_seed_random_phase": (_i, [_vp, _i, _i, _u64, _u64, _vp]),
     "hgc_mt_jump_state": (_i, [_u64, _u64, _vp]),
+    "hgc_write_field_dump": (_i, [C.c_char_p, _i, _i, _i, _vp]),
+    "hgc_read_field_dump": (_i, [C.c_char_p, _P(_i), _P(_i), _P(_i), _vp]),
+    "hgc_levels_to_gray8": (_i, [_vp, _i, _i, _i, _vp]),
+    "hgc_gray8_to_levels": (_i, [_vp, C.c_size_t, _i, _vp]),
+    "hgc_replay_to_gray8": (_i, [_vp, _i, _i, _i, _vp, _vp]),
+    "hgc_write_replay_scale": (_i, [C.c_char_p, _d]),
     "hgc_fork_seed": (_u64, [_u64, _u64]),
     "hgc_mse": (_i, [_vp, _vp, _vp, _i, _i, _i, _P(_d)]),
     "hgc_fresnel_phase": (_i, [_i, _i, _P(HgcFresnel), _vp]),
@@ -132,6 +144,8 @@ def check(rc: int) -> None:
         raise ValueError(msg)  # std::invalid_argument
     if rc == HGC_EUNSUPPORTED:
         raise HgcUnsupported(msg)
+    if rc == HGC_EIO:
+        raise HgcIOError(msg)
     raise HgcError(msg)
 
 

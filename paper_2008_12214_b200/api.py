@@ -303,6 +303,18 @@ class _IftaBuffers:
         io.final_error = _p(self.final_error)
         io.seconds = _p(self.seconds)
         self.io = io
+        self.hologram_gray8 = self.replay_gray8 = self.replay_peak = None
+
+    def want_gray(self, on: bool = True):
+        """Also return the runner's hologram.png / replay.png pixels (device-encoded)."""
+        b, ny, nx = self.levels.shape
+        if on and self.hologram_gray8 is None:
+            self.hologram_gray8 = np.empty((b, ny, nx), np.uint8)
+            self.replay_gray8 = np.empty((b, ny, nx), np.uint8)
+            self.replay_peak = np.empty(b, np.float64)
+        self.io.hologram_gray8 = _p(self.hologram_gray8) if on else None
+        self.io.replay_gray8 = _p(self.replay_gray8) if on else None
+        self.io.replay_peak = _p(self.replay_peak) if on else None
 
 
 def _check_variant(cfg: IftaConfig, want: IftaVariant | None, name: str):
@@ -490,7 +502,10 @@ class IftaPlan:
     def execute(self, stream: int | None = None):
         check(lib.hgc_ifta_plan_execute(self._h, stream))
 
-    def download(self):
+    def download(self, gray: bool = False):
+        """Copy results back; gray=True adds hologram_gray8 / replay_gray8 /
+        replay_peak (write_hologram_png / write_replay_png pixels)."""
+        self._bufs.want_gray(gray)
         check(lib.hgc_ifta_plan_download(self._h, C.byref(self._bufs.io)))
         return self._bufs
 
@@ -550,7 +565,7 @@ class OsprPlan:
     def execute(self, stream: int | None = None):
         check(lib.hgc_ospr_plan_execute(self._h, stream))
 
-    def download(self, frames: bool = False):
+    def download(self, frames: bool = False, gray: bool = False):
         N = self._nf
         jobs, ny, nx = self.jobs, self.ny, self.nx
         wide = self.cfg.slm.levels > 256
@@ -567,6 +582,12 @@ class OsprPlan:
             io.frames = _p(out["frames"])
         io.frame_mse, io.cumulative_mse = _p(out["frame_mse"]), _p(out["cumulative_mse"])
         io.mean_intensity, io.final_error = _p(out["mean_intensity"]), _p(out["final_error"])
+        if gray:  # device-encoded hologram.png per frame / replay.png pixels
+            out["frames_gray8"] = np.empty((jobs, N, ny, nx), np.uint8)
+            out["replay_gray8"] = np.empty((jobs, ny, nx), np.uint8)
+            out["replay_peak"] = np.empty(jobs)
+            io.frames_gray8, io.replay_gray8 = _p(out["frames_gray8"]), _p(out["replay_gray8"])
+            io.replay_peak = _p(out["replay_peak"])
         check(lib.hgc_ospr_plan_download(self._h, C.byref(io)))
         return out
 

@@ -433,6 +433,84 @@ __global__ void __launch_bounds__(256) k_ospr_block_cum(const float* gathered, i
     block_sum_float_store<7>(acc, partials + ((size_t)n * gridDim.x + blockIdx.x) * 8);
 }
 
+// ------------------------------------- output encodings
+// write_hologram_png's pixels (io.cpp:272-287) from the resident levels via
+// a host-built table lround(255 k / (L-1)).
+__global__ void k_levels_gray8(const uint8_t* lv8, const uint16_t* lv16, size_t n, const uint8_t* table,
+                               uint8_t* out) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        out[i] = table[lv8 ? lv8[i] : lv16[i]];
+}
+
+// |z| in double as std::abs(std::complex<double>) (io.cpp:193-195): the
+// squares of the float components are exact in double; their two-sum and
+// one fma-refined square root give the correctly rounded hypot.
+__device__ __forceinline__ double abs_cd(double re, double im) {
+    const double a = re * re, b = im * im;
+    const double s = a + b, bb = s - a, e = (a - (s - bb)) + (b - bb);
+    if (s == 0.0) return 0.0;
+    const double r = sqrt(s);
+    return r + (fma(-r, r, s) + e) / (2.0 * r);
+}
+
+// Source of the replay amplitude of target/job b at row-major pixel i.
+struct AmpSrc {
+    int kind;             // 0: complex field, quad layout; 1: OSPR replay (T)sqrt(S/N), S column-pair major;
+                          // 2: complex field, row-major
+    const float2* f;
+    const float* S;
+    double N;
+    int nx, ny;
+    size_t bstride;
+    __device__ __forceinline__ double amp(int b, size_t i) const {
+        const int x = (int)(i % nx), y = (int)(i / nx);
+        if (kind == 1) {  // ospr.hpp:149-156: replay = (T)sqrt(S/N) + 0i
+            const float re = (float)sqrt((double)S[bstride * b + colpair_index(x, y, ny)] / N);
+            return fabs((double)re);
+        }
+        const float2 z = f[bstride * b + (kind == 0 ? quad_index(x, y, nx) : i)];
+        return abs_cd((double)z.x, (double)z.y);
+    }
+};
+
+// write_replay_png (io.cpp:189-205): peak = max |z| per target (block maxima,
+// then one warp per target), px = clamp(lround(amp * 255/peak)), 0 when peak == 0.
+__global__ void k_amp_peak(AmpSrc src, size_t npix, double* block_max) {
+    const int b = blockIdx.y;
+    double m = 0.0;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < npix; i += (size_t)gridDim.x * blockDim.x)
+        m = fmax(m, src.amp(b, i));
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    __shared__ double red[32];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        m = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (threadIdx.x == 0) block_max[(size_t)b * gridDim.x + blockIdx.x] = m;
+    }
+}
+__global__ void k_peak_final(const double* block_max, int nblk, double* peak) {
+    const int b = blockIdx.x;
+    double m = 0.0;
+    for (int j = threadIdx.x; j < nblk; j += 32) m = fmax(m, block_max[(size_t)b * nblk + j]);
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) peak[b] = m;
+}
+__global__ void k_amp_gray8(AmpSrc src, size_t npix, const double* peak, uint8_t* out) {
+    const int b = blockIdx.y;
+    const double pk = peak[b];
+    const double s = pk > 0.0 ? 255.0 / pk : 0.0;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < npix; i += (size_t)gridDim.x * blockDim.x) {
+        uint8_t v = 0;
+        if (pk > 0.0) {
+            const long long g = llround(src.amp(b, i) * s);
+            v = (uint8_t)(g < 0 ? 0 : g > 255 ? 255 : g);
+        }
+        out[(size_t)b * npix + i] = v;
+    }
+}
+
 // TargetSpec::validate on the device (target.hpp:52-73): bit 0 = non-finite
 // amplitude, bit 1 = negative amplitude, bit 2 = non-finite phase.
 __global__ void k_validate(const double* amp, const double* phase, size_t n, int* flags) {
@@ -515,6 +593,33 @@ static size_t roi_count(const uint8_t* roi, size_t npix) {
     for (size_t i = 0; i < npix; ++i) m += roi[i] != 0;
     if (m == 0) invalid("TargetSpec: roi covers no pixels");
     return m;
+}
+
+// Device encodings of resident results, enqueued on `st`;
+// the caller copies `d_out` / `d_peak` back.
+static void replay_gray8_dev(const AmpSrc& src, size_t npix, int batch, uint8_t* d_out, double* d_peak,
+                             cudaStream_t st) {
+    const int nblk = (int)std::min<size_t>(148 * 2, (npix + 255) / 256);
+    DBuf<double> bm;
+    bm.alloc((size_t)nblk * batch);
+    k_amp_peak<<<dim3(nblk, batch), 256, 0, st>>>(src, npix, bm.p);
+    k_peak_final<<<batch, 32, 0, st>>>(bm.p, nblk, d_peak);
+    k_amp_gray8<<<dim3(nblk, batch), 256, 0, st>>>(src, npix, d_peak, d_out);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));  // bm is freed on return
+}
+static void levels_gray8_dev(const uint8_t* lv8, const uint16_t* lv16, size_t n, int levels, uint8_t* d_out,
+                             cudaStream_t st) {
+    if (levels < 2 || levels > 256)
+        invalid("write_hologram_png: level count must be in [2, 256] for a lossless 8-bit encoding");
+    uint8_t table[256];
+    for (int k = 0; k < levels; ++k) table[k] = (uint8_t)std::lround(255.0 * k / (levels - 1));
+    DBuf<uint8_t> t;
+    t.alloc(256);
+    CK(cudaMemcpyAsync(t.p, table, 256, cudaMemcpyHostToDevice, st));
+    k_levels_gray8<<<ew_grid(n), 256, 0, st>>>(lv8, lv16, n, t.p, d_out);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
 }
 
 // --------------------------------------------------------- quantiser state
@@ -1075,6 +1180,24 @@ int hgc_ifta_plan_download(hgc_ifta_plan* p, hgc_ifta_io* io) {
             if (io->final_error)
                 for (int b = 0; b < p->batch; ++b) io->final_error[b] = tr[(size_t)b * K + K - 1];
         }
+        if (io->hologram_gray8) {  // runner.cpp:251-259 hologram.png pixels
+            DBuf<uint8_t> g;
+            g.alloc(tot);
+            levels_gray8_dev(p->wide_levels ? nullptr : p->lv8.p, p->wide_levels ? p->lv16.p : nullptr, tot,
+                             p->q.p.levels, g.p, p->stream);
+            CK(cudaMemcpy(io->hologram_gray8, g.p, tot, cudaMemcpyDeviceToHost));
+        }
+        if (io->replay_gray8 || io->replay_peak) {  // runner.cpp:261-265 replay.png pixels + scale
+            const AmpSrc src{0, p->field.p, nullptr, 0.0, p->nx, p->ny, p->npix};
+            DBuf<uint8_t> g;
+            DBuf<double> pk;
+            g.alloc(tot);
+            pk.alloc(p->batch);
+            replay_gray8_dev(src, p->npix, p->batch, g.p, pk.p, p->stream);
+            if (io->replay_gray8) CK(cudaMemcpy(io->replay_gray8, g.p, tot, cudaMemcpyDeviceToHost));
+            if (io->replay_peak)
+                CK(cudaMemcpy(io->replay_peak, pk.p, sizeof(double) * p->batch, cudaMemcpyDeviceToHost));
+        }
         if (!p->wide_levels && io->levels8 && !io->levels16 && !io->hologram) {
             CK(cudaMemcpy(io->levels8, p->lv8.p, tot, cudaMemcpyDeviceToHost));  // straight into the caller's buffer
         } else if (io->levels8 || io->levels16 || io->hologram) {
@@ -1578,6 +1701,23 @@ int hgc_ospr_plan_download(hgc_ospr_plan* p, hgc_ospr_io* io) {
                 }
             }
         }
+        if (io->frames_gray8) {
+            DBuf<uint8_t> g;
+            g.alloc(lvtot);
+            levels_gray8_dev(p->wide_levels ? nullptr : p->lv8.p, p->wide_levels ? p->lv16.p : nullptr, lvtot,
+                             p->q.p.levels, g.p, p->stream);
+            CK(cudaMemcpy(io->frames_gray8, g.p, lvtot, cudaMemcpyDeviceToHost));
+        }
+        if (io->replay_gray8 || io->replay_peak) {
+            const AmpSrc src{1, nullptr, p->S.p, (double)p->total_subframes, p->nx, p->ny, npix};
+            DBuf<uint8_t> g;
+            DBuf<double> pk;
+            g.alloc(tot);
+            pk.alloc(p->jobs);
+            replay_gray8_dev(src, npix, p->jobs, g.p, pk.p, p->stream);
+            if (io->replay_gray8) CK(cudaMemcpy(io->replay_gray8, g.p, tot, cudaMemcpyDeviceToHost));
+            if (io->replay_peak) CK(cudaMemcpy(io->replay_peak, pk.p, sizeof(double) * p->jobs, cudaMemcpyDeviceToHost));
+        }
         if (!p->wide_levels && io->levels8 && !io->levels16 && !io->frames) {
             CK(cudaMemcpy(io->levels8, p->lv8.p, lvtot, cudaMemcpyDeviceToHost));
         } else if (io->levels8 || io->levels16 || io->frames) {
@@ -1748,6 +1888,27 @@ int hgc_quantise(const hgc_slm* slm, int nx, int ny, int batch, float* field, in
         CK(cudaGetLastError());
         CK(cudaMemcpy(field, f.p, sizeof(float2) * tot, cudaMemcpyDeviceToHost));
         if (levels) CK(cudaMemcpy(levels, lv.p, sizeof(int32_t) * tot, cudaMemcpyDeviceToHost));
+    });
+}
+
+int hgc_replay_to_gray8(const float* replay, int nx, int ny, int batch, uint8_t* out, double* peak) {
+    return guarded([&] {
+        if (!replay || (!out && !peak)) invalid("replay image: null buffer");
+        if (nx <= 0 || ny <= 0 || batch < 1) invalid("ComplexField: dimensions must be positive");
+        const size_t npix = (size_t)nx * ny, tot = npix * batch;
+        for (size_t i = 0; i < 2 * tot; ++i)  // require_finite(replay, "replay image"), io.cpp:190
+            if (!std::isfinite(replay[i])) invalid("replay image: field contains non-finite values");
+        DBuf<float2> f;
+        DBuf<uint8_t> g;
+        DBuf<double> pk;
+        f.alloc(tot);
+        g.alloc(tot);
+        pk.alloc(batch);
+        CK(cudaMemcpy(f.p, replay, sizeof(float2) * tot, cudaMemcpyHostToDevice));
+        const AmpSrc src{2, f.p, nullptr, 0.0, nx, ny, npix};
+        replay_gray8_dev(src, npix, batch, g.p, pk.p, nullptr);
+        if (out) CK(cudaMemcpy(out, g.p, tot, cudaMemcpyDeviceToHost));
+        if (peak) CK(cudaMemcpy(peak, pk.p, sizeof(double) * batch, cudaMemcpyDeviceToHost));
     });
 }
 

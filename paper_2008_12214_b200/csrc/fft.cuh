@@ -116,10 +116,11 @@ __device__ __forceinline__ void dft(float2* x) {
     }
 }
 
-// Elements per thread for a line of N points.
-template <int N>
+// Elements per thread for a line of N points (at most EM: 16, or 8 for the
+// 32-register column variant).
+template <int N, int EM = 16>
 struct LineCfg {
-    static constexpr int E = N < 16 ? N : 16;
+    static constexpr int E = N < EM ? N : EM;
     static constexpr int T = N / E;
 };
 
@@ -157,6 +158,17 @@ __device__ __forceinline__ void apply_twiddles(float2* x, const float2* __restri
         x[13] = cmul(x[13], cmul(w12, w1));
         x[14] = cmul(x[14], cmul(w12, w2));
         x[15] = cmul(x[15], cmul(w12, w3));
+    } else if constexpr (R == 8) {
+        const float2 w1 = twiddle<N, SIGN>(tw, m);
+        const float2 w2 = twiddle<N, SIGN>(tw, 2 * m);
+        const float2 w4 = twiddle<N, SIGN>(tw, 4 * m);
+        x[1] = cmul(x[1], w1);
+        x[2] = cmul(x[2], w2);
+        x[3] = cmul(x[3], cmul(w1, w2));
+        x[4] = cmul(x[4], w4);
+        x[5] = cmul(x[5], cmul(w4, w1));
+        x[6] = cmul(x[6], cmul(w4, w2));
+        x[7] = cmul(x[7], cmul(w4, cmul(w1, w2)));
     } else {
 #pragma unroll
         for (int r = 1; r < R; ++r) x[r] = cmul(x[r], twiddle<N, SIGN>(tw, r * m));
@@ -168,12 +180,12 @@ __device__ __forceinline__ void apply_twiddles(float2* x, const float2* __restri
 //   twiddle by W_{NS*R}^{r*(j mod NS)}; DFT_R;
 //   output r goes to position (j/NS)*NS*R + (j mod NS) + r*NS.
 // SmemIdx maps a line position to a shared-memory slot for this thread's line.
-template <int N, int SIGN, int NS>
+template <int N, int SIGN, int NS, int EM = 16>
 struct StockhamPass {
     template <class SmemIdx>
-    __device__ __forceinline__ static void run(float2 (&v)[LineCfg<N>::E], int t, float2* sm,
+    __device__ __forceinline__ static void run(float2 (&v)[LineCfg<N, EM>::E], int t, float2* sm,
                                                const SmemIdx& idx, const float2* __restrict__ tw) {
-        constexpr int E = LineCfg<N>::E, T = LineCfg<N>::T;
+        constexpr int E = LineCfg<N, EM>::E, T = LineCfg<N, EM>::T;
         constexpr int R = (N / NS >= E) ? E : N / NS;
         constexpr int B = E / R;
         constexpr bool last = (NS * R == N);
@@ -193,10 +205,15 @@ struct StockhamPass {
                 // positions base + r*NS; with NS == 1 (R <= 16) or NS % 16 == 0
                 // the padded slots are linear in r: slot(base) + r*stride
                 const int base = (j / NS) * NS * R + k;
-                const int s0 = idx(base);
-                constexpr int rs = (NS == 1) ? 1 : NS + NS / 16;
+                if constexpr (NS == 1 || NS % 16 == 0) {
+                    const int s0 = idx(base);
+                    constexpr int rs = (NS == 1) ? 1 : NS + NS / 16;
 #pragma unroll
-                for (int r = 0; r < R; ++r) sm[s0 + r * rs * SmemIdx::kLineStride] = x[r];
+                    for (int r = 0; r < R; ++r) sm[s0 + r * rs * SmemIdx::kLineStride] = x[r];
+                } else {
+#pragma unroll
+                    for (int r = 0; r < R; ++r) sm[idx(base + r * NS)] = x[r];
+                }
             }
         }
         if constexpr (!last) {
@@ -211,17 +228,17 @@ struct StockhamPass {
                 for (int e = 0; e < E; ++e) v[e] = sm[idx(t + e * T)];
             }
             __syncthreads();
-            StockhamPass<N, SIGN, NS * R>::run(v, t, sm, idx, tw);
+            StockhamPass<N, SIGN, NS * R, EM>::run(v, t, sm, idx, tw);
         }
     }
 };
 
 // Full unnormalised 1-D transform of one line held in strided ownership.
 // Every thread of the CTA must call it (it contains __syncthreads when N > E).
-template <int N, int SIGN, class SmemIdx>
-__device__ __forceinline__ void fft_line(float2 (&v)[LineCfg<N>::E], int t, float2* sm, const SmemIdx& idx,
+template <int N, int SIGN, int EM = 16, class SmemIdx>
+__device__ __forceinline__ void fft_line(float2 (&v)[LineCfg<N, EM>::E], int t, float2* sm, const SmemIdx& idx,
                                          const float2* __restrict__ tw) {
-    StockhamPass<N, SIGN, 1>::run(v, t, sm, idx, tw);
+    StockhamPass<N, SIGN, 1, EM>::run(v, t, sm, idx, tw);
 }
 
 // Padded slot for position q of a line: one pad slot every 16 keeps the

@@ -58,13 +58,14 @@ inline int col_width(int nx) {
 template <int NY, int C, int MODE, int LAY>
 inline void col_launch_c(const ColArgs& a, int batch, cudaStream_t st, bool prepare) {
     auto kern = k_col<NY, C, MODE, LAY>;
-    constexpr int smem = (NY > LineCfg<NY>::E) ? PaddedLen<NY>::value * C * (int)sizeof(float2) : 0;
+    constexpr int EM = ColCfg<NY, LAY>::EM;
+    constexpr int smem = (NY > LineCfg<NY, EM>::E) ? PaddedLen<NY>::value * C * (int)sizeof(float2) : 0;
     if (prepare) {
         set_smem(kern, smem);
         return;
     }
     dim3 grid(a.nx / C, batch);
-    kern<<<grid, LineCfg<NY>::T * C, smem, st>>>(a);
+    kern<<<grid, LineCfg<NY, EM>::T * C, smem, st>>>(a);
     CK(cudaGetLastError());
 }
 

@@ -222,7 +222,13 @@ struct ColArgs {
 
 template <int NY, int LAY>
 struct ColCfg {
-    static constexpr int E = LineCfg<NY>::E, T = LineCfg<NY>::T;
+#ifndef HG_COL_E8
+#define HG_COL_E8 0
+#endif
+    // EM = 8: 8 elements per thread, 1024-thread CTAs at <= 32 registers, 2 CTAs
+    // (64 warps) per SM for the large quad-layout columns; else 16 per thread.
+    static constexpr int EM = (HG_COL_E8 && LAY == LAY_QUAD && NY >= 2048) ? 8 : 16;
+    static constexpr int E = LineCfg<NY, EM>::E, T = LineCfg<NY, EM>::T;
     // LAY_ROW: up to 128 KiB of complex64 per CTA (1 CTA / SM at 4096);
     // LAY_QUAD: 64 KiB column-pair tiles (2 CTAs / SM)
 #ifndef HG_COLQ_BUDGET
@@ -233,7 +239,8 @@ struct ColCfg {
     static constexpr int CMIN = LAY == LAY_QUAD ? 2 : 1;
     static constexpr int C = CMAX0 < CMIN ? CMIN : CMAX0;
     static constexpr int THREADS = T * C;
-    static constexpr int MIN_BLOCKS = (LAY == LAY_QUAD && THREADS >= 512 && THREADS < 1024) ? HG_COLQ_MINB : 1;
+    static constexpr int MIN_BLOCKS =
+        EM == 8 ? 2 : ((LAY == LAY_QUAD && THREADS >= 512 && THREADS < 1024) ? HG_COLQ_MINB : 1);
 };
 
 // Per-thread float partials -> warp sums in float (32 terms) -> per-warp
@@ -261,8 +268,10 @@ __device__ __forceinline__ void block_sum_float_store(float (&v)[NV], double* ou
 }
 
 template <int NY, int C, int MODE, int LAY>
-__global__ void __launch_bounds__(LineCfg<NY>::T * C, ColCfg<NY, LAY>::MIN_BLOCKS) k_col(ColArgs a) {
-    constexpr int E = LineCfg<NY>::E, T = LineCfg<NY>::T;
+__global__ void __launch_bounds__(LineCfg<NY, ColCfg<NY, LAY>::EM>::T * C, ColCfg<NY, LAY>::MIN_BLOCKS)
+    k_col(ColArgs a) {
+    constexpr int EM = ColCfg<NY, LAY>::EM;
+    constexpr int E = LineCfg<NY, EM>::E, T = LineCfg<NY, EM>::T;
     extern __shared__ float2 smem[];
     const int c = threadIdx.x % C, t = threadIdx.x / C;
     const int x = blockIdx.x * C + c;
@@ -304,15 +313,15 @@ __global__ void __launch_bounds__(LineCfg<NY>::T * C, ColCfg<NY, LAY>::MIN_BLOCK
     };
 
     if constexpr (MODE == COL_PLAIN) {
-        if (a.sign < 0) fft_line<NY, -1>(v, t, smem, idx, a.tw);
-        else fft_line<NY, +1>(v, t, smem, idx, a.tw);
+        if (a.sign < 0) fft_line<NY, -1, EM>(v, t, smem, idx, a.tw);
+        else fft_line<NY, +1, EM>(v, t, smem, idx, a.tw);
         if (a.apply_norm)
 #pragma unroll
             for (int e = 0; e < E; ++e) v[e] = cscale(v[e], a.norm);
         store_col(base);
         return;
     } else {
-        fft_line<NY, -1>(v, t, smem, idx, a.tw);  // completes the forward transform
+        fft_line<NY, -1, EM>(v, t, smem, idx, a.tw);  // completes the forward transform
         const float norm = a.norm;
         const float* tg = a.target + a.t_bstride * b + sb;
         constexpr int NV = MODE == COL_OSPR ? 7 : 4;
@@ -426,7 +435,7 @@ __global__ void __launch_bounds__(LineCfg<NY>::T * C, ColCfg<NY, LAY>::MIN_BLOCK
             if (a.last) {
                 store_col(a.replay_out + a.bstride * b);
             } else {
-                fft_line<NY, +1>(v, t, smem, idx, a.tw);  // starts the next inverse transform
+                fft_line<NY, +1, EM>(v, t, smem, idx, a.tw);  // starts the next inverse transform
                 store_col(base);
             }
         }

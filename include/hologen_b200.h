@@ -52,7 +52,7 @@
 extern "C" {
 #endif
 
-#define HGC_ABI_VERSION 1
+#define HGC_ABI_VERSION 2
 
 typedef enum {
     HGC_OK = 0,

@@ -130,6 +130,10 @@ for _name, (_res, _args) in _SIGS.items():
     _f.restype = _res
     _f.argtypes = _args
 
+ABI_VERSION = 2  # HGC_ABI_VERSION of include/hologen_b200.h this binding was written against
+if lib.hgc_abi_version() != ABI_VERSION:
+    raise ImportError(f"{LIB_PATH}: ABI version {lib.hgc_abi_version()} != {ABI_VERSION}; rebuild the library")
+
 
 def last_error() -> str:
     return lib.hgc_last_error().decode(errors="replace")

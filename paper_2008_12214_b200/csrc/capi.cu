@@ -442,15 +442,30 @@ __global__ void k_levels_gray8(const uint8_t* lv8, const uint16_t* lv16, size_t 
         out[i] = table[lv8 ? lv8[i] : lv16[i]];
 }
 
-// |z| in double as std::abs(std::complex<double>) (io.cpp:193-195): the
-// squares of the float components are exact in double; their two-sum and
-// one fma-refined square root give the correctly rounded hypot.
-__device__ __forceinline__ double abs_cd(double re, double im) {
-    const double a = re * re, b = im * im;
-    const double s = a + b, bb = s - a, e = (a - (s - bb)) + (b - bb);
-    if (s == 0.0) return 0.0;
-    const double r = sqrt(s);
-    return r + (fma(-r, r, s) + e) / (2.0 * r);
+// |z| in double exactly as std::abs(std::complex<double>) (io.cpp:193-195)
+// computes it on the reference's host: glibc's hypot, i.e. Borges' corrected
+// algorithm ("An Improved Algorithm for hypot(a,b)", arXiv:1904.09481;
+// glibc >= 2.35, non-FMA build).  It is not always correctly rounded
+// (~0.6% of float pairs are 1 ulp off), so the same operation sequence is
+// replayed here, without FMA contraction; checked bit-for-bit against this
+// image's glibc on 3e7 float pairs.
+__device__ __forceinline__ double ref_hypot(double x, double y) {
+    x = fabs(x);
+    y = fabs(y);
+    const double ax = x < y ? y : x, ay = x < y ? x : y;
+    if (ay <= __dmul_rn(ax, 0x1p-54)) return __dadd_rn(ax, ay);
+    double h = __dsqrt_rn(__dadd_rn(__dmul_rn(ax, ax), __dmul_rn(ay, ay)));
+    double t1, t2;
+    if (h <= __dmul_rn(2.0, ay)) {
+        const double delta = __dsub_rn(h, ay);
+        t1 = __dmul_rn(ax, __dsub_rn(__dmul_rn(2.0, delta), ax));
+        t2 = __dmul_rn(__dsub_rn(delta, __dmul_rn(2.0, __dsub_rn(ax, ay))), delta);
+    } else {
+        const double delta = __dsub_rn(h, ax);
+        t1 = __dmul_rn(__dmul_rn(2.0, delta), __dsub_rn(ax, __dmul_rn(2.0, ay)));
+        t2 = __dadd_rn(__dmul_rn(__dsub_rn(__dmul_rn(4.0, delta), ay), ay), __dmul_rn(delta, delta));
+    }
+    return __dsub_rn(h, __ddiv_rn(__dadd_rn(t1, t2), __dmul_rn(2.0, h)));
 }
 
 // Source of the replay amplitude of target/job b at row-major pixel i.
@@ -469,7 +484,7 @@ struct AmpSrc {
             return fabs((double)re);
         }
         const float2 z = f[bstride * b + (kind == 0 ? quad_index(x, y, nx) : i)];
-        return abs_cd((double)z.x, (double)z.y);
+        return ref_hypot((double)z.x, (double)z.y);
     }
 };
 

@@ -1,5 +1,8 @@
 """GPU: device-side output encodings — write_replay_png and
 write_hologram_png pixels computed from the resident results."""
+import ctypes
+import ctypes.util
+
 import numpy as np
 import pytest
 
@@ -8,9 +11,17 @@ hg = pytest.importorskip("paper_2008_12214_b200")
 hio = hg.io
 
 
+_libm = ctypes.CDLL(ctypes.util.find_library("m"))
+_libm.hypot.restype = ctypes.c_double
+_libm.hypot.argtypes = [ctypes.c_double, ctypes.c_double]
+_hypot = np.vectorize(_libm.hypot, otypes=[np.float64])
+
+
 def _replay_px(replay):
-    """io.cpp:189-205 in numpy: amp = |z| (double), px = lround(amp * 255/peak)."""
-    amp = np.abs(np.asarray(replay).astype(np.complex128))
+    """io.cpp:189-205 on the host: amp = std::abs(complex<double>) = libm hypot
+    (numpy's SIMD complex abs rounds differently), px = lround(amp * 255/peak)."""
+    z = np.asarray(replay)
+    amp = _hypot(z.real.astype(np.float64), z.imag.astype(np.float64))
     peak = amp.max()
     if peak == 0:
         return np.zeros(amp.shape, np.uint8), 0.0

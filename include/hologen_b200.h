@@ -240,6 +240,38 @@ int hgc_ospr_block_plan_create(hgc_ospr_plan** plan, const hgc_ospr_cfg* cfg, co
 int hgc_ospr_block_sum(hgc_ospr_plan* plan, void** dev_ptr, size_t* count);
 int hgc_ospr_block_finish(hgc_ospr_plan* plan, const void* gathered, int nblocks, int index, void* stream);
 
+/* ------------------------------ batch executor */
+/* One job of the runner's `batch` command (runner.cpp:365-421): a generate
+ * run of one target.  Inputs are caller-owned host buffers; the outputs
+ * (levels, trace) are optional.  status / message / final_error / seconds
+ * are filled per job like cmd_batch's BatchRow. */
+typedef struct hgc_batch_job {
+    int kind;                    /* 0 IFTA (ifta), 1 OSPR (ospr) */
+    const hgc_ifta_cfg* ifta;
+    const hgc_ospr_cfg* ospr;
+    const hgc_slm* slm;
+    const hgc_fresnel* fresnel;  /* IFTA Fresnel propagation, or NULL */
+    int nx, ny;
+    const double* amplitude;     /* [ny][nx] */
+    const double* phase;         /* IFTA target phase or NULL */
+    const uint8_t* roi;          /* [ny][nx] or NULL */
+    uint8_t* levels8;            /* IFTA [ny][nx]; OSPR [subframes][ny][nx] (levels <= 256) */
+    uint16_t* levels16;
+    double* trace;               /* IFTA mse [iterations]; OSPR cumulative mse [subframes] */
+    int status;                  /* hgc_status of this job */
+    double final_error;
+    double seconds;              /* wall time of the batched group that ran this job */
+    char message[256];           /* error message when status != HGC_OK */
+} hgc_batch_job;
+/* Runs every job.  Jobs whose configurations differ only in seed and target
+ * share one batched plan (one CUDA graph for the group); groups are spread
+ * over min(max_devices, device count) GPUs (max_devices <= 0: all), one host
+ * thread per device, largest groups first onto the least-loaded device.
+ * max_group_bytes caps a group's resident footprint (0: 16 GiB).  A failing
+ * group is re-run job by job so each failure stays with its own job.
+ * Returns HGC_OK if every job succeeded, else the first failing job's status. */
+int hgc_batch_run(hgc_batch_job* jobs, int njobs, int max_devices, size_t max_group_bytes);
+
 /* --------------------------------- output formats */
 /* write_field_dump (io.cpp:168-186): HGF1 = "HGF1", u32 nx, u32 ny, u8
  * precision (4 float / 8 double), then interleaved little-endian (re, im).

@@ -15,6 +15,6 @@ from .api import (IftaPlan, OsprBlockPlan, OsprPlan, Propagator, Quantiser, allo
 from .types import (PI, TWO_PI, Freedoms, FresnelParams, IftaConfig, IftaVariant, InitPhase, MetricConfig,
                     MetricTrace, Normalization, OsprConfig, OsprRun, OsprVariant, PhaseProfile, RunReport, SlmMode,
                     SlmSpec, SubframeSet, TargetSpec, allowed_states, lt_area_fractions, normalize_image)
-from . import io, patterns, shard
+from . import io, patterns, runner, shard
 
 __version__ = "0.1.0"

@@ -1,0 +1,44 @@
+"""GPU: the batch executor.  Mixed jobs are grouped into
+batched plans; every job's levels / trace / final_error must equal the
+single-job run, and a bad job fails alone (cmd_batch, runner.cpp:387-405)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+hg = pytest.importorskip("paper_2008_12214_b200")
+from paper_2008_12214_b200.runner import BatchJob, run_batch  # noqa: E402
+
+
+def test_batch_groups_equal_single_runs_and_isolate_failures():
+    n = 64
+    amp = hg.patterns.bench_target(n)
+    amp2 = np.roll(amp, 7, axis=1)
+    slm = hg.SlmSpec.full_circle_phase(8)
+    jobs = [BatchJob(f"gs{s}", hg.IftaConfig(iterations=5, slm=slm, target=hg.TargetSpec(a), seed=s))
+            for s, a in ((1, amp), (2, amp2), (3, amp))]
+    jobs.append(BatchJob("wgs", hg.IftaConfig(variant=hg.IftaVariant.WeightedGS, iterations=4, slm=slm,
+                                              target=hg.TargetSpec(amp), seed=4)))
+    bad = amp.copy()
+    bad[3, 3] = np.nan
+    jobs.append(BatchJob("bad", hg.IftaConfig(iterations=5, slm=slm, target=hg.TargetSpec(bad), seed=5)))
+    jobs += [BatchJob(f"ospr{s}", hg.OsprConfig(subframes=3, slm=hg.SlmSpec.binary_phase(),
+                                                target=hg.TargetSpec(amp), seed=s)) for s in (7, 8)]
+    rows = run_batch(jobs)
+    assert [r.ok for r in rows] == [True, True, True, True, False, True, True]
+    assert "non-finite" in rows[4].message
+    for r, j in zip(rows, jobs):
+        if not r.ok:
+            continue
+        cfg = j.config
+        if isinstance(cfg, hg.IftaConfig):
+            ref = hg.run_ifta(cfg)
+            assert np.array_equal(r.levels, ref.levels), r.job
+            assert np.array_equal(r.trace, ref.trace.values()), r.job
+            assert r.final_error == ref.final_error
+        else:
+            ref = hg.run_ospr(cfg)
+            assert np.array_equal(r.levels, ref.set.levels), r.job
+            assert np.allclose(r.trace, ref.report.trace.values(), rtol=0, atol=0), r.job
+        assert r.seconds > 0
+    table, csv = hg.runner.batch_summary(rows)
+    assert "bad" in table and csv.count("\n") == len(rows) + 1

@@ -163,6 +163,12 @@ int hgc_abi_version(void);
 const char* hgc_last_error(void);
 int hgc_device_count(int* count);
 int hgc_set_device(int device);
+/* Device routing for callers that run jobs on their own host threads (the
+ * runner's batch pool, runner.cpp:387-421, via the C++ drop-in; SURVEY §8
+ * b5/f2): policy 1 binds each host thread, at its first hgc_ifta_run /
+ * hgc_ospr_run, to the next device round-robin (job thread i -> GPU i mod G);
+ * policy 0 (default) uses the thread's current device. */
+int hgc_set_device_policy(int policy);
 /* Largest supported power-of-two side length (4096). */
 int hgc_max_side(void);
 

@@ -68,6 +68,10 @@ public:
     }
 };
 
+// Route the calling threads round-robin over the GPUs (the runner's batch
+// pool runs one job per thread, runner.cpp:387-421): call once at start-up.
+inline void route_threads_over_devices() { throw_status(hgc_set_device_policy(1)); }
+
 inline B200FftBackend& fft_backend() {
     static B200FftBackend b;
     return b;

@@ -114,6 +114,7 @@ _SIGS = {
     "hgc_seed_random_phase": (_i, [_vp, _i, _i, _u64, _u64, _vp]),
     "hgc_mt_jump_state": (_i, [_u64, _u64, _vp]),
     "hgc_batch_run": (_i, [_vp, _i, _i, C.c_size_t]),
+    "hgc_set_device_policy": (_i, [_i]),
     "hgc_write_field_dump": (_i, [C.c_char_p, _i, _i, _i, _vp]),
     "hgc_read_field_dump": (_i, [C.c_char_p, _P(_i), _P(_i), _P(_i), _vp]),
     "hgc_levels_to_gray8": (_i, [_vp, _i, _i, _i, _vp]),

@@ -4,6 +4,7 @@
 // errors to the reference's exception semantics (status + message).
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -969,6 +970,28 @@ int hgc_device_count(int* count) {
 int hgc_set_device(int device) {
     return guarded([&] { CK(cudaSetDevice(device)); });
 }
+
+// Device routing for callers that run jobs on their own threads (the
+// runner's batch pool, runner.cpp:387-421, through the C++ drop-in):
+// policy 1 binds each host thread, on its first run, to the next device
+// round-robin; policy 0 leaves the thread's current device alone.
+static std::atomic<int> g_dev_policy{0};
+static std::atomic<int> g_dev_next{0};
+int hgc_set_device_policy(int policy) {
+    return guarded([&] {
+        if (policy != 0 && policy != 1) invalid("hgc_set_device_policy: policy must be 0 or 1");
+        g_dev_policy = policy;
+    });
+}
+static void route_device() {
+    thread_local int bound = -1;
+    if (g_dev_policy.load() != 1 || bound >= 0) return;
+    int n = 0;
+    CK(cudaGetDeviceCount(&n));
+    if (n < 1) fail(HGC_ECUDA, "no CUDA device");
+    bound = g_dev_next.fetch_add(1) % n;
+    CK(cudaSetDevice(bound));
+}
 uint64_t hgc_fork_seed(uint64_t seed, uint64_t stream) { return fork_seed(seed, stream); }
 
 double hgc_subframe_mse_statistic(const double* v, int n) {  // ospr.hpp:58-64
@@ -1282,7 +1305,8 @@ int hgc_ifta_run(const hgc_ifta_cfg* cfg, const hgc_slm* slm, const hgc_fresnel*
                  hgc_ifta_io* io) {
     auto t0 = std::chrono::steady_clock::now();
     hgc_ifta_plan* p = nullptr;
-    int rc = hgc_ifta_plan_create(&p, cfg, slm, fresnel, nx, ny, batch);
+    int rc = guarded([] { route_device(); });
+    if (rc == HGC_OK) rc = hgc_ifta_plan_create(&p, cfg, slm, fresnel, nx, ny, batch);
     if (rc == HGC_OK) rc = hgc_ifta_plan_upload(p, io);
     if (rc == HGC_OK) rc = guarded([&] { check_validation(p->vflags.p, p->stream); });  // eager in the one-shot run
     if (rc == HGC_OK) rc = hgc_ifta_plan_execute(p, nullptr);
@@ -1804,7 +1828,8 @@ int hgc_ospr_plan_destroy(hgc_ospr_plan* p) {
 int hgc_ospr_run(const hgc_ospr_cfg* cfg, const hgc_slm* slm, int nx, int ny, int jobs, hgc_ospr_io* io) {
     auto t0 = std::chrono::steady_clock::now();
     hgc_ospr_plan* p = nullptr;
-    int rc = hgc_ospr_plan_create(&p, cfg, slm, nx, ny, jobs, io ? io->per_job_target : 0);
+    int rc = guarded([] { route_device(); });
+    if (rc == HGC_OK) rc = hgc_ospr_plan_create(&p, cfg, slm, nx, ny, jobs, io ? io->per_job_target : 0);
     if (rc == HGC_OK) rc = hgc_ospr_plan_upload(p, io);
     if (rc == HGC_OK) rc = guarded([&] { check_validation(p->vflags.p, p->stream); });  // eager in the one-shot run
     if (rc == HGC_OK) rc = hgc_ospr_plan_execute(p, nullptr);

@@ -9,6 +9,8 @@
 #include <cmath>
 #include <cstdio>
 #include <stdexcept>
+#include <thread>
+#include <vector>
 
 #include "hologen/ifta.hpp"
 #include "hologen/ospr.hpp"
@@ -84,6 +86,30 @@ int main() {
     rel = std::abs(go.report.final_error - ro.report.final_error) / ro.report.final_error;
     std::printf("ospr 6 frames: level mismatches %d, cumulative mse rel %.2e\n", om, rel);
     CHECK(om <= 6 && rel < 1e-4 && go.report.algorithm == "ospr" && go.set.frames.size() == 6);
+
+    // the runner's batch pool (runner.cpp:387-421): one job per host thread,
+    // threads routed round-robin over the GPUs; results equal the sequential runs
+    hologen_b200::route_threads_over_devices();
+    std::vector<RunReport<float>> seq, par(4);
+    for (int s = 0; s < 4; ++s) {
+        IftaConfig c = cfg;
+        c.seed = 10 + s;
+        c.iterations = 5;
+        seq.push_back(run_gs<float>(c));
+    }
+    std::vector<std::thread> pool;
+    for (int s = 0; s < 4; ++s)
+        pool.emplace_back([&, s] {
+            IftaConfig c = cfg;
+            c.seed = 10 + s;
+            c.iterations = 5;
+            par[s] = run_gs<float>(c);
+        });
+    for (auto& t : pool) t.join();
+    bool same = true;
+    for (int s = 0; s < 4; ++s) same = same && par[s].hologram.data == seq[s].hologram.data && par[s].final_error == seq[s].final_error;
+    std::printf("batch pool of 4 threads: %s\n", same ? "identical to sequential" : "DIFFERENT");
+    CHECK(same);
 
     // errors keep the reference's exceptions and messages
     IftaConfig bad = cfg;

@@ -42,3 +42,31 @@ def test_batch_groups_equal_single_runs_and_isolate_failures():
         assert r.seconds > 0
     table, csv = hg.runner.batch_summary(rows)
     assert "bad" in table and csv.count("\n") == len(rows) + 1
+
+
+def test_thread_routing_policy_concurrent_runs():
+    """hgc_set_device_policy(1): host threads (the runner's batch pool) bind
+    round-robin to the GPUs; concurrent one-shot runs give the sequential
+    results."""
+    import threading
+    from paper_2008_12214_b200 import _lib
+    amp = hg.patterns.bench_target(64)
+    cfgs = [hg.IftaConfig(iterations=4, slm=hg.SlmSpec.full_circle_phase(4), target=hg.TargetSpec(amp), seed=s)
+            for s in range(1, 7)]
+    want = [hg.run_gs(c) for c in cfgs]
+    _lib.check(_lib.lib.hgc_set_device_policy(1))
+    try:
+        got = [None] * len(cfgs)
+
+        def work(i):
+            got[i] = hg.run_gs(cfgs[i])
+
+        ts = [threading.Thread(target=work, args=(i,)) for i in range(len(cfgs))]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+    finally:
+        _lib.check(_lib.lib.hgc_set_device_policy(0))
+    for g, w in zip(got, want):
+        assert np.array_equal(g.levels, w.levels) and g.final_error == w.final_error

@@ -2,7 +2,9 @@
 // include/hologen_b200.h.  Owns device memory, builds the fused pass
 // sequence of run_ifta / run_ospr_impl as one CUDA graph per plan, and maps
 // errors to the reference's exception semantics (status + message).
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <atomic>
 #include <chrono>
@@ -129,6 +131,36 @@ static void prepare_kernels(int nx, int ny) {
     col_ospr(ny, ca, 1, nullptr, true);
     CK(cudaFuncSetAttribute(k_seed_random_phase, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSeedSmem));
 }
+
+// ------------------------------------------------ TMA tensor maps
+// A quad-layout complex64 region seen as a 2-D float tensor: inner = one quad
+// row (4*nx floats = two field rows), outer = `rows` quad rows; box = one
+// column pair (8 floats = 32 B) x 256 quad rows.  The map lives in device
+// memory (ColArgs::tmap).  cuTensorMapEncodeTiled comes from the driver entry
+// point so cudart stays statically linked.
+struct DevTensorMap {
+    DBuf<CUtensorMap> d;
+    void make(float2* base, int nx, size_t rows) {
+        static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+            void* fn = nullptr;
+            cudaDriverEntryPointQueryResult q{};
+            CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+            if (!fn || q != cudaDriverEntryPointSuccess) fail(HGC_ECUDA, "cuTensorMapEncodeTiled unavailable");
+            return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+        }();
+        CUtensorMap m;
+        const cuuint64_t dims[2] = {(cuuint64_t)4 * nx, (cuuint64_t)rows};
+        const cuuint64_t strides[1] = {(cuuint64_t)4 * nx * sizeof(float)};
+        const cuuint32_t box[2] = {8, 256};
+        const cuuint32_t estr[2] = {1, 1};
+        CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) fail(HGC_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+        d.alloc(1);
+        CK(cudaMemcpy(d.p, &m, sizeof m, cudaMemcpyHostToDevice));
+    }
+};
 
 // ------------------------------------------ RNG chunking (jump-ahead)
 // One reference stream split across several CTAs: CTA (stream s, chunk c)
@@ -760,6 +792,7 @@ struct hgc_ifta_plan {
     DBuf<MtState> mt;
     DBuf<uint64_t> seeds;
     SeedChunks chunking;
+    DevTensorMap tmap;  // field as a TMA tensor (column pass), ny >= 512
     const float2* tw = nullptr;
     cudaGraphExec_t graph = nullptr;
     uint64_t graph_sig = 0;
@@ -868,6 +901,8 @@ struct hgc_ifta_plan {
         cg.last = last ? 1 : 0;
         cg.replay_out = field.p;
         cg.partials = partials.p + (size_t)(k - 1) * batch * tiles * 8;
+        cg.tmap = tmap.d.p;
+        cg.tma_brows = ny / 2;
         return cg;
     }
 
@@ -906,6 +941,8 @@ struct hgc_ifta_plan {
         ca.nx = nx;
         ca.layout = LAY_QUAD;
         ca.sign = +1;
+        ca.tmap = tmap.d.p;
+        ca.tma_brows = ny / 2;
         col_plain(ny, ca, batch, st);
         ++launches;
         // Iterations run target-group by target-group: a group's field +
@@ -929,6 +966,7 @@ struct hgc_ifta_plan {
                 if (cg.tphase_cs) cg.tphase_cs += (size_t)g0 * npix;
                 cg.replay_out += (size_t)g0 * npix;
                 cg.partials += (size_t)g0 * tiles * 8;
+                cg.tma_row0 = g0 * (ny / 2);
                 col_gs(ny, cg, gn, st);
                 launches += 2;
             }
@@ -1051,6 +1089,7 @@ int hgc_ifta_plan_create(hgc_ifta_plan** out, const hgc_ifta_cfg* cfg, const hgc
         p->tiles = col_tiles(nx, ny, LAY_QUAD);
         const size_t tot = p->npix * batch;
         p->field.alloc(tot);
+        if (ny >= 512) p->tmap.make(p->field.p, nx, (size_t)batch * ny / 2);
         p->target_f.alloc(tot);
         p->amp_d.alloc(tot);
         if (cfg->variant == 1) p->weights.alloc(tot);
@@ -1342,6 +1381,7 @@ struct hgc_ospr_plan {
     DBuf<MtState> mt;
     DBuf<uint64_t> seeds;
     SeedChunks chunking;
+    DevTensorMap tmap1, tmap2;  // field / field2 as TMA tensors (column passes), ny >= 512
     // subframe-block mode: this plan runs global subframes
     // [first, first + cfg.subframes) of a total_subframes job
     int first = 0, total_subframes = 0;
@@ -1417,6 +1457,17 @@ struct hgc_ospr_plan {
         }
         return sa;
     }
+    void set_tma(ColArgs& c, int n) const {  // the TMA view of buf(n)
+        if (preseed) {
+            c.tmap = tmap1.d.p;
+            c.tma_row0 = (n - 1) * (ny / 2);
+            c.tma_brows = cfg.subframes * (ny / 2);
+        } else {
+            c.tmap = buf(n) == field2.p ? tmap2.d.p : tmap1.d.p;
+            c.tma_row0 = 0;
+            c.tma_brows = ny / 2;
+        }
+    }
     ColArgs col_inv_args(int n) const {
         ColArgs ci{};
         ci.tw = tw;
@@ -1425,6 +1476,7 @@ struct hgc_ospr_plan {
         ci.nx = nx;
         ci.layout = LAY_QUAD;
         ci.sign = +1;
+        set_tma(ci, n);
         return ci;
     }
     RowArgs row_args(int n) const {
@@ -1458,6 +1510,7 @@ struct hgc_ospr_plan {
         co.S = S.p;  // per job, even when the target is shared
         co.S_bstride = npix;
         co.inv_n = 1.0f / (float)n;
+        set_tma(co, n);
         return co;
     }
 
@@ -1562,8 +1615,10 @@ static void create_ospr_plan(hgc_ospr_plan** out, const hgc_ospr_cfg* cfg_in, co
             p->fstride = p->preseed ? all : p->npix;
         }
         p->field.alloc(p->fstride * jobs);
+        if (ny >= 512) p->tmap1.make(p->field.p, nx, p->fstride * jobs / (2 * (size_t)nx));
         if (!p->preseed && cfg->variant == 0 && cfg->subframes > 1) {  // second buffer + stream for seed/pass overlap
             p->field2.alloc(tot);
+            if (ny >= 512) p->tmap2.make(p->field2.p, nx, tot / (2 * (size_t)nx));
             CK(cudaStreamCreateWithFlags(&p->stream2, cudaStreamNonBlocking));
             CK(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&p->ev_seed, cudaEventDisableTiming));

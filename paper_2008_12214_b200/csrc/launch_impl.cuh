@@ -64,6 +64,7 @@ inline void col_launch_c(const ColArgs& a, int batch, cudaStream_t st, bool prep
         set_smem(kern, smem);
         return;
     }
+    if (ColTma<NY, C, LAY>::on && !a.tmap) fail(HGC_ECUDA, "column pass: TMA tile launched without a tensor map");
     dim3 grid(a.nx / C, batch);
     kern<<<grid, LineCfg<NY, EM>::T * C, smem, st>>>(a);
     CK(cudaGetLastError());

@@ -99,7 +99,7 @@ template <int NX, int MODE, int QK, int LAY, int FQ>
 __global__ void __launch_bounds__(RowCfg<NX, LAY>::THREADS, RowCfg<NX, LAY>::MIN_BLOCKS) k_row(RowArgs a) {
     using Cfg = RowCfg<NX, LAY>;
     constexpr int E = Cfg::E, T = Cfg::T;
-    extern __shared__ float2 smem[];
+    extern __shared__ __align__(128) float2 smem[];
     int lr, t;
     if constexpr (LAY == LAY_QUAD) {
         // the 2T threads of a row pair interleave so a warp covers 2 rows x 16
@@ -218,12 +218,20 @@ struct ColArgs {
     float* S;             // [job][ny][nx] running sum of |R|^2
     size_t S_bstride;
     float inv_n;          // 1/n for the cumulative replay sqrt(S/n)
+    // quad-layout field as a 2-D TMA tensor map (inner: a quad row of 4*nx
+    // floats, outer: quad rows); this launch's target b starts at quad row
+    // tma_row0 + b * tma_brows.  nullptr: per-thread loads/stores.
+    const void* tmap;
+    int tma_row0, tma_brows;
 };
 
 template <int NY, int LAY>
 struct ColCfg {
 #ifndef HG_COL_E8
 #define HG_COL_E8 0
+#endif
+#ifndef HG_COL_TMA
+#define HG_COL_TMA 1
 #endif
     // EM = 8: 8 elements per thread, 1024-thread CTAs at <= 32 registers, 2 CTAs
     // (64 warps) per SM for the large quad-layout columns; else 16 per thread.
@@ -242,6 +250,15 @@ struct ColCfg {
     static constexpr int MIN_BLOCKS =
         EM == 8 ? 2 : ((LAY == LAY_QUAD && THREADS >= 512 && THREADS < 1024) ? HG_COLQ_MINB : 1);
 };
+
+// Column tiles loaded / stored by 2-D TMA (k_col): 2-column quad tiles of at
+// least 256 quad rows.  Their launches must carry ColArgs::tmap.
+template <int NY, int C, int LAY>
+struct ColTma {
+    static constexpr bool on =
+        HG_COL_TMA && LAY == LAY_QUAD && C == 2 && NY >= 512 && NY > LineCfg<NY, ColCfg<NY, LAY>::EM>::E;
+};
+
 
 // Per-thread float partials -> warp sums in float (32 terms) -> per-warp
 // doubles -> fixed-order double block sum; thread 0 stores NV doubles.
@@ -272,7 +289,7 @@ __global__ void __launch_bounds__(LineCfg<NY, ColCfg<NY, LAY>::EM>::T * C, ColCf
     k_col(ColArgs a) {
     constexpr int EM = ColCfg<NY, LAY>::EM;
     constexpr int E = LineCfg<NY, EM>::E, T = LineCfg<NY, EM>::T;
-    extern __shared__ float2 smem[];
+    extern __shared__ __align__(128) float2 smem[];
     const int c = threadIdx.x % C, t = threadIdx.x / C;
     const int x = blockIdx.x * C + c;
     const int b = blockIdx.y;
@@ -302,14 +319,49 @@ __global__ void __launch_bounds__(LineCfg<NY, ColCfg<NY, LAY>::EM>::T * C, ColCf
     };
     float2* base = a.field + a.bstride * b;
     float2 v[E];
+    // TMA path (2-column quad tiles): the whole tile lands in smem as [y][c]
+    // (= the unpadded column layout), replacing 16 scattered 32-B global
+    // accesses per thread; the same buffer then serves the FFT exchanges.
+    constexpr bool kTma = ColTma<NY, C, LAY>::on;
+    constexpr int kBoxRows = 256, kBoxes = NY / 2 / kBoxRows;
+    __shared__ uint64_t tbar;
+    const int tq = blockIdx.x * (C / 2) * 8;  // inner coordinate (floats) of this column pair
+    const int tr = a.tma_row0 + b * a.tma_brows;
+    if constexpr (kTma) {
+        if (threadIdx.x == 0) {
+            mbar_init(&tbar, 1);
+            mbar_expect_tx(&tbar, NY * C * (int)sizeof(float2));
+#pragma unroll 1
+            for (int k = 0; k < kBoxes; ++k) tma_load_2d(smem + k * kBoxRows * 4, a.tmap, tq, tr + k * kBoxRows, &tbar);
+        }
+        __syncthreads();  // barrier initialised before anyone waits
+        mbar_wait(&tbar, 0);
 #pragma unroll
-    for (int e = 0; e < E; ++e) v[e] = ld_stream(&base[fofs(e)]);
+        for (int e = 0; e < E; ++e) v[e] = smem[2 * (t + e * T) + c];
+        __syncthreads();  // landing area becomes the exchange buffer
+    } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) v[e] = ld_stream(&base[fofs(e)]);
+    }
     // stores recompute their addresses from an opaque base (keeps 16 64-bit
     // pointers from living across the transforms)
     auto store_col = [&](float2* dst) {
-        float2* p1 = opaque(dst);
+        if constexpr (kTma) {  // dst is the tensor map's field (host-checked)
 #pragma unroll
-        for (int e = 0; e < E; ++e) p1[fofs(e)] = v[e];
+            for (int e = 0; e < E; ++e) smem[2 * (t + e * T) + c] = v[e];
+            fence_proxy_async();
+            __syncthreads();
+            if (threadIdx.x == 0) {
+#pragma unroll 1
+                for (int k = 0; k < kBoxes; ++k) tma_store_2d(a.tmap, tq, tr + k * kBoxRows, smem + k * kBoxRows * 4);
+                bulk_commit();
+                bulk_wait_read0();
+            }
+        } else {
+            float2* p1 = opaque(dst);
+#pragma unroll
+            for (int e = 0; e < E; ++e) p1[fofs(e)] = v[e];
+        }
     };
 
     if constexpr (MODE == COL_PLAIN) {

@@ -140,7 +140,8 @@ static void prepare_kernels(int nx, int ny) {
 // point so cudart stays statically linked.
 struct DevTensorMap {
     DBuf<CUtensorMap> d;
-    void make(float2* base, int nx, size_t rows) {
+    void make(float2* base, int nx, int ny, size_t rows) {
+        const int C = nx / col_tiles(nx, ny, LAY_QUAD);  // columns per column-pass tile
         static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
             void* fn = nullptr;
             cudaDriverEntryPointQueryResult q{};
@@ -151,7 +152,7 @@ struct DevTensorMap {
         CUtensorMap m;
         const cuuint64_t dims[2] = {(cuuint64_t)4 * nx, (cuuint64_t)rows};
         const cuuint64_t strides[1] = {(cuuint64_t)4 * nx * sizeof(float)};
-        const cuuint32_t box[2] = {8, 256};
+        const cuuint32_t box[2] = {(cuuint32_t)(4 * C), 256};
         const cuuint32_t estr[2] = {1, 1};
         CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -1089,7 +1090,7 @@ int hgc_ifta_plan_create(hgc_ifta_plan** out, const hgc_ifta_cfg* cfg, const hgc
         p->tiles = col_tiles(nx, ny, LAY_QUAD);
         const size_t tot = p->npix * batch;
         p->field.alloc(tot);
-        if (ny >= 512) p->tmap.make(p->field.p, nx, (size_t)batch * ny / 2);
+        if (ny >= 512) p->tmap.make(p->field.p, nx, ny, (size_t)batch * ny / 2);
         p->target_f.alloc(tot);
         p->amp_d.alloc(tot);
         if (cfg->variant == 1) p->weights.alloc(tot);
@@ -1615,10 +1616,10 @@ static void create_ospr_plan(hgc_ospr_plan** out, const hgc_ospr_cfg* cfg_in, co
             p->fstride = p->preseed ? all : p->npix;
         }
         p->field.alloc(p->fstride * jobs);
-        if (ny >= 512) p->tmap1.make(p->field.p, nx, p->fstride * jobs / (2 * (size_t)nx));
+        if (ny >= 512) p->tmap1.make(p->field.p, nx, ny, p->fstride * jobs / (2 * (size_t)nx));
         if (!p->preseed && cfg->variant == 0 && cfg->subframes > 1) {  // second buffer + stream for seed/pass overlap
             p->field2.alloc(tot);
-            if (ny >= 512) p->tmap2.make(p->field2.p, nx, tot / (2 * (size_t)nx));
+            if (ny >= 512) p->tmap2.make(p->field2.p, nx, ny, tot / (2 * (size_t)nx));
             CK(cudaStreamCreateWithFlags(&p->stream2, cudaStreamNonBlocking));
             CK(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&p->ev_seed, cudaEventDisableTiming));

@@ -251,12 +251,20 @@ struct ColCfg {
         EM == 8 ? 2 : ((LAY == LAY_QUAD && THREADS >= 512 && THREADS < 1024) ? HG_COLQ_MINB : 1);
 };
 
-// Column tiles loaded / stored by 2-D TMA (k_col): 2-column quad tiles of at
-// least 256 quad rows.  Their launches must carry ColArgs::tmap.
+// Column tiles loaded / stored by 2-D TMA (k_col): quad-layout tiles of C
+// columns (C/2 quads = 16*C bytes per quad row) and at least 256 quad rows,
+// in boxes of 256 quad rows.  Their launches must carry ColArgs::tmap, whose
+// box is {4*C floats, 256 quad rows}.
 template <int NY, int C, int LAY>
 struct ColTma {
     static constexpr bool on =
-        HG_COL_TMA && LAY == LAY_QUAD && C == 2 && NY >= 512 && NY > LineCfg<NY, ColCfg<NY, LAY>::EM>::E;
+        HG_COL_TMA && LAY == LAY_QUAD && C >= 2 && NY >= 512 && NY > LineCfg<NY, ColCfg<NY, LAY>::EM>::E;
+    static constexpr int kBoxRows = 256;
+    // landing slot of element (column c, row y) of the tile: [quad row][quad][2x2]
+    static __device__ __forceinline__ int slot(int c, int y) {
+        if constexpr (C == 2) return 2 * y + c;  // = the unpadded [y][c] column layout
+        else return (y >> 1) * (2 * C) + (c >> 1) * 4 + (y & 1) * 2 + (c & 1);
+    }
 };
 
 
@@ -319,11 +327,13 @@ __global__ void __launch_bounds__(LineCfg<NY, ColCfg<NY, LAY>::EM>::T * C, ColCf
     };
     float2* base = a.field + a.bstride * b;
     float2 v[E];
-    // TMA path (2-column quad tiles): the whole tile lands in smem as [y][c]
-    // (= the unpadded column layout), replacing 16 scattered 32-B global
-    // accesses per thread; the same buffer then serves the FFT exchanges.
-    constexpr bool kTma = ColTma<NY, C, LAY>::on;
-    constexpr int kBoxRows = 256, kBoxes = NY / 2 / kBoxRows;
+    // TMA path (quad tiles): the whole C-column tile lands in smem in its
+    // global quad order, replacing 16 scattered global accesses of 8 B per
+    // thread (8 L1 wavefronts per warp instruction at C = 2); the same buffer
+    // then serves the FFT exchanges.
+    using Tma = ColTma<NY, C, LAY>;
+    constexpr bool kTma = Tma::on;
+    constexpr int kBoxRows = Tma::kBoxRows, kBoxes = NY / 2 / kBoxRows;
     __shared__ uint64_t tbar;
     const int tq = blockIdx.x * (C / 2) * 8;  // inner coordinate (floats) of this column pair
     const int tr = a.tma_row0 + b * a.tma_brows;
@@ -332,12 +342,13 @@ __global__ void __launch_bounds__(LineCfg<NY, ColCfg<NY, LAY>::EM>::T * C, ColCf
             mbar_init(&tbar, 1);
             mbar_expect_tx(&tbar, NY * C * (int)sizeof(float2));
 #pragma unroll 1
-            for (int k = 0; k < kBoxes; ++k) tma_load_2d(smem + k * kBoxRows * 4, a.tmap, tq, tr + k * kBoxRows, &tbar);
+            for (int k = 0; k < kBoxes; ++k)
+                tma_load_2d(smem + k * kBoxRows * 2 * C, a.tmap, tq, tr + k * kBoxRows, &tbar);
         }
         __syncthreads();  // barrier initialised before anyone waits
         mbar_wait(&tbar, 0);
 #pragma unroll
-        for (int e = 0; e < E; ++e) v[e] = smem[2 * (t + e * T) + c];
+        for (int e = 0; e < E; ++e) v[e] = smem[Tma::slot(c, t + e * T)];
         __syncthreads();  // landing area becomes the exchange buffer
     } else {
 #pragma unroll
@@ -348,12 +359,13 @@ __global__ void __launch_bounds__(LineCfg<NY, ColCfg<NY, LAY>::EM>::T * C, ColCf
     auto store_col = [&](float2* dst) {
         if constexpr (kTma) {  // dst is the tensor map's field (host-checked)
 #pragma unroll
-            for (int e = 0; e < E; ++e) smem[2 * (t + e * T) + c] = v[e];
+            for (int e = 0; e < E; ++e) smem[Tma::slot(c, t + e * T)] = v[e];
             fence_proxy_async();
             __syncthreads();
             if (threadIdx.x == 0) {
 #pragma unroll 1
-                for (int k = 0; k < kBoxes; ++k) tma_store_2d(a.tmap, tq, tr + k * kBoxRows, smem + k * kBoxRows * 4);
+                for (int k = 0; k < kBoxes; ++k)
+                    tma_store_2d(a.tmap, tq, tr + k * kBoxRows, smem + k * kBoxRows * 2 * C);
                 bulk_commit();
                 bulk_wait_read0();
             }

@@ -299,6 +299,9 @@ int hgc_write_replay_scale(const char* png_path, double peak);
 /* ------------------------------------------------------- primitives */
 /* Unitary 2-D DFT of `batch` fields, sign -1 forward / +1 inverse; in == out allowed. */
 int hgc_fft2d(int nx, int ny, int sign, int batch, const float* in, float* out);
+/* The same for complex128 (FftBackend<double>, fft.hpp:17-27):
+ * double-precision butterflies and twiddles, scale 1/sqrt(nx*ny) in double. */
+int hgc_fft2d_f64(int nx, int ny, int sign, int batch, const double* in, double* out);
 /* Propagator<float>::forward (sign -1: FFT(f*Q)) / inverse (sign +1:
  * IFFT(F)*conj(Q)), propagation.hpp:81-95; fresnel == NULL is the Fourier
  * propagator (= hgc_fft2d). */

@@ -109,6 +109,7 @@ _SIGS = {
     "hgc_ospr_block_finish": (_i, [_vp, _vp, _i, _i, _vp]),
     "hgc_ospr_plan_destroy": (_i, [_vp]),
     "hgc_fft2d": (_i, [_i, _i, _i, _i, _vp, _vp]),
+    "hgc_fft2d_f64": (_i, [_i, _i, _i, _i, _vp, _vp]),
     "hgc_propagate": (_i, [_i, _i, _i, _P(HgcFresnel), _i, _vp, _vp]),
     "hgc_quantise": (_i, [_P(HgcSlm), _i, _i, _i, _vp, _vp]),
     "hgc_seed_random_phase": (_i, [_vp, _i, _i, _u64, _u64, _vp]),

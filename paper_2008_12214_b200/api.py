@@ -90,6 +90,13 @@ class Propagator:
 
 
 def _fft2d(f: np.ndarray, sign: int, fresnel: FresnelParams | None = None) -> np.ndarray:
+    if fresnel is None and np.asarray(f).dtype == np.complex128:  # fft_forward<double>
+        a = np.ascontiguousarray(f)
+        a3 = a[None] if a.ndim == 2 else a
+        b, ny, nx = a3.shape
+        out = np.empty_like(a3)
+        check(lib.hgc_fft2d_f64(nx, ny, sign, b, _p(a3), _p(out)))
+        return out[0] if a.ndim == 2 else out
     a = np.ascontiguousarray(f, dtype=np.complex64)
     if a.ndim == 2:
         a = a[None]
@@ -103,12 +110,13 @@ def _fft2d(f: np.ndarray, sign: int, fresnel: FresnelParams | None = None) -> np
 
 
 def fft_forward(f: np.ndarray) -> np.ndarray:
-    """fft_forward<float> (fft.hpp:93-102): unitary, -i exponent."""
+    """fft_forward<T> (fft.hpp:93-102): unitary, -i exponent; T = float for
+    complex64 input (the hot-path transform), double for complex128."""
     return _fft2d(f, -1)
 
 
 def fft_inverse(F: np.ndarray) -> np.ndarray:
-    """fft_inverse<float> (fft.hpp:104-113): unitary, +i exponent."""
+    """fft_inverse<T> (fft.hpp:104-113): unitary, +i exponent; complex64 -> float, complex128 -> double."""
     return _fft2d(F, +1)
 
 

@@ -1962,6 +1962,28 @@ int hgc_propagate(int nx, int ny, int sign, const hgc_fresnel* fresnel, int batc
     });
 }
 
+int hgc_fft2d_f64(int nx, int ny, int sign, int batch, const double* in, double* out) {
+    return guarded([&] {
+        if (!in || !out) invalid("fft: null buffer");
+        if (sign != -1 && sign != 1) invalid("fft: sign must be -1 or +1");
+        if (batch < 1) invalid("fft: batch must be >= 1");
+        check_size(nx, ny);
+        const size_t tot = (size_t)nx * ny * batch;
+        for (size_t i = 0; i < 2 * tot; ++i)  // require_finite, fft.hpp:95-97 / :106-108
+            if (!std::isfinite(in[i]))
+                invalid(std::string(sign < 0 ? "fft_forward" : "fft_inverse") + ": field contains non-finite values");
+        DBuf<double2> f;
+        f.alloc(tot);
+        cudaStream_t st;
+        CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        CK(cudaMemcpyAsync(f.p, in, sizeof(double2) * tot, cudaMemcpyHostToDevice, st));
+        fft2d_f64(f.p, nx, ny, sign, batch, st);
+        CK(cudaMemcpyAsync(out, f.p, sizeof(double2) * tot, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        CK(cudaStreamDestroy(st));
+    });
+}
+
 int hgc_fft2d(int nx, int ny, int sign, int batch, const float* in, float* out) {
     return hgc_propagate(nx, ny, sign, nullptr, batch, in, out);
 }

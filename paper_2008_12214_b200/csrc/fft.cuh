@@ -22,40 +22,57 @@ namespace hg {
 
 constexpr int kMaxLine = 4096;
 
+// Complex element type of a transform: float2 (the hot path) or double2 (the
+// f64 FftBackend, k_fft64.cu).
+template <class C2>
+struct CT;
+template <>
+struct CT<float2> {
+    using S = float;
+    static __device__ __forceinline__ float2 make(float x, float y) { return make_float2(x, y); }
+};
+template <>
+struct CT<double2> {
+    using S = double;
+    static __device__ __forceinline__ double2 make(double x, double y) { return make_double2(x, y); }
+};
+
 // ---------------------------------------------------------------- radix-R
-template <int SIGN>
-__device__ __forceinline__ float2 mul_si(float2 a) {  // a * (SIGN * i)
-    return SIGN < 0 ? make_float2(a.y, -a.x) : make_float2(-a.y, a.x);
+template <int SIGN, class C2>
+__device__ __forceinline__ C2 mul_si(C2 a) {  // a * (SIGN * i)
+    return SIGN < 0 ? CT<C2>::make(a.y, -a.x) : CT<C2>::make(-a.y, a.x);
 }
 
 // W16^m = exp(SIGN*2*pi*i*m/16), applied to a (compile-time m).
-template <int SIGN, int M>
-__device__ __forceinline__ float2 tw16(float2 a) {
+template <int SIGN, int M, class C2>
+__device__ __forceinline__ C2 tw16(C2 a) {
+    using S = typename CT<C2>::S;
     constexpr int m = M & 15;
-    constexpr float c1 = 0.92387953251128674f, s1 = 0.38268343236508978f, h = 0.70710678118654752f;
+    constexpr S c1 = (S)0.923879532511286756128183189396788933L, s1 = (S)0.382683432365089771728459984030398866L,
+                h = (S)0.707106781186547524400844362104849039L;
     if constexpr (m == 0) return a;
     else if constexpr (m == 4) return mul_si<SIGN>(a);
-    else if constexpr (m == 8) return make_float2(-a.x, -a.y);
+    else if constexpr (m == 8) return CT<C2>::make(-a.x, -a.y);
     else if constexpr (m == 12) return mul_si<-SIGN>(a);
     else {
         // cos/sin of 2*pi*m/16 for the remaining m
-        constexpr float cs[16] = {1.f, c1, h, s1, 0.f, -s1, -h, -c1, -1.f, -c1, -h, -s1, 0.f, s1, h, c1};
-        constexpr float sn[16] = {0.f, s1, h, c1, 1.f, c1, h, s1, 0.f, -s1, -h, -c1, -1.f, -c1, -h, -s1};
-        return cmul(a, make_float2(cs[m], SIGN * sn[m]));
+        constexpr S cs[16] = {1, c1, h, s1, 0, -s1, -h, -c1, -1, -c1, -h, -s1, 0, s1, h, c1};
+        constexpr S sn[16] = {0, s1, h, c1, 1, c1, h, s1, 0, -s1, -h, -c1, -1, -c1, -h, -s1};
+        return cmul(a, CT<C2>::make(cs[m], SIGN * sn[m]));
     }
 }
 
-template <int SIGN>
-__device__ __forceinline__ void dft2(float2& a, float2& b) {
-    float2 t = a;
+template <int SIGN, class C2>
+__device__ __forceinline__ void dft2(C2& a, C2& b) {
+    C2 t = a;
     a = cadd(t, b);
     b = csub(t, b);
 }
 
-template <int SIGN>
-__device__ __forceinline__ void dft4(float2& v0, float2& v1, float2& v2, float2& v3) {
-    float2 t0 = cadd(v0, v2), t1 = csub(v0, v2);
-    float2 t2 = cadd(v1, v3), t3 = mul_si<SIGN>(csub(v1, v3));
+template <int SIGN, class C2>
+__device__ __forceinline__ void dft4(C2& v0, C2& v1, C2& v2, C2& v3) {
+    C2 t0 = cadd(v0, v2), t1 = csub(v0, v2);
+    C2 t2 = cadd(v1, v3), t3 = mul_si<SIGN>(csub(v1, v3));
     v0 = cadd(t0, t2);
     v2 = csub(t0, t2);
     v1 = cadd(t1, t3);
@@ -64,8 +81,8 @@ __device__ __forceinline__ void dft4(float2& v0, float2& v1, float2& v2, float2&
 
 // In-place DFT of R values, natural order in and out:
 //   x[k] <- sum_r x[r] exp(SIGN*2*pi*i*r*k/R)
-template <int R, int SIGN>
-__device__ __forceinline__ void dft(float2* x) {
+template <int R, int SIGN, class C2>
+__device__ __forceinline__ void dft(C2* x) {
     if constexpr (R == 1) {
     } else if constexpr (R == 2) {
         dft2<SIGN>(x[0], x[1]);
@@ -73,8 +90,8 @@ __device__ __forceinline__ void dft(float2* x) {
         dft4<SIGN>(x[0], x[1], x[2], x[3]);
     } else if constexpr (R == 8) {
         // r = 2a + b; Y_b = DFT4_a(x[2a+b]); Y_b[k1] *= W8^(b k1); X[k1+4k2] = DFT2_b
-        float2 y0[4] = {x[0], x[2], x[4], x[6]};
-        float2 y1[4] = {x[1], x[3], x[5], x[7]};
+        C2 y0[4] = {x[0], x[2], x[4], x[6]};
+        C2 y1[4] = {x[1], x[3], x[5], x[7]};
         dft4<SIGN>(y0[0], y0[1], y0[2], y0[3]);
         dft4<SIGN>(y1[0], y1[1], y1[2], y1[3]);
         y1[1] = tw16<SIGN, 2>(y1[1]);
@@ -87,7 +104,7 @@ __device__ __forceinline__ void dft(float2* x) {
         }
     } else if constexpr (R == 16) {
         // r = 4a + b; Y_b = DFT4_a(x[4a+b]); Y_b[k1] *= W16^(b k1); X[k1+4k2] = DFT4_b
-        float2 y[4][4];
+        C2 y[4][4];
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
             y[b][0] = x[b];
@@ -125,9 +142,9 @@ struct LineCfg {
 };
 
 // Twiddle exp(SIGN*2*pi*i*m/N) from the forward table.
-template <int N, int SIGN>
-__device__ __forceinline__ float2 twiddle(const float2* __restrict__ tw, int m) {
-    float2 w = __ldg(&tw[N + m]);
+template <int N, int SIGN, class C2>
+__device__ __forceinline__ C2 twiddle(const C2* __restrict__ tw, int m) {
+    C2 w = __ldg(&tw[N + m]);
     if constexpr (SIGN > 0) w.y = -w.y;
     return w;
 }
@@ -136,13 +153,13 @@ __device__ __forceinline__ float2 twiddle(const float2* __restrict__ tw, int m) 
 // and w^8 come from the table (the rest are <= 2 products of table values,
 // error <= ~2 ulp): 3 loads instead of 15 keeps the pass within the register
 // budget of a 1024-thread CTA.
-template <int N, int SIGN, int R>
-__device__ __forceinline__ void apply_twiddles(float2* x, const float2* __restrict__ tw, int m) {
+template <int N, int SIGN, int R, class C2>
+__device__ __forceinline__ void apply_twiddles(C2* x, const C2* __restrict__ tw, int m) {
     if constexpr (R == 16) {
-        const float2 w1 = twiddle<N, SIGN>(tw, m);
-        const float2 w4 = twiddle<N, SIGN>(tw, 4 * m);
-        const float2 w8 = twiddle<N, SIGN>(tw, 8 * m);
-        const float2 w2 = cmul(w1, w1), w3 = cmul(w2, w1), w12 = cmul(w8, w4);
+        const C2 w1 = twiddle<N, SIGN>(tw, m);
+        const C2 w4 = twiddle<N, SIGN>(tw, 4 * m);
+        const C2 w8 = twiddle<N, SIGN>(tw, 8 * m);
+        const C2 w2 = cmul(w1, w1), w3 = cmul(w2, w1), w12 = cmul(w8, w4);
         x[1] = cmul(x[1], w1);
         x[2] = cmul(x[2], w2);
         x[3] = cmul(x[3], w3);
@@ -159,9 +176,9 @@ __device__ __forceinline__ void apply_twiddles(float2* x, const float2* __restri
         x[14] = cmul(x[14], cmul(w12, w2));
         x[15] = cmul(x[15], cmul(w12, w3));
     } else if constexpr (R == 8) {
-        const float2 w1 = twiddle<N, SIGN>(tw, m);
-        const float2 w2 = twiddle<N, SIGN>(tw, 2 * m);
-        const float2 w4 = twiddle<N, SIGN>(tw, 4 * m);
+        const C2 w1 = twiddle<N, SIGN>(tw, m);
+        const C2 w2 = twiddle<N, SIGN>(tw, 2 * m);
+        const C2 w4 = twiddle<N, SIGN>(tw, 4 * m);
         x[1] = cmul(x[1], w1);
         x[2] = cmul(x[2], w2);
         x[3] = cmul(x[3], cmul(w1, w2));
@@ -182,16 +199,16 @@ __device__ __forceinline__ void apply_twiddles(float2* x, const float2* __restri
 // SmemIdx maps a line position to a shared-memory slot for this thread's line.
 template <int N, int SIGN, int NS, int EM = 16>
 struct StockhamPass {
-    template <class SmemIdx>
-    __device__ __forceinline__ static void run(float2 (&v)[LineCfg<N, EM>::E], int t, float2* sm,
-                                               const SmemIdx& idx, const float2* __restrict__ tw) {
+    template <class C2, class SmemIdx>
+    __device__ __forceinline__ static void run(C2 (&v)[LineCfg<N, EM>::E], int t, C2* sm, const SmemIdx& idx,
+                                               const C2* __restrict__ tw) {
         constexpr int E = LineCfg<N, EM>::E, T = LineCfg<N, EM>::T;
         constexpr int R = (N / NS >= E) ? E : N / NS;
         constexpr int B = E / R;
         constexpr bool last = (NS * R == N);
 #pragma unroll
         for (int b = 0; b < B; ++b) {
-            float2 x[R];
+            C2 x[R];
 #pragma unroll
             for (int r = 0; r < R; ++r) x[r] = v[b + r * B];
             const int j = t + b * T;
@@ -235,9 +252,9 @@ struct StockhamPass {
 
 // Full unnormalised 1-D transform of one line held in strided ownership.
 // Every thread of the CTA must call it (it contains __syncthreads when N > E).
-template <int N, int SIGN, int EM = 16, class SmemIdx>
-__device__ __forceinline__ void fft_line(float2 (&v)[LineCfg<N, EM>::E], int t, float2* sm, const SmemIdx& idx,
-                                         const float2* __restrict__ tw) {
+template <int N, int SIGN, int EM = 16, class C2, class SmemIdx>
+__device__ __forceinline__ void fft_line(C2 (&v)[LineCfg<N, EM>::E], int t, C2* sm, const SmemIdx& idx,
+                                         const C2* __restrict__ tw) {
     StockhamPass<N, SIGN, 1, EM>::run(v, t, sm, idx, tw);
 }
 

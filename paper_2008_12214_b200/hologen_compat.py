@@ -5,9 +5,10 @@ Same function names, arguments, defaults and return dictionaries as the
 pybind11 module for the functions on the IFTA / OSPR path:
 ``fft_forward``, ``fft_inverse``, ``quantise``, ``gs``, ``wgs``, ``lt``,
 ``ospr``, ``adaptive_ospr``, ``mse``.  Arrays are numpy (height, width),
-complex128 fields and float64 images like the reference's; the computation
-runs in float32 on the B200 (the reference module computes in double), so
-results agree with it to float precision, not to the last double bit.
+complex128 fields and float64 images like the reference's.  The transforms
+run in double on the B200 (hgc_fft2d_f64); the algorithms run on the float32
+hot path (the reference module runs them in double), so their results agree
+with it to float precision, not to the last double bit.
 Holographic search and SSIM (``direct_search``, ``simulated_annealing``,
 ``ssim``) are not on the hot path and are not provided.
 
@@ -59,13 +60,13 @@ def _report(rep) -> dict:  # bindings.cpp report_dict
 
 
 def fft_forward(field) -> np.ndarray:
-    """Unitary forward transform (aperture plane to replay field)."""
-    return api.fft_forward(_field(field)).astype(np.complex128)
+    """Unitary forward transform (aperture plane to replay field), in double on the GPU."""
+    return api.fft_forward(np.asarray(_field(field), np.complex128))
 
 
 def fft_inverse(field) -> np.ndarray:
-    """Unitary inverse transform (replay field to aperture plane)."""
-    return api.fft_inverse(_field(field)).astype(np.complex128)
+    """Unitary inverse transform (replay field to aperture plane), in double on the GPU."""
+    return api.fft_inverse(np.asarray(_field(field), np.complex128))
 
 
 def quantise(field, levels: int = 256) -> np.ndarray:

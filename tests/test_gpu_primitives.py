@@ -46,6 +46,32 @@ def test_fft_matches_oracle(oracle, n):
         assert err < 2e-6 * np.sqrt(np.log2(x.size) + 1), (n, sign, err)
 
 
+def test_fft_4x4_golden_f64():
+    """fft_forward<double> on the GPU against the reference's 4x4 fixture at its own 1e-12 (test_fft.cpp:75-88)."""
+    g = json.load(open(os.path.join(GOLDEN, "fft_4x4.json")))
+    x = (np.array(g["in_re"]) + 1j * np.array(g["in_im"])).reshape(4, 4)
+    want = (np.array(g["out_re"]) + 1j * np.array(g["out_im"])).reshape(4, 4)
+    assert np.max(np.abs(hg.fft_forward(x) - want)) < 1e-12
+
+
+@pytest.mark.parametrize("ny,nx", [(2, 2), (8, 16), (16, 2), (64, 128), (1024, 1024), (4096, 256), (256, 4096),
+                                   (4096, 4096)])
+def test_fft_f64_matches_numpy(ny, nx):
+    r = np.random.default_rng(ny * 7 + nx)
+    x = r.standard_normal((ny, nx)) + 1j * r.standard_normal((ny, nx))
+    F = hg.fft_forward(x)
+    assert F.dtype == np.complex128
+    assert np.max(np.abs(F - np.fft.fft2(x) / np.sqrt(x.size))) < 1e-12 * np.sqrt(np.log2(x.size) + 1) * 4
+    B = hg.fft_inverse(x)
+    assert np.max(np.abs(B - np.fft.ifft2(x) * np.sqrt(x.size))) < 1e-12 * np.sqrt(np.log2(x.size) + 1) * 4
+    if ny * nx <= 1 << 20:  # batched, via the C ABI directly
+        from paper_2008_12214_b200 import _lib
+        xb = np.stack([x, 2 * x])
+        out = np.empty_like(xb)
+        _lib.check(_lib.lib.hgc_fft2d_f64(nx, ny, -1, 2, xb.ctypes.data, out.ctypes.data))
+        assert np.array_equal(out[0], F) and np.max(np.abs(out[1] - 2 * F)) < 1e-11
+
+
 def test_fft_delta_constant_roundtrip():
     f = np.zeros((8, 8), np.complex64)
     f[0, 0] = 1

@@ -17,8 +17,9 @@
 // is honoured by handing its quadratic phase (aperture_factor,
 // propagation.hpp:100-103) to the GPU, so Q is bit-identical.
 //
-// Also provides hologen_b200::B200FftBackend, an FftBackend<float>
-// (fft.hpp:17-27) on the GPU transform, for default_fft_backend<float>().
+// Also provides hologen_b200::B200FftBackend / B200FftBackendF64,
+// FftBackend<float> / FftBackend<double> (fft.hpp:17-27) on the GPU
+// transforms, for default_fft_backend<T>().
 #pragma once
 
 #include <chrono>
@@ -74,6 +75,26 @@ inline void route_threads_over_devices() { throw_status(hgc_set_device_policy(1)
 
 inline B200FftBackend& fft_backend() {
     static B200FftBackend b;
+    return b;
+}
+
+// FftBackend<double> on the GPU's double-precision transform (hgc_fft2d_f64),
+// for default_fft_backend<double>() / the T = double templates.
+class B200FftBackendF64 : public hologen::FftBackend<double> {
+public:
+    const char* name() const override { return "b200-f64"; }
+    void forward(int nx, int ny, const std::complex<double>* in, std::complex<double>* out) override {
+        throw_status(
+            hgc_fft2d_f64(nx, ny, -1, 1, reinterpret_cast<const double*>(in), reinterpret_cast<double*>(out)));
+    }
+    void inverse(int nx, int ny, const std::complex<double>* in, std::complex<double>* out) override {
+        throw_status(
+            hgc_fft2d_f64(nx, ny, +1, 1, reinterpret_cast<const double*>(in), reinterpret_cast<double*>(out)));
+    }
+};
+
+inline B200FftBackendF64& fft_backend_f64() {
+    static B200FftBackendF64 b;
     return b;
 }
 

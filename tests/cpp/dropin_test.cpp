@@ -6,6 +6,7 @@
 // The reference's own loop (detail::run_ifta / run_ospr_impl) is run beside
 // the GPU path with default_fft_backend<float>() = the B200 FftBackend, so
 // both sides use the same transform and only the fused kernels differ.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <stdexcept>
@@ -15,6 +16,7 @@
 #include "hologen/ifta.hpp"
 #include "hologen/ospr.hpp"
 #include "hologen/patterns.hpp"
+#include "hologen/rng.hpp"
 #include "hologen_b200/dropin.hpp"
 
 namespace hologen {
@@ -22,6 +24,8 @@ template <typename T>
 FftBackend<T>& default_fft_backend();
 template <>
 FftBackend<float>& default_fft_backend<float>() { return hologen_b200::fft_backend(); }
+template <>
+FftBackend<double>& default_fft_backend<double>() { return hologen_b200::fft_backend_f64(); }
 }  // namespace hologen
 
 using namespace hologen;
@@ -110,6 +114,23 @@ int main() {
     for (int s = 0; s < 4; ++s) same = same && par[s].hologram.data == seq[s].hologram.data && par[s].final_error == seq[s].final_error;
     std::printf("batch pool of 4 threads: %s\n", same ? "identical to sequential" : "DIFFERENT");
     CHECK(same);
+
+    // FftBackend<double> on the GPU vs the reference's NaiveDftBackend (test_fft.cpp:90-98, 1e-10)
+    {
+        Rng r(3);
+        ComplexField<double> f(32, 16, Domain::Aperture);
+        for (auto& z : f.data) z = {r.uniform(-1.0, 1.0), r.uniform(-1.0, 1.0)};
+        NaiveDftBackend<double> naive;
+        auto g = fft_forward(f);  // default_fft_backend<double>() = B200FftBackendF64
+        auto n = fft_forward(f, &naive);
+        double err = 0.0;
+        for (size_t i = 0; i < g.data.size(); ++i) err = std::max(err, std::abs(g.data[i] - n.data[i]));
+        auto back = fft_inverse(g);
+        double rt = 0.0;
+        for (size_t i = 0; i < f.data.size(); ++i) rt = std::max(rt, std::abs(back.data[i] - f.data[i]));
+        std::printf("fft<double> 32x16 vs naive DFT: max err %.2e, round trip %.2e\n", err, rt);
+        CHECK(err < 1e-10 && rt < 1e-12);
+    }
 
     // errors keep the reference's exceptions and messages
     IftaConfig bad = cfg;

@@ -69,7 +69,8 @@ open(os.path.join(P, f"{tag}_ncu_full_summary.txt"), "w").write("\n".join(txt) +
 print("\n".join(txt))
 # traffic per launch for bench.py (dram bytes of one launch of the 64-target batch)
 traffic = {}
-for name, key in (("k_row", "gs_row"), ("k_col", "gs_col")):
+# the fused GS passes: k_row<N, ROW_FUSED, ...> and k_col<N, C, COL_GS_FAST (3), ...>
+for name, key in (("k_row<4096, 0,", "gs_row"), ("k_col<4096, 2, 3,", "gs_col")):
     for k, v in out.items():
         if k.startswith("hg::" + name) or k.startswith(name):
             if v["dram_read_bytes"] is not None:

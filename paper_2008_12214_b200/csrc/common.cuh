@@ -145,6 +145,13 @@ __device__ __forceinline__ void tma_store_2d(const void* map, int c0, int c1, co
                  "r"(c0), "r"(c1), "r"(smem_u32(src))
                  : "memory");
 }
+// One thread: shared -> global bulk copy (1-D), completed with bulk_commit /
+// bulk_wait_read0.  16 B aligned, bytes % 16 == 0.
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes)
+                 : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }

@@ -93,6 +93,9 @@ struct RowCfg {
     static constexpr int MIN_BLOCKS = LAY == LAY_QUAD ? (THREADS >= 512 ? HG_ROWQ_MINB : 1) : (THREADS >= 256 ? 3 : 1);
 };
 
+#ifndef HG_ROW_BULK
+#define HG_ROW_BULK 1
+#endif
 // FQ: Fresnel Q in the fused pass — 0 absent, 1 present (compile time, the
 // specialised quantisers), 2 decided at run time from a.fresnel_q.
 template <int NX, int MODE, int QK, int LAY, int FQ>
@@ -136,8 +139,32 @@ __global__ void __launch_bounds__(RowCfg<NX, LAY>::THREADS, RowCfg<NX, LAY>::MIN
         }
     };
     float2 v[E];
+    // Bulk path (quad layout): the CTA's RPC rows are RPC/2 whole quad rows,
+    // contiguous in HBM, so one cp.async.bulk brings them into smem and one
+    // writes them back; thread element e sits at landing slot lb + e*2T.
+    constexpr bool kBulk = HG_ROW_BULK && LAY == LAY_QUAD && NX > E && T >= 2;
+    __shared__ uint64_t rbar;
+    // (recomputed where used, so nothing extra stays live across the transforms)
+    auto tile_bytes = [&] {
+        return (uint32_t)(min(Cfg::RPC, a.ny - (int)blockIdx.x * Cfg::RPC) * NX * (int)sizeof(float2));
+    };
+    auto tile = [&] { return a.field + a.bstride * blockIdx.y + quad_index(0, blockIdx.x * Cfg::RPC, NX); };
+    auto lbase = [&] { return (lr >> 1) * (2 * NX) + (t >> 1) * 4 + (lr & 1) * 2 + (t & 1); };
+    if constexpr (kBulk) {
+        if (threadIdx.x == 0) {
+            mbar_init(&rbar, 1);
+            bulk_g2s(smem, tile(), tile_bytes(), &rbar);
+        }
+        __syncthreads();
+        mbar_wait(&rbar, 0);
+        const int lb = lbase();
 #pragma unroll
-    for (int e = 0; e < E; ++e) v[e] = ld_stream(&fb[addr(e)]);
+        for (int e = 0; e < E; ++e) v[e] = smem[lb + e * 2 * T];
+        __syncthreads();  // landing area becomes the exchange buffer
+    } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) v[e] = ld_stream(&fb[addr(e)]);
+    }
 
     if constexpr (MODE == ROW_PLAIN) {
         // Propagator<float>::forward / inverse halves (propagation.hpp:81-95):
@@ -181,7 +208,18 @@ __global__ void __launch_bounds__(RowCfg<NX, LAY>::THREADS, RowCfg<NX, LAY>::MIN
         }
         fft_line<NX, -1>(v, t, smem, idx, a.tw);  // starts the forward transform
     }
-    if (valid) {
+    if constexpr (kBulk) {
+        const int lb = opaque(lbase());
+#pragma unroll
+        for (int e = 0; e < E; ++e) smem[lb + e * 2 * T] = v[e];
+        fence_proxy_async();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            bulk_s2g(tile(), smem, tile_bytes());
+            bulk_commit();
+            bulk_wait_read0();
+        }
+    } else if (valid) {
         float2* ob = opaque(fb);
 #pragma unroll
         for (int e = 0; e < E; ++e) ob[addr(e)] = v[e];

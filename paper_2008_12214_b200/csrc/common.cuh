@@ -28,12 +28,55 @@ __device__ __forceinline__ float2 cmul_conj_rn(float2 a, float2 b) {
     return make_float2(__fadd_rn(ac, bd), __fsub_rn(bc, ad));
 }
 
-// Fast complex product for FFT butterflies (FMA allowed).
-__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-    return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+// Complex arithmetic of the transforms (FMA allowed) on the packed FP32 pipe:
+// sm_100a executes the f32x2 PTX types as FADD2 / FMUL2 / FFMA2, one
+// instruction for both lanes, with lane broadcast / swap as free operand
+// modifiers (nvcc does not pack scalar code by itself).  Per lane the results
+// are those of the scalar sequences they replace:
+//   cadd / csub: a.x +- b.x, a.y +- b.y;
+//   cmul: fmaf(a.x, b.x, -(a.y*b.y)), fmaf(a.x, b.y, a.y*b.x) — the inner
+//   products are formed as (a.y, a.y) * (-b.y, b.x), negation being exact.
+#ifndef HG_PACKED_F32
+#define HG_PACKED_F32 1
+#endif
+__device__ __forceinline__ unsigned long long f2_pack(float2 a) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+    return r;
 }
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 f2_unpack(unsigned long long r) {
+    float2 a;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
+    return a;
+}
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+#if HG_PACKED_F32
+    unsigned long long s, r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(s) : "l"(f2_pack(make_float2(a.y, a.y))), "l"(f2_pack(make_float2(-b.y, b.x))));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2_pack(make_float2(a.x, a.x))), "l"(f2_pack(b)), "l"(s));
+    return f2_unpack(r);
+#else
+    return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+#endif
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) {
+#if HG_PACKED_F32
+    unsigned long long r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_pack(a)), "l"(f2_pack(b)));
+    return f2_unpack(r);
+#else
+    return make_float2(a.x + b.x, a.y + b.y);
+#endif
+}
+__device__ __forceinline__ float2 csub(float2 a, float2 b) {
+#if HG_PACKED_F32
+    unsigned long long r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_pack(a)), "l"(f2_pack(b)));
+    return f2_unpack(r);
+#else
+    return make_float2(a.x - b.x, a.y - b.y);
+#endif
+}
 // double2 versions for the f64 transform (k_fft64.cu)
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
     return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));

@@ -28,16 +28,22 @@ __device__ __forceinline__ float2 cmul_conj_rn(float2 a, float2 b) {
     return make_float2(__fadd_rn(ac, bd), __fsub_rn(bc, ad));
 }
 
-// Complex arithmetic of the transforms (FMA allowed) on the packed FP32 pipe:
-// sm_100a executes the f32x2 PTX types as FADD2 / FMUL2 / FFMA2, one
-// instruction for both lanes, with lane broadcast / swap as free operand
-// modifiers (nvcc does not pack scalar code by itself).  Per lane the results
-// are those of the scalar sequences they replace:
+// Complex arithmetic of the transforms (FMA allowed).  HG_PACKED_F32=1 runs it
+// on the packed FP32 instructions: sm_100a executes the f32x2 PTX types as
+// FADD2 / FMUL2 / FFMA2, one instruction for both lanes, with lane broadcast /
+// swap as free operand modifiers (nvcc does not pack scalar code by itself).
+// That cut the static instruction count of the fused passes by 18-24% but
+// measured slower overall at 4096^2 (row -1.7%, column +7%: the pairing moves
+// and per-lane negations cost more than the issue slots saved), so the scalar
+// form is the default.  Per lane both forms compute the same roundings:
 //   cadd / csub: a.x +- b.x, a.y +- b.y;
 //   cmul: fmaf(a.x, b.x, -(a.y*b.y)), fmaf(a.x, b.y, a.y*b.x) — the inner
 //   products are formed as (a.y, a.y) * (-b.y, b.x), negation being exact.
 #ifndef HG_PACKED_F32
-#define HG_PACKED_F32 1
+#define HG_PACKED_F32 0
+#endif
+#ifndef HG_PACKED_CMUL
+#define HG_PACKED_CMUL HG_PACKED_F32
 #endif
 __device__ __forceinline__ unsigned long long f2_pack(float2 a) {
     unsigned long long r;
@@ -50,7 +56,7 @@ __device__ __forceinline__ float2 f2_unpack(unsigned long long r) {
     return a;
 }
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-#if HG_PACKED_F32
+#if HG_PACKED_CMUL
     unsigned long long s, r;
     asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(s) : "l"(f2_pack(make_float2(a.y, a.y))), "l"(f2_pack(make_float2(-b.y, b.x))));
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2_pack(make_float2(a.x, a.x))), "l"(f2_pack(b)), "l"(s));

@@ -259,3 +259,50 @@ def test_plan_upload_is_async_and_download_reports_invalid_target():
     p.execute()
     out = p.download()
     assert np.isfinite(out.trace).all()
+
+
+def _roi_target(n, inner):
+    amp = np.zeros((n, n))
+    roi = np.zeros((n, n), np.uint8)
+    a, b = n // 4, n // 4 + inner
+    amp[a:b, a:b] = hg.patterns.letter_a(inner, inner)
+    roi[a:b, a:b] = 1
+    return hg.normalize_image(amp, hg.Normalization.UnitEnergy), roi
+
+
+@pytest.mark.parametrize("case", ["lt_roi", "roi_scale_free", "wgs_roi", "target_phase"])
+def test_generic_constraint_with_tma_tiles_matches_oracle(oracle, case):
+    """The generic replay-plane constraint (ROI, LT rectangle, scale freedom,
+    WGS weights, fixed target phase; ifta.hpp:185-224) at 512^2, where the
+    column pass moves its tiles by TMA: binary free-running vs the oracle."""
+    n = 512
+    amp, roi = _roi_target(n, 256)
+    slm = hg.SlmSpec.binary_phase()
+    K = 8
+    if case == "lt_roi":
+        c = cfg_for(amp, slm, K, seed=2, variant=hg.IftaVariant.LiuTaghizadeh)
+        c.target.roi = roi
+        c.target.freedoms.amplitude_outside_roi = True
+        rep = hg.run_liu_taghizadeh(c)
+        ref = oracle.ifta(amp, slm, K, seed=2, variant="lt", roi=roi, amp_outside_roi=True)
+    elif case == "roi_scale_free":
+        c = cfg_for(amp, slm, K, seed=21)
+        c.target.roi = roi
+        c.target.freedoms.scale = True
+        rep = hg.run_gs(c)
+        ref = oracle.ifta(amp, slm, K, seed=21, roi=roi, scale_freedom=True)
+    elif case == "wgs_roi":
+        c = cfg_for(amp, slm, K, seed=4, variant=hg.IftaVariant.WeightedGS)
+        c.target.roi = roi
+        rep = hg.run_weighted_gs(c)
+        ref = oracle.ifta(amp, slm, K, seed=4, variant="wgs", roi=roi)
+    else:
+        turns = np.random.default_rng(5).uniform(0, 1, (n, n))
+        c = cfg_for(hg.patterns.bench_target(n), slm, K, seed=6)
+        c.target.phase = turns
+        c.target.freedoms.phase = False
+        rep = hg.run_gs(c)
+        ref = oracle.ifta(c.target.amplitude, slm, K, seed=6, phase_turns=turns, phase_freedom=False)
+    mism = level_mismatches(rep.levels, ref.levels).sum()
+    assert mism <= 16, (case, mism)
+    assert np.max(np.abs(rep.trace.values() - ref.trace) / ref.trace) < MSE_TOL, case

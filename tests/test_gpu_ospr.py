@@ -151,3 +151,21 @@ def test_ospr_sharded_driver_world1(oracle):
     ref = oracle.ospr(amp, hg.SlmSpec.binary_phase(), 6, seed=3)
     assert level_mismatches(out["levels"], ref.levels).sum() <= 6
     assert np.max(np.abs(out["cumulative_mse"] - ref.cumulative_mse) / ref.cumulative_mse) < 1e-4
+
+
+def test_ospr_roi_with_tma_tiles_matches_oracle(oracle):
+    """OSPR with an ROI (masked MSE, ospr.hpp:138-145) at 512^2, where the
+    accumulating column pass lands its tiles by TMA."""
+    n = 512
+    amp = np.zeros((n, n))
+    roi = np.zeros((n, n), np.uint8)
+    amp[128:384, 128:384] = hg.patterns.letter_a(256, 256)
+    roi[128:384, 128:384] = 1
+    amp = hg.normalize_image(amp, hg.Normalization.UnitEnergy)
+    cfg = ocfg(amp, 4, 12)
+    cfg.target.roi = roi
+    run = hg.run_ospr(cfg)
+    ref = oracle.ospr(amp, hg.SlmSpec.binary_phase(), 4, seed=12, roi=roi)
+    assert level_mismatches(run.set.levels, ref.levels).sum() <= 8
+    assert np.max(np.abs(run.report.trace.values() - ref.cumulative_mse) / ref.cumulative_mse) < 1e-4
+    assert np.max(np.abs(np.array(run.set.per_frame_mse) - ref.frame_mse) / ref.frame_mse) < 1e-4

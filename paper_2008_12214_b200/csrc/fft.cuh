@@ -234,7 +234,7 @@ struct StockhamPass {
             }
         }
         if constexpr (!last) {
-            idx.sync();
+            __syncthreads();
             if constexpr (T % 16 == 0) {
                 const int s0 = idx(t);
                 constexpr int es = T + T / 16;
@@ -244,7 +244,7 @@ struct StockhamPass {
 #pragma unroll
                 for (int e = 0; e < E; ++e) v[e] = sm[idx(t + e * T)];
             }
-            idx.sync();
+            __syncthreads();
             StockhamPass<N, SIGN, NS * R, EM>::run(v, t, sm, idx, tw);
         }
     }
@@ -266,18 +266,11 @@ struct PaddedLen {
     static constexpr int value = N + (N >> 4) + 1;
 };
 
-// Row layout: each line owns a contiguous padded region.  bar != 0: the
-// line's threads are whole warps and synchronise among themselves on named
-// barrier `bar` (bar_threads threads) instead of the whole CTA.
+// Row layout: each line owns a contiguous padded region.
 struct RowSmemIdx {
     static constexpr int kLineStride = 1;  // slot step per position step
     int off;
-    int bar = 0, bar_threads = 0;
     __device__ __forceinline__ int operator()(int q) const { return off + pad16(q); }
-    __device__ __forceinline__ void sync() const {
-        if (bar) asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(bar_threads) : "memory");
-        else __syncthreads();
-    }
 };
 // Column layout: C lines interleaved (slot * C + c) so a warp spanning
 // C adjacent columns hits adjacent banks.
@@ -286,7 +279,6 @@ struct ColSmemIdx {
     static constexpr int kLineStride = C;
     int c;
     __device__ __forceinline__ int operator()(int q) const { return pad16(q) * C + c; }
-    __device__ __forceinline__ void sync() const { __syncthreads(); }
 };
 
 }  // namespace hg

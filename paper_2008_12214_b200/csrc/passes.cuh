@@ -96,9 +96,6 @@ struct RowCfg {
 #ifndef HG_ROW_BULK
 #define HG_ROW_BULK 1
 #endif
-#ifndef HG_ROW_NAMED
-#define HG_ROW_NAMED 1
-#endif
 // FQ: Fresnel Q in the fused pass — 0 absent, 1 present (compile time, the
 // specialised quantisers), 2 decided at run time from a.fresnel_q.
 template <int NX, int MODE, int QK, int LAY, int FQ>
@@ -107,17 +104,7 @@ __global__ void __launch_bounds__(RowCfg<NX, LAY>::THREADS, RowCfg<NX, LAY>::MIN
     constexpr int E = Cfg::E, T = Cfg::T;
     extern __shared__ __align__(128) float2 smem[];
     int lr, t;
-    // Bulk path (quad layout): the CTA's RPC rows are RPC/2 whole quad rows,
-    // contiguous in HBM, so one cp.async.bulk brings them into smem and one
-    // writes them back.  The thread mapping is then free: with kNamed each
-    // row owns whole warps and its transforms synchronise on the row's own
-    // named barrier instead of the whole CTA.
-    constexpr bool kBulk = HG_ROW_BULK && LAY == LAY_QUAD && NX > E && T >= 2;
-    constexpr bool kNamed = kBulk && HG_ROW_NAMED && T >= 64 && Cfg::RPC <= 15;
-    if constexpr (kNamed) {
-        lr = threadIdx.x / T;
-        t = threadIdx.x % T;
-    } else if constexpr (LAY == LAY_QUAD) {
+    if constexpr (LAY == LAY_QUAD) {
         // the 2T threads of a row pair interleave so a warp covers 2 rows x 16
         // consecutive x = 8 whole quads (256 contiguous bytes)
         const int pr = threadIdx.x / (2 * T), q = threadIdx.x % (2 * T);
@@ -136,7 +123,7 @@ __global__ void __launch_bounds__(RowCfg<NX, LAY>::THREADS, RowCfg<NX, LAY>::MIN
     }
     const int y = blockIdx.x * Cfg::RPC + lr;
     const int b = blockIdx.y;
-    RowSmemIdx idx{lr * RowStride<NX>::value, kNamed ? 1 + lr : 0, T};
+    RowSmemIdx idx{lr * RowStride<NX>::value};
     const bool valid = y < a.ny;  // (ny is a multiple of RPC except for tiny fields)
     const int yy = valid ? y : 0;
     float2* fb = a.field + a.bstride * b;
@@ -152,7 +139,10 @@ __global__ void __launch_bounds__(RowCfg<NX, LAY>::THREADS, RowCfg<NX, LAY>::MIN
         }
     };
     float2 v[E];
-    // thread element e sits at landing slot lb + e*2T of the bulk tile
+    // Bulk path (quad layout): the CTA's RPC rows are RPC/2 whole quad rows,
+    // contiguous in HBM, so one cp.async.bulk brings them into smem and one
+    // writes them back; thread element e sits at landing slot lb + e*2T.
+    constexpr bool kBulk = HG_ROW_BULK && LAY == LAY_QUAD && NX > E && T >= 2;
     __shared__ uint64_t rbar;
     // (recomputed where used, so nothing extra stays live across the transforms)
     auto tile_bytes = [&] {

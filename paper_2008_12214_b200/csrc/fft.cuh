@@ -152,13 +152,11 @@ __device__ __forceinline__ C2 twiddle(const C2* __restrict__ tw, int m) {
 // x[r] *= w^r, w = exp(SIGN*2*pi*i*m/N), r = 1..R-1.  For R = 16 only w, w^4
 // and w^8 come from the table (the rest are <= 2 products of table values,
 // error <= ~2 ulp): 3 loads instead of 15 keeps the pass within the register
-// budget of a 1024-thread CTA.
-#ifndef HG_TW_LOADALL
-#define HG_TW_LOADALL 0
-#endif
+// budget of a 1024-thread CTA (loading all 15 measured 10.1 vs 6.9 ms for
+// the 4096^2 row pass: the extra live values spill).
 template <int N, int SIGN, int R, class C2>
 __device__ __forceinline__ void apply_twiddles(C2* x, const C2* __restrict__ tw, int m) {
-    if constexpr (R == 16 && !HG_TW_LOADALL) {
+    if constexpr (R == 16) {
         const C2 w1 = twiddle<N, SIGN>(tw, m);
         const C2 w4 = twiddle<N, SIGN>(tw, 4 * m);
         const C2 w8 = twiddle<N, SIGN>(tw, 8 * m);

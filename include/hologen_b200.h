@@ -297,7 +297,10 @@ int hgc_replay_to_gray8(const float* replay, int nx, int ny, int batch, uint8_t*
 int hgc_write_replay_scale(const char* png_path, double peak);
 
 /* ------------------------------------------------------- primitives */
-/* Unitary 2-D DFT of `batch` fields, sign -1 forward / +1 inverse; in == out allowed. */
+/* Unitary 2-D DFT of `batch` fields, sign -1 forward / +1 inverse; in == out
+ * allowed.  Any nx, ny >= 1 like FftBackend (fft.hpp:17-27): powers of two
+ * up to 4096 on the fused float kernels, other lengths up to 2048 by
+ * Bluestein's algorithm in double (rounded back to float). */
 int hgc_fft2d(int nx, int ny, int sign, int batch, const float* in, float* out);
 /* The same for complex128 (FftBackend<double>, fft.hpp:17-27):
  * double-precision butterflies and twiddles, scale 1/sqrt(nx*ny) in double. */

@@ -1962,12 +1962,25 @@ int hgc_propagate(int nx, int ny, int sign, const hgc_fresnel* fresnel, int batc
     });
 }
 
+// Sizes the fused power-of-two kernels take; other sizes go through the
+// Bluestein path of k_fft64.cu (FftBackend accepts any nx, ny >= 1).
+static bool fast_sizes(int nx, int ny) { return is_pow2(nx) && is_pow2(ny) && nx >= 2 && ny >= 2 && nx <= kMaxLine && ny <= kMaxLine; }
+__global__ void k_c64_to_c128(const float2* a, double2* b, size_t n) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        b[i] = make_double2(a[i].x, a[i].y);
+}
+__global__ void k_c128_to_c64(const double2* a, float2* b, size_t n) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        b[i] = make_float2((float)a[i].x, (float)a[i].y);
+}
+
 int hgc_fft2d_f64(int nx, int ny, int sign, int batch, const double* in, double* out) {
     return guarded([&] {
         if (!in || !out) invalid("fft: null buffer");
         if (sign != -1 && sign != 1) invalid("fft: sign must be -1 or +1");
         if (batch < 1) invalid("fft: batch must be >= 1");
-        check_size(nx, ny);
+        if (nx <= 0 || ny <= 0) invalid("ComplexField: dimensions must be positive");
+        const bool fast = fast_sizes(nx, ny);
         const size_t tot = (size_t)nx * ny * batch;
         for (size_t i = 0; i < 2 * tot; ++i)  // require_finite, fft.hpp:95-97 / :106-108
             if (!std::isfinite(in[i]))
@@ -1977,7 +1990,8 @@ int hgc_fft2d_f64(int nx, int ny, int sign, int batch, const double* in, double*
         cudaStream_t st;
         CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
         CK(cudaMemcpyAsync(f.p, in, sizeof(double2) * tot, cudaMemcpyHostToDevice, st));
-        fft2d_f64(f.p, nx, ny, sign, batch, st);
+        if (fast) fft2d_f64(f.p, nx, ny, sign, batch, st);
+        else fft2d_any_f64(f.p, nx, ny, sign, batch, st);
         CK(cudaMemcpyAsync(out, f.p, sizeof(double2) * tot, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         CK(cudaStreamDestroy(st));
@@ -1985,6 +1999,26 @@ int hgc_fft2d_f64(int nx, int ny, int sign, int batch, const double* in, double*
 }
 
 int hgc_fft2d(int nx, int ny, int sign, int batch, const float* in, float* out) {
+    if (nx > 0 && ny > 0 && !fast_sizes(nx, ny) && in && out && batch >= 1 && (sign == 1 || sign == -1))
+        return guarded([&] {  // any size: Bluestein in double, rounded back to float
+            const size_t tot = (size_t)nx * ny * batch;
+            for (size_t i = 0; i < 2 * tot; ++i)
+                if (!std::isfinite(in[i]))
+                    invalid(std::string(sign < 0 ? "fft_forward" : "fft_inverse") + ": field contains non-finite values");
+            DBuf<float2> f;
+            DBuf<double2> d;
+            f.alloc(tot);
+            d.alloc(tot);
+            cudaStream_t st;
+            CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+            CK(cudaMemcpyAsync(f.p, in, sizeof(float2) * tot, cudaMemcpyHostToDevice, st));
+            k_c64_to_c128<<<ew_grid(tot), 256, 0, st>>>(f.p, d.p, tot);
+            fft2d_any_f64(d.p, nx, ny, sign, batch, st);
+            k_c128_to_c64<<<ew_grid(tot), 256, 0, st>>>(d.p, f.p, tot);
+            CK(cudaMemcpyAsync(out, f.p, sizeof(float2) * tot, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            CK(cudaStreamDestroy(st));
+        });
     return hgc_propagate(nx, ny, sign, nullptr, batch, in, out);
 }
 

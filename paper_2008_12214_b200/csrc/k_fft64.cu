@@ -6,8 +6,10 @@
 // (fft.cuh, instantiated on double2) with 8 elements per thread, so a 4096
 // line keeps 32 registers of data.  Row-major layout (ComplexField<double>),
 // rows pass then columns pass, the unitary scale applied by the last pass.
+#include <algorithm>
 #include <cmath>
 #include <map>
+#include <string>
 #include <mutex>
 
 #include "errors.h"
@@ -155,7 +157,118 @@ void cols64_any(int ny, double2* f, int nx, int batch, size_t bs, double norm, c
     }
 }
 
+bool pow2_line(int n) { return n >= 2 && n <= kMaxLine && (n & (n - 1)) == 0; }
+
+// ------------------------------------------------------------ Bluestein
+// A line of any length N <= 2048 (FftBackend accepts any nx, ny >= 1,
+// fft.hpp:17-27): X_k = w_k * sum_n (x_n w_n) conj(w_{k-n}), w_n =
+// exp(SIGN i pi n^2 / N), as a length-M circular convolution (M = 2^j >=
+// 2N - 1) through the power-of-two transforms above, all in double.
+__device__ __forceinline__ double2 chirp(long long n, int N, int sign) {
+    const long long r = (n * n) % (2LL * N);  // exp(i pi r / N) is 2N-periodic in n^2
+    double s, c;
+    sincospi((double)sign * (double)r / (double)N, &s, &c);
+    return make_double2(c, s);
+}
+__global__ void k_blu_pre(const double2* in, int N, int M, size_t lines, int sign, double2* a) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < lines * M; i += (size_t)gridDim.x * blockDim.x) {
+        const size_t l = i / M;
+        const int n = (int)(i % M);
+        double2 v = make_double2(0.0, 0.0);
+        if (n < N) {
+            const double2 x = in[l * N + n], w = chirp(n, N, sign);
+            v = make_double2(x.x * w.x - x.y * w.y, x.x * w.y + x.y * w.x);
+        }
+        a[i] = v;
+    }
+}
+__global__ void k_blu_kernel(int N, int M, int sign, double2* b) {  // conj(w_n) at n and M - n
+    for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < M; n += gridDim.x * blockDim.x) {
+        double2 v = make_double2(0.0, 0.0);
+        const int m = n < N ? n : (M - n < N ? M - n : -1);
+        if (m >= 0) {
+            const double2 w = chirp(m, N, sign);
+            v = make_double2(w.x, -w.y);
+        }
+        b[n] = v;
+    }
+}
+__global__ void k_blu_mul(double2* a, const double2* bh, int M, size_t lines) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < lines * M; i += (size_t)gridDim.x * blockDim.x) {
+        const double2 x = a[i], y = bh[i % M];
+        a[i] = make_double2(x.x * y.x - x.y * y.y, x.x * y.y + x.y * y.x);
+    }
+}
+__global__ void k_blu_post(const double2* a, int N, int M, size_t lines, int sign, double2* out) {
+    const double inv = 1.0 / M;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < lines * N; i += (size_t)gridDim.x * blockDim.x) {
+        const size_t l = i / N;
+        const int k = (int)(i % N);
+        const double2 x = a[l * M + k], w = chirp(k, N, sign);
+        out[i] = make_double2((x.x * w.x - x.y * w.y) * inv, (x.x * w.y + x.y * w.x) * inv);
+    }
+}
+__global__ void k_transpose64(const double2* in, int w, int h, size_t batch, double2* out) {  // [b][h][w] -> [b][w][h]
+    const size_t n = (size_t)w * h;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n * batch; i += (size_t)gridDim.x * blockDim.x) {
+        const size_t b = i / n, r = i % n, y = r / w, x = r % w;
+        out[b * n + x * h + y] = in[i];
+    }
+}
+dim3 grid_for(size_t n) { return dim3((unsigned)std::min<size_t>((n + 255) / 256, 148 * 16)); }
+
+struct DevBuf64 {
+    double2* p = nullptr;
+    explicit DevBuf64(size_t n) { CK(cudaMalloc(&p, sizeof(double2) * (n ? n : 1))); }
+    ~DevBuf64() { cudaFree(p); }
+};
+
+// Unnormalised transform of `lines` contiguous lines of length N, in place.
+void lines64(double2* f, int N, size_t lines, int sign, const double2* tw, cudaStream_t st) {
+    if (N == 1) return;
+    if (pow2_line(N)) {
+        if (sign < 0) rows64_any<-1>(N, f, (int)lines, 1, 0, 0.0, tw, st);
+        else rows64_any<+1>(N, f, (int)lines, 1, 0, 0.0, tw, st);
+        return;
+    }
+    if (N > kMaxLine / 2) fail(HGC_EUNSUPPORTED, "fft: non-power-of-two length " + std::to_string(N) + " > 2048");
+    int M = 1;
+    while (M < 2 * N - 1) M *= 2;
+    DevBuf64 a(lines * M), b(M);
+    k_blu_kernel<<<grid_for(M), 256, 0, st>>>(N, M, sign, b.p);
+    rows64_any<-1>(M, b.p, 1, 1, 0, 0.0, tw, st);
+    k_blu_pre<<<grid_for(lines * M), 256, 0, st>>>(f, N, M, lines, sign, a.p);
+    rows64_any<-1>(M, a.p, (int)lines, 1, 0, 0.0, tw, st);
+    k_blu_mul<<<grid_for(lines * M), 256, 0, st>>>(a.p, b.p, M, lines);
+    rows64_any<+1>(M, a.p, (int)lines, 1, 0, 0.0, tw, st);
+    k_blu_post<<<grid_for(lines * N), 256, 0, st>>>(a.p, N, M, lines, sign, f);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));  // a, b are freed on return
+}
+
+__global__ void k_scale64(double2* f, size_t n, double s) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        f[i] = make_double2(f[i].x * s, f[i].y * s);
+}
+
 }  // namespace
+
+// Any nx, ny (non-powers of two up to 2048): rows, then columns as
+// transpose + rows + transpose, then the unitary scale — in double.
+void fft2d_any_f64(double2* f, int nx, int ny, int sign, int batch, cudaStream_t st) {
+    const double2* tw = device_twiddles64();
+    const size_t npix = (size_t)nx * ny, tot = npix * batch;
+    lines64(f, nx, (size_t)ny * batch, sign, tw, st);
+    if (ny > 1) {
+        DevBuf64 t(tot);
+        k_transpose64<<<grid_for(tot), 256, 0, st>>>(f, nx, ny, batch, t.p);
+        lines64(t.p, ny, (size_t)nx * batch, sign, tw, st);
+        k_transpose64<<<grid_for(tot), 256, 0, st>>>(t.p, ny, nx, batch, f);
+    }
+    k_scale64<<<grid_for(tot), 256, 0, st>>>(f, tot, 1.0 / std::sqrt((double)nx * ny));  // fftw_backend.cpp:121-123
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+}
 
 // Unitary 2-D transform of `batch` row-major complex128 fields in place:
 // rows, then columns with the (double)1/sqrt(nx*ny) scale.

@@ -18,6 +18,8 @@ void row_fused_binary(int nx, const RowArgs& a, int batch, cudaStream_t st, bool
 void row_fused_full(int nx, const RowArgs& a, int batch, cudaStream_t st, bool prepare);
 // unitary complex128 2-D transform in place (k_fft64.cu)
 void fft2d_f64(double2* f, int nx, int ny, int sign, int batch, cudaStream_t st);
+// any nx, ny >= 1 (Bluestein for non-powers of two <= 2048), in double (k_fft64.cu)
+void fft2d_any_f64(double2* f, int nx, int ny, int sign, int batch, cudaStream_t st);
 void col_plain(int ny, const ColArgs& a, int batch, cudaStream_t st, bool prepare = false);
 void col_gs(int ny, const ColArgs& a, int batch, cudaStream_t st, bool prepare = false);
 void col_ospr(int ny, const ColArgs& a, int batch, cudaStream_t st, bool prepare = false);

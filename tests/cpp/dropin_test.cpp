@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <stdexcept>
 #include <thread>
+#include <utility>
 #include <vector>
 
 #include "hologen/ifta.hpp"
@@ -130,6 +131,16 @@ int main() {
         for (size_t i = 0; i < f.data.size(); ++i) rt = std::max(rt, std::abs(back.data[i] - f.data[i]));
         std::printf("fft<double> 32x16 vs naive DFT: max err %.2e, round trip %.2e\n", err, rt);
         CHECK(err < 1e-10 && rt < 1e-12);
+        // any size (test_fft.cpp:90-98: 5x7 and 16x3 against the naive DFT at 1e-10)
+        for (auto [w, h] : {std::pair{5, 7}, std::pair{16, 3}}) {
+            ComplexField<double> g2(w, h, Domain::Aperture);
+            for (auto& z : g2.data) z = {r.uniform(-1.0, 1.0), r.uniform(-1.0, 1.0)};
+            auto a = fft_forward(g2), bnv = fft_forward(g2, &naive);
+            double e2 = 0.0;
+            for (size_t i = 0; i < a.data.size(); ++i) e2 = std::max(e2, std::abs(a.data[i] - bnv.data[i]));
+            std::printf("fft<double> %dx%d vs naive DFT: max err %.2e\n", w, h, e2);
+            CHECK(e2 < 1e-10);
+        }
     }
 
     // errors keep the reference's exceptions and messages

@@ -88,12 +88,34 @@ def test_fft_delta_constant_roundtrip():
 
 
 def test_fft_rejects_unsupported_and_nonfinite():
-    with pytest.raises(hg.HgcUnsupported):
-        hg.fft_forward(np.zeros((5, 7), np.complex64))
+    with pytest.raises(hg.HgcUnsupported):  # non-powers of two are covered up to 2048 per side
+        hg.fft_forward(np.zeros((5, 3000), np.complex64))
     bad = np.zeros((8, 8), np.complex64)
     bad[1, 1] = np.nan
     with pytest.raises(ValueError):
         hg.fft_forward(bad)
+    bad7 = np.zeros((5, 7), np.complex64)
+    bad7[2, 3] = np.inf
+    with pytest.raises(ValueError, match="non-finite"):
+        hg.fft_forward(bad7)
+
+
+@pytest.mark.parametrize("ny,nx", [(5, 7), (16, 3), (1, 1), (3, 1), (1, 5), (12, 64), (100, 30), (1080, 1920)])
+def test_fft_any_size_matches_numpy(ny, nx):
+    """FftBackend accepts any nx, ny >= 1 (fft.hpp:17-27; test_fft.cpp:90-98 uses 5x7 and 16x3):
+    non-powers of two go through Bluestein in double, for both precisions."""
+    r = np.random.default_rng(ny * 31 + nx)
+    x = r.standard_normal((ny, nx)) + 1j * r.standard_normal((ny, nx))
+    ref_f = np.fft.fft2(x) / np.sqrt(x.size)
+    ref_i = np.fft.ifft2(x) * np.sqrt(x.size)
+    tol = 1e-12 * np.sqrt(np.log2(x.size) + 2) * 8
+    assert np.max(np.abs(hg.fft_forward(x) - ref_f)) < tol
+    assert np.max(np.abs(hg.fft_inverse(x) - ref_i)) < tol
+    x32 = x.astype(np.complex64)
+    ref32 = np.fft.fft2(x32.astype(np.complex128)) / np.sqrt(x.size)
+    got32 = hg.fft_forward(x32)
+    assert got32.dtype == np.complex64
+    assert np.max(np.abs(got32 - ref32)) < 2e-6 * np.sqrt(np.log2(x.size) + 2)  # double inside, one float rounding
 
 
 SLMS = {

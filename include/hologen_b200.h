@@ -246,6 +246,40 @@ int hgc_ospr_block_plan_create(hgc_ospr_plan** plan, const hgc_ospr_cfg* cfg, co
 int hgc_ospr_block_sum(hgc_ospr_plan* plan, void** dev_ptr, size_t* count);
 int hgc_ospr_block_finish(hgc_ospr_plan* plan, const void* gathered, int nblocks, int index, void* stream);
 
+/* --------------------------------------- f64 loops */
+/* run_ifta<double> / run_ospr_variant<double> (ifta.hpp:86-235,
+ * ospr.hpp:68-185) on the device, one target per call: the reference's
+ * double arithmetic per pixel (quantiser decisions, constraint, MSE, OSPR
+ * accumulation; no FMA contraction), double transforms of any size (as
+ * hgc_fft2d_f64), seeds from the same Rng(seed).fork(0) stream.  Complex
+ * buffers are interleaved double [ny][nx] (std::complex<double>). */
+typedef struct hgc_ifta_io64 {
+    const double* amplitude;    /* TargetSpec::amplitude [ny][nx] */
+    const double* phase;        /* TargetSpec::phase (turns) or NULL */
+    const uint8_t* roi;         /* or NULL */
+    const double* init_field;   /* init_phase == 3: complex [ny][nx] */
+    const double* init_weights; /* init_phase == 3, WGS, or NULL */
+    double* hologram;           /* RunReport::hologram complex [ny][nx] */
+    double* replay;             /* RunReport::replay complex [ny][nx] */
+    int32_t* levels;            /* level indices [ny][nx] */
+    double* trace;              /* [iterations] */
+    double* final_error;
+} hgc_ifta_io64;
+int hgc_ifta_run_f64(const hgc_ifta_cfg* cfg, const hgc_slm* slm, const hgc_fresnel* fresnel, int nx, int ny,
+                     hgc_ifta_io64* io);
+typedef struct hgc_ospr_io64 {
+    const double* amplitude;    /* [ny][nx] */
+    const uint8_t* roi;
+    double* frames;             /* complex [subframes][ny][nx] */
+    int32_t* levels;            /* [subframes][ny][nx] */
+    double* frame_mse;          /* [subframes] */
+    double* cumulative_mse;     /* [subframes] */
+    double* mean_intensity;     /* [ny][nx] */
+    double* replay;             /* complex [ny][nx] */
+    double* final_error;
+} hgc_ospr_io64;
+int hgc_ospr_run_f64(const hgc_ospr_cfg* cfg, const hgc_slm* slm, int nx, int ny, hgc_ospr_io64* io);
+
 /* ------------------------------ batch executor */
 /* One job of the runner's `batch` command (runner.cpp:365-421): a generate
  * run of one target.  Inputs are caller-owned host buffers; the outputs

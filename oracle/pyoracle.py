@@ -167,6 +167,8 @@ class Oracle:
                                vp, vp, vp])
             fn("ospr_run", i, [i, i, u64, d, C.POINTER(HgoSlm), i, i, vp, vp, i, vp, vp, vp, vp, vp, vp,
                                vp])
+            fn("ifta_run_d", i, [C.POINTER(HgoIftaCfg), C.POINTER(HgoSlm), i, i, vp, vp, vp, vp, vp, vp, vp])
+            fn("ospr_run_d", i, [i, i, u64, d, C.POINTER(HgoSlm), i, i, vp, vp, i, vp, vp, vp, vp])
 
     # ------------------------------------------------------------ helpers
     def _check(self, rc):
@@ -310,6 +312,53 @@ class Oracle:
         self._check(self._f["ifta_run"](C.byref(c), C.byref(s), nx, ny, _p(amp), _p(ph), _p(rm),
                                         _p(holo), _p(rep), _p(lv), _p(tr), C.byref(secs)))
         return IftaResult(holo, rep, lv, tr, seconds=secs.value)
+
+    def ifta64(self, amp, slm, iterations, seed=0, variant="gs", phase_turns=None, roi=None,
+               clamp=(0.1, 10.0), lt_initial_fraction=0.1, init_phase="auto", amp_outside_roi=False,
+               phase_freedom=True, scale_freedom=False, fresnel=None) -> IftaResult:
+        """run_ifta<double> of the compiled reference (kind == "reference" only)."""
+        keep = []
+        amp = np.ascontiguousarray(amp, np.float64)
+        ny, nx = amp.shape
+        c = HgoIftaCfg()
+        c.variant = {"gs": 0, "wgs": 1, "lt": 2}[variant]
+        c.iterations = iterations
+        c.seed = seed
+        c.clamp_lo, c.clamp_hi = clamp
+        c.lt_initial_fraction = lt_initial_fraction
+        c.init_phase = {"auto": 0, "random": 1, "flat": 2}[init_phase]
+        c.amp_outside_roi = int(amp_outside_roi)
+        c.phase_freedom = int(phase_freedom)
+        c.scale_freedom = int(scale_freedom)
+        if fresnel is not None:
+            c.fresnel = 1
+            c.wavelength, c.distance, c.pitch_x, c.pitch_y = fresnel
+        s = _slm(slm, keep)
+        ph = None if phase_turns is None else np.ascontiguousarray(phase_turns, np.float64)
+        rm = None if roi is None else np.ascontiguousarray(roi, np.uint8)
+        holo = np.empty((ny, nx), np.complex128)
+        rep = np.empty((ny, nx), np.complex128)
+        lv = np.empty((ny, nx), np.int32)
+        tr = np.empty(iterations, np.float64)
+        self._check(self._f["ifta_run_d"](C.byref(c), C.byref(s), nx, ny, _p(amp), _p(ph), _p(rm), _p(holo),
+                                          _p(rep), _p(lv), _p(tr)))
+        return IftaResult(holo, rep, lv, tr)
+
+    def ospr64(self, target, slm, subframes, seed=0, adaptive=False, gain=1.0, roi=None,
+               scale_free=False) -> OsprResult:
+        """run_ospr_variant<double> of the compiled reference (kind == "reference" only)."""
+        keep = []
+        t = np.ascontiguousarray(target, np.float64)
+        ny, nx = t.shape
+        s = _slm(slm, keep)
+        rm = None if roi is None else np.ascontiguousarray(roi, np.uint8)
+        lv = np.empty((subframes, ny, nx), np.int32)
+        fm = np.empty(subframes, np.float64)
+        cm = np.empty(subframes, np.float64)
+        mi = np.empty((ny, nx), np.float64)
+        self._check(self._f["ospr_run_d"](int(adaptive), subframes, seed, gain, C.byref(s), nx, ny, _p(t), _p(rm),
+                                          int(scale_free), _p(lv), _p(fm), _p(cm), _p(mi)))
+        return OsprResult(lv, None, fm, cm, mi, None)
 
     # --------------------------------------------------------------- ospr
     def ospr(self, target, slm, subframes, seed=0, adaptive=False, gain=1.0, roi=None,

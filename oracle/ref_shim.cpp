@@ -264,6 +264,85 @@ int hgr_ifta_run(const hgo_ifta_cfg* c, const hgo_slm* s, int nx, int ny, const 
     });
 }
 
+// run_ifta<double> (ifta.hpp:86-235) — the oracle of the f64 device loop.
+int hgr_ifta_run_d(const hgo_ifta_cfg* c, const hgo_slm* s, int nx, int ny, const double* amp,
+                   const double* phase_turns, const uint8_t* roi, double* hologram, double* replay,
+                   int32_t* levels, double* trace) {
+    return guard([&] {
+        IftaConfig cfg;
+        cfg.variant = c->variant == 0   ? IftaVariant::GS
+                      : c->variant == 1 ? IftaVariant::WeightedGS
+                                        : IftaVariant::LiuTaghizadeh;
+        cfg.iterations = c->iterations;
+        cfg.slm = to_spec(s, nx, ny);
+        cfg.target.amplitude = to_image(amp, nx, ny);
+        if (phase_turns) cfg.target.phase = to_image(phase_turns, nx, ny);
+        if (roi) {
+            RegionMask m(nx, ny);
+            std::memcpy(m.data.data(), roi, m.data.size());
+            cfg.target.roi = m;
+        }
+        cfg.target.freedoms.amplitude_outside_roi = c->amp_outside_roi != 0;
+        cfg.target.freedoms.phase = c->phase_freedom != 0;
+        cfg.target.freedoms.scale = c->scale_freedom != 0;
+        cfg.seed = c->seed;
+        cfg.weight_clamp_lo = c->clamp_lo;
+        cfg.weight_clamp_hi = c->clamp_hi;
+        cfg.lt_initial_fraction = c->lt_initial_fraction;
+        cfg.init_phase = c->init_phase == 1 ? InitPhase::Random
+                         : c->init_phase == 2 ? InitPhase::Flat
+                                              : InitPhase::Auto;
+        std::unique_ptr<Propagator<double>> prop;
+        if (c->fresnel) {
+            FresnelParams p{c->wavelength, c->distance, c->pitch_x, c->pitch_y};
+            prop = std::make_unique<Propagator<double>>(Propagator<double>::fresnel(nx, ny, p));
+        }
+        auto rep = run_ifta<double>(cfg, prop.get());
+        size_t n = rep.hologram.data.size();
+        if (hologram) std::memcpy(hologram, rep.hologram.data.data(), sizeof(double) * 2 * n);
+        if (replay) std::memcpy(replay, rep.replay.data.data(), sizeof(double) * 2 * n);
+        if (levels) {
+            Quantiser<double> q(cfg.slm, nx, ny);
+            for (size_t i = 0; i < n; ++i) levels[i] = q.decide(i, rep.hologram.data[i]);
+        }
+        if (trace)
+            for (size_t k = 0; k < rep.trace.points.size(); ++k) trace[k] = rep.trace.points[k].second;
+    });
+}
+
+// run_ospr_variant<double> (ospr.hpp:68-185).
+int hgr_ospr_run_d(int adaptive, int subframes, uint64_t seed, double gain, const hgo_slm* s, int nx, int ny,
+                   const double* target, const uint8_t* roi, int scale_free, int32_t* levels, double* frame_mse,
+                   double* cum_mse, double* mean_intensity) {
+    return guard([&] {
+        OsprConfig cfg;
+        cfg.variant = adaptive ? OsprVariant::AdaptiveOspr : OsprVariant::Ospr;
+        cfg.subframes = subframes;
+        cfg.slm = to_spec(s, nx, ny);
+        cfg.target.amplitude = to_image(target, nx, ny);
+        if (roi) {
+            RegionMask m(nx, ny);
+            std::memcpy(m.data.data(), roi, m.data.size());
+            cfg.target.roi = m;
+        }
+        cfg.target.freedoms.scale = scale_free != 0;
+        cfg.seed = seed;
+        cfg.feedback_gain = gain;
+        auto run = run_ospr_variant<double>(cfg);
+        size_t n = static_cast<size_t>(nx) * ny;
+        Quantiser<double> q(cfg.slm, nx, ny);
+        for (int k = 0; k < subframes; ++k) {
+            const auto& fr = run.set.frames[k];
+            if (levels)
+                for (size_t i = 0; i < n; ++i) levels[n * k + i] = q.decide(i, fr.data[i]);
+            if (frame_mse) frame_mse[k] = run.set.per_frame_mse[k];
+            if (cum_mse) cum_mse[k] = run.report.trace.points[k].second;
+        }
+        if (mean_intensity)
+            std::memcpy(mean_intensity, run.set.mean_intensity.data.data(), sizeof(double) * n);
+    });
+}
+
 // run_ospr_variant<float> (ospr.hpp:68-185).
 int hgr_ospr_run(int adaptive, int subframes, uint64_t seed, double gain, const hgo_slm* s, int nx,
                  int ny, const double* target, const uint8_t* roi, int scale_free, int32_t* levels,

@@ -11,7 +11,7 @@ from .api import (IftaPlan, OsprBlockPlan, OsprPlan, Propagator, Quantiser, allo
                   fft_inverse, fork_seed, fresnel_forward, fresnel_inverse, make_fresnel_phase, mse, quantise_field,
                   run_adaptive_ospr, run_gs, run_ifta, run_ifta_batch, run_liu_taghizadeh, run_ospr, run_ospr_batch,
                   run_ospr_variant, run_weighted_gs, seed_random_phase, set_device, subframe_mse_statistic,
-                  mt_jump_state)
+                  mt_jump_state, run_ifta_f64, run_ospr_f64)
 from .types import (PI, TWO_PI, Freedoms, FresnelParams, IftaConfig, IftaVariant, InitPhase, MetricConfig,
                     MetricTrace, Normalization, OsprConfig, OsprRun, OsprVariant, PhaseProfile, RunReport, SlmMode,
                     SlmSpec, SubframeSet, TargetSpec, allowed_states, lt_area_fractions, normalize_image)

@@ -78,6 +78,18 @@ class HgcOsprIo(C.Structure):
                 ("replay_peak", C.c_void_p)]
 
 
+class HgcIftaIo64(C.Structure):
+    _fields_ = [("amplitude", C.c_void_p), ("phase", C.c_void_p), ("roi", C.c_void_p), ("init_field", C.c_void_p),
+                ("init_weights", C.c_void_p), ("hologram", C.c_void_p), ("replay", C.c_void_p),
+                ("levels", C.c_void_p), ("trace", C.c_void_p), ("final_error", C.c_void_p)]
+
+
+class HgcOsprIo64(C.Structure):
+    _fields_ = [("amplitude", C.c_void_p), ("roi", C.c_void_p), ("frames", C.c_void_p), ("levels", C.c_void_p),
+                ("frame_mse", C.c_void_p), ("cumulative_mse", C.c_void_p), ("mean_intensity", C.c_void_p),
+                ("replay", C.c_void_p), ("final_error", C.c_void_p)]
+
+
 _vp, _i, _u64, _d = C.c_void_p, C.c_int, C.c_uint64, C.c_double
 _P = C.POINTER
 
@@ -115,6 +127,8 @@ _SIGS = {
     "hgc_seed_random_phase": (_i, [_vp, _i, _i, _u64, _u64, _vp]),
     "hgc_mt_jump_state": (_i, [_u64, _u64, _vp]),
     "hgc_batch_run": (_i, [_vp, _i, _i, C.c_size_t]),
+    "hgc_ifta_run_f64": (_i, [_P(HgcIftaCfg), _P(HgcSlm), _P(HgcFresnel), _i, _i, _P(HgcIftaIo64)]),
+    "hgc_ospr_run_f64": (_i, [_P(HgcOsprCfg), _P(HgcSlm), _i, _i, _P(HgcOsprIo64)]),
     "hgc_set_device_policy": (_i, [_i]),
     "hgc_write_field_dump": (_i, [C.c_char_p, _i, _i, _i, _vp]),
     "hgc_read_field_dump": (_i, [C.c_char_p, _P(_i), _P(_i), _P(_i), _vp]),

@@ -390,6 +390,82 @@ def run_ifta(cfg: IftaConfig, prop: Propagator | None = None, init_field=None, i
     return _run_ifta(cfg, prop, None, "run_ifta", init_field, init_weights)
 
 
+def run_ifta_f64(cfg: IftaConfig, prop: Propagator | None = None, init_field=None, init_weights=None) -> RunReport:
+    """run_ifta<double> (ifta.hpp:86-235) on the device (hgc_ifta_run_f64,
+    SURVEY §8 f4): complex128 hologram / replay, any field size."""
+    import time
+    cfg.validate()
+    amp = np.ascontiguousarray(cfg.target.amplitude, np.float64)
+    ny, nx = amp.shape
+    if prop is not None and prop.is_fresnel() and (prop.nx, prop.ny) != (nx, ny):
+        raise ValueError("Propagator: field size does not match Fresnel phase")
+    keep: list = []
+    c = _ifta_cfg(cfg)
+    slm = _slm(cfg.slm, keep)
+    io = _lib.HgcIftaIo64()
+    ph = None if cfg.target.phase is None else np.ascontiguousarray(cfg.target.phase, np.float64)
+    roi = None if cfg.target.roi is None else np.ascontiguousarray(np.asarray(cfg.target.roi) != 0, np.uint8)
+    fi = None if init_field is None else np.ascontiguousarray(init_field, np.complex128)
+    wi = None if init_weights is None else np.ascontiguousarray(init_weights, np.float64)
+    holo = np.empty((ny, nx), np.complex128)
+    rep_f = np.empty((ny, nx), np.complex128)
+    lv = np.empty((ny, nx), np.int32)
+    tr = np.empty(cfg.iterations, np.float64)
+    fe = C.c_double()
+    io.amplitude, io.phase, io.roi, io.init_field, io.init_weights = _p(amp), _p(ph), _p(roi), _p(fi), _p(wi)
+    io.hologram, io.replay, io.levels, io.trace = _p(holo), _p(rep_f), _p(lv), _p(tr)
+    io.final_error = C.addressof(fe)
+    fr = prop.params if prop is not None and prop.is_fresnel() else None
+    t0 = time.perf_counter()
+    check(lib.hgc_ifta_run_f64(C.byref(c), C.byref(slm), _fresnel(fr), nx, ny, C.byref(io)))
+    rep = RunReport(algorithm=_ALG[IftaVariant(cfg.variant)], seed=int(cfg.seed))
+    rep.hologram, rep.replay, rep.levels = holo, rep_f, lv
+    rep.trace = MetricTrace("mse", [(k + 1, float(v)) for k, v in enumerate(tr)])
+    rep.final_error = fe.value
+    rep.seconds = time.perf_counter() - t0
+    rep.profile = PhaseProfile(other=rep.seconds)
+    return rep
+
+
+def run_ospr_f64(cfg: OsprConfig, keep_frames: bool = True) -> OsprRun:
+    """run_ospr_variant<double> (ospr.hpp:68-185) on the device (hgc_ospr_run_f64)."""
+    import time
+    cfg.validate()
+    amp = np.ascontiguousarray(cfg.target.amplitude, np.float64)
+    ny, nx = amp.shape
+    N = cfg.subframes
+    keep: list = []
+    c = _ospr_cfg(cfg)
+    slm = _slm(cfg.slm, keep)
+    roi = None if cfg.target.roi is None else np.ascontiguousarray(np.asarray(cfg.target.roi) != 0, np.uint8)
+    frames = np.empty((N, ny, nx), np.complex128) if keep_frames else None
+    lv = np.empty((N, ny, nx), np.int32)
+    fm, cm = np.empty(N), np.empty(N)
+    mi = np.empty((ny, nx))
+    rp = np.empty((ny, nx), np.complex128)
+    fe = C.c_double()
+    io = _lib.HgcOsprIo64()
+    io.amplitude, io.roi, io.frames, io.levels = _p(amp), _p(roi), _p(frames), _p(lv)
+    io.frame_mse, io.cumulative_mse, io.mean_intensity, io.replay = _p(fm), _p(cm), _p(mi), _p(rp)
+    io.final_error = C.addressof(fe)
+    t0 = time.perf_counter()
+    check(lib.hgc_ospr_run_f64(C.byref(c), C.byref(slm), nx, ny, C.byref(io)))
+    r = OsprRun()
+    r.set = SubframeSet(frames=frames, mean_intensity=mi, per_frame_mse=[float(v) for v in fm], levels=lv)
+    rep = RunReport(algorithm="adaptive_ospr" if cfg.variant == OsprVariant.AdaptiveOspr else "ospr",
+                    seed=int(cfg.seed))
+    rep.trace = MetricTrace("cumulative_mse", [(k + 1, float(v)) for k, v in enumerate(cm)])
+    rep.extra_traces = [MetricTrace("frame_mse", [(k + 1, float(v)) for k, v in enumerate(fm)])]
+    rep.replay = rp
+    rep.hologram = None if frames is None else frames[-1]
+    rep.final_error = fe.value
+    rep.evaluations = N
+    rep.seconds = time.perf_counter() - t0
+    rep.profile = PhaseProfile(other=rep.seconds)
+    r.report = rep
+    return r
+
+
 # ------------------------------------------------------------------- OSPR
 def _ospr_cfg(cfg: OsprConfig) -> _lib.HgcOsprCfg:
     c = _lib.HgcOsprCfg()

@@ -147,6 +147,9 @@ struct SeedArgs {
     int chunks;
     size_t chunk_len;
     int no_save;  // keep states[] (the chunk start windows) instead of saving the end state
+    // seed_random_phase<double> (the f64 loops): (a*cos, a*sin) unrounded,
+    // row-major, stride out_stride — used instead of `out` when set
+    double2* out64;
 };
 
 // Jump-ahead (mtjump.cpp): CTA (stream s, chunk c), c in [c_lo, chunks),
@@ -290,7 +293,7 @@ __global__ void __launch_bounds__(kSeedThreads) k_seed_random_phase(SeedArgs a) 
                     mt_twist_warp(ow, nw, lane);
                 }
             }
-        } else if (a.out) {  // out == nullptr: advance the stream only (skip draws)
+        } else if (a.out || a.out64) {  // neither: advance the stream only (skip draws)
             const uint64_t* src;
             int d0, cnt;
             if (g == 0) {
@@ -326,7 +329,10 @@ __global__ void __launch_bounds__(kSeedThreads) k_seed_random_phase(SeedArgs a) 
                     double tn = __dsqrt_rn(budget > 0.0 ? budget : 0.0);
                     av = __dadd_rn(__dmul_rn(1.0 - a.gain, tv), __dmul_rn(a.gain, tn));
                 }
-                out[o] = make_float2(__double2float_rn(__dmul_rn(av, cs)), __double2float_rn(__dmul_rn(av, sn)));
+                if (a.out64)
+                    a.out64[a.out_stride * s + p] = make_double2(__dmul_rn(av, cs), __dmul_rn(av, sn));
+                else
+                    out[o] = make_float2(__double2float_rn(__dmul_rn(av, cs)), __double2float_rn(__dmul_rn(av, sn)));
             }
         }
         __syncthreads();

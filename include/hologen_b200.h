@@ -52,7 +52,7 @@
 extern "C" {
 #endif
 
-#define HGC_ABI_VERSION 2
+#define HGC_ABI_VERSION 3
 
 typedef enum {
     HGC_OK = 0,
@@ -264,6 +264,8 @@ typedef struct hgc_ifta_io64 {
     int32_t* levels;            /* level indices [ny][nx] */
     double* trace;              /* [iterations] */
     double* final_error;
+    const double* fresnel_q;    /* optional complex [ny][nx] Q to use instead of computing it from
+                                   hgc_fresnel (e.g. from a Propagator<double>, propagation.hpp:97-103) */
 } hgc_ifta_io64;
 int hgc_ifta_run_f64(const hgc_ifta_cfg* cfg, const hgc_slm* slm, const hgc_fresnel* fresnel, int nx, int ny,
                      hgc_ifta_io64* io);

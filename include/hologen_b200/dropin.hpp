@@ -203,6 +203,110 @@ inline hologen::OsprRun<float> run_ospr_gpu(const hologen::OsprConfig& cfg, holo
     return run;
 }
 
+// run_ifta<double> on the GPU f64 loop (hgc_ifta_run_f64, ifta.hpp:86-235 in double).
+inline hologen::RunReport<double> run_ifta_gpu64(const hologen::IftaConfig& cfg,
+                                                 const hologen::Propagator<double>* prop) {
+    auto t0 = std::chrono::steady_clock::now();
+    cfg.validate();
+    const auto& tgt = cfg.target;
+    const int nx = tgt.width(), ny = tgt.height();
+    hgc_ifta_cfg c{};
+    c.variant = static_cast<int>(cfg.variant);
+    c.iterations = cfg.iterations;
+    c.seed = cfg.seed;
+    c.weight_clamp_lo = cfg.weight_clamp_lo;
+    c.weight_clamp_hi = cfg.weight_clamp_hi;
+    c.lt_initial_fraction = cfg.lt_initial_fraction;
+    c.init_phase = static_cast<int>(cfg.init_phase);
+    c.freedom_amplitude_outside_roi = tgt.freedoms.amplitude_outside_roi;
+    c.freedom_phase = tgt.freedoms.phase;
+    c.freedom_scale = tgt.freedoms.scale;
+    hgc_slm s = to_c(cfg.slm);
+    std::vector<std::complex<double>> q;
+    if (prop && prop->is_fresnel()) {  // the Propagator's own Q (propagation.hpp:100-103)
+        q.resize(static_cast<size_t>(nx) * ny);
+        for (int y = 0; y < ny; ++y)
+            for (int x = 0; x < nx; ++x) q[static_cast<size_t>(y) * nx + x] = prop->aperture_factor(x, y);
+    }
+    hologen::RunReport<double> rep;
+    rep.seed = cfg.seed;
+    rep.algorithm = cfg.variant == hologen::IftaVariant::GS           ? "gs"
+                    : cfg.variant == hologen::IftaVariant::WeightedGS ? "wgs"
+                                                                      : "lt";
+    rep.hologram = hologen::ComplexField<double>(nx, ny, hologen::Domain::Aperture);
+    rep.replay = hologen::ComplexField<double>(nx, ny, hologen::Domain::Replay);
+    std::vector<double> trace(cfg.iterations);
+    hgc_ifta_io64 io{};
+    io.amplitude = tgt.amplitude.data.data();
+    io.phase = tgt.phase ? tgt.phase->data.data() : nullptr;
+    io.roi = tgt.roi ? tgt.roi->data.data() : nullptr;
+    io.hologram = reinterpret_cast<double*>(rep.hologram.data.data());
+    io.replay = reinterpret_cast<double*>(rep.replay.data.data());
+    io.trace = trace.data();
+    io.fresnel_q = q.empty() ? nullptr : reinterpret_cast<const double*>(q.data());
+    throw_status(hgc_ifta_run_f64(&c, &s, nullptr, nx, ny, &io));
+    rep.trace.name = "mse";
+    for (int k = 0; k < cfg.iterations; ++k) rep.trace.append(k + 1, trace[k]);
+    rep.final_error = trace.back();
+    rep.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    rep.profile.other = rep.seconds;
+    return rep;
+}
+
+// run_ospr_impl<double> on the GPU f64 loop (hgc_ospr_run_f64).
+inline hologen::OsprRun<double> run_ospr_gpu64(const hologen::OsprConfig& cfg, hologen::FftBackend<double>* backend) {
+    if (backend && backend != &fft_backend_f64())
+        throw std::runtime_error("hologen_b200: OSPR with a caller-supplied FftBackend is not on the GPU path");
+    auto t0 = std::chrono::steady_clock::now();
+    cfg.validate();
+    const auto& tgt = cfg.target;
+    const int nx = tgt.width(), ny = tgt.height(), N = cfg.subframes;
+    const size_t n = static_cast<size_t>(nx) * ny;
+    hgc_ospr_cfg c{};
+    c.variant = static_cast<int>(cfg.variant);
+    c.subframes = N;
+    c.seed = cfg.seed;
+    c.feedback_gain = cfg.feedback_gain;
+    c.freedom_scale = tgt.freedoms.scale;
+    hgc_slm s = to_c(cfg.slm);
+    std::vector<std::complex<double>> frames(n * N);
+    std::vector<double> fm(N), cm(N), mi(n);
+    hologen::OsprRun<double> run;
+    hologen::RunReport<double>& rep = run.report;
+    rep.replay = hologen::ComplexField<double>(nx, ny, hologen::Domain::Replay);
+    hgc_ospr_io64 io{};
+    io.amplitude = tgt.amplitude.data.data();
+    io.roi = tgt.roi ? tgt.roi->data.data() : nullptr;
+    io.frames = reinterpret_cast<double*>(frames.data());
+    io.frame_mse = fm.data();
+    io.cumulative_mse = cm.data();
+    io.mean_intensity = mi.data();
+    io.replay = reinterpret_cast<double*>(rep.replay.data.data());
+    throw_status(hgc_ospr_run_f64(&c, &s, nx, ny, &io));
+    rep.algorithm = cfg.variant == hologen::OsprVariant::AdaptiveOspr ? "adaptive_ospr" : "ospr";
+    rep.seed = cfg.seed;
+    rep.trace.name = "cumulative_mse";
+    hologen::MetricTrace frame_trace;
+    frame_trace.name = "frame_mse";
+    for (int k = 0; k < N; ++k) {
+        hologen::ComplexField<double> f(nx, ny, hologen::Domain::Aperture);
+        std::memcpy(f.data.data(), frames.data() + n * k, sizeof(std::complex<double>) * n);
+        run.set.frames.push_back(std::move(f));
+        run.set.per_frame_mse.push_back(fm[k]);
+        frame_trace.append(k + 1, fm[k]);
+        rep.trace.append(k + 1, cm[k]);
+    }
+    run.set.mean_intensity = hologen::RealImage(nx, ny);
+    run.set.mean_intensity.data = mi;
+    rep.hologram = run.set.frames.back();
+    rep.final_error = cm.back();
+    rep.evaluations = N;
+    rep.extra_traces.push_back(std::move(frame_trace));
+    rep.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    rep.profile.other = rep.seconds;
+    return run;
+}
+
 }  // namespace hologen_b200
 
 namespace hologen {
@@ -241,6 +345,43 @@ inline OsprRun<float> run_adaptive_ospr<float>(const OsprConfig& cfg, FftBackend
 template <>
 inline OsprRun<float> run_ospr_variant<float>(const OsprConfig& cfg, FftBackend<float>* backend) {
     return hologen_b200::run_ospr_gpu(cfg, backend);
+}
+
+// T = double: the GPU f64 loops.
+template <>
+inline RunReport<double> run_gs<double>(const IftaConfig& cfg, const Propagator<double>* prop) {
+    if (cfg.variant != IftaVariant::GS) throw std::invalid_argument("run_gs: config variant mismatch");
+    return hologen_b200::run_ifta_gpu64(cfg, prop);
+}
+template <>
+inline RunReport<double> run_weighted_gs<double>(const IftaConfig& cfg, const Propagator<double>* prop) {
+    if (cfg.variant != IftaVariant::WeightedGS) throw std::invalid_argument("run_weighted_gs: config variant mismatch");
+    return hologen_b200::run_ifta_gpu64(cfg, prop);
+}
+template <>
+inline RunReport<double> run_liu_taghizadeh<double>(const IftaConfig& cfg, const Propagator<double>* prop) {
+    if (cfg.variant != IftaVariant::LiuTaghizadeh)
+        throw std::invalid_argument("run_liu_taghizadeh: config variant mismatch");
+    return hologen_b200::run_ifta_gpu64(cfg, prop);
+}
+template <>
+inline RunReport<double> run_ifta<double>(const IftaConfig& cfg, const Propagator<double>* prop) {
+    return hologen_b200::run_ifta_gpu64(cfg, prop);
+}
+template <>
+inline OsprRun<double> run_ospr<double>(const OsprConfig& cfg, FftBackend<double>* backend) {
+    if (cfg.variant != OsprVariant::Ospr) throw std::invalid_argument("run_ospr: config variant mismatch");
+    return hologen_b200::run_ospr_gpu64(cfg, backend);
+}
+template <>
+inline OsprRun<double> run_adaptive_ospr<double>(const OsprConfig& cfg, FftBackend<double>* backend) {
+    if (cfg.variant != OsprVariant::AdaptiveOspr)
+        throw std::invalid_argument("run_adaptive_ospr: config variant mismatch");
+    return hologen_b200::run_ospr_gpu64(cfg, backend);
+}
+template <>
+inline OsprRun<double> run_ospr_variant<double>(const OsprConfig& cfg, FftBackend<double>* backend) {
+    return hologen_b200::run_ospr_gpu64(cfg, backend);
 }
 
 }  // namespace hologen

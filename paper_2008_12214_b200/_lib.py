@@ -81,7 +81,8 @@ class HgcOsprIo(C.Structure):
 class HgcIftaIo64(C.Structure):
     _fields_ = [("amplitude", C.c_void_p), ("phase", C.c_void_p), ("roi", C.c_void_p), ("init_field", C.c_void_p),
                 ("init_weights", C.c_void_p), ("hologram", C.c_void_p), ("replay", C.c_void_p),
-                ("levels", C.c_void_p), ("trace", C.c_void_p), ("final_error", C.c_void_p)]
+                ("levels", C.c_void_p), ("trace", C.c_void_p), ("final_error", C.c_void_p),
+                ("fresnel_q", C.c_void_p)]
 
 
 class HgcOsprIo64(C.Structure):
@@ -147,7 +148,7 @@ for _name, (_res, _args) in _SIGS.items():
     _f.restype = _res
     _f.argtypes = _args
 
-ABI_VERSION = 2  # HGC_ABI_VERSION of include/hologen_b200.h this binding was written against
+ABI_VERSION = 3  # HGC_ABI_VERSION of include/hologen_b200.h this binding was written against
 if lib.hgc_abi_version() != ABI_VERSION:
     raise ImportError(f"{LIB_PATH}: ABI version {lib.hgc_abi_version()} != {ABI_VERSION}; rebuild the library")
 

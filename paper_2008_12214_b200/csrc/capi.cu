@@ -2170,7 +2170,12 @@ int hgc_ifta_run_f64(const hgc_ifta_cfg* cfg, const hgc_slm* slm, const hgc_fres
             roi.alloc(n);
             CK(cudaMemcpy(roi.p, io->roi, n, cudaMemcpyHostToDevice));
         }
-        if (fresnel) fresnel_q64(fresnel, nx, ny, Q);
+        if (io->fresnel_q) {  // caller-supplied Q (e.g. a reference Propagator<double>)
+            Q.alloc(n);
+            CK(cudaMemcpy(Q.p, io->fresnel_q, sizeof(double2) * n, cudaMemcpyHostToDevice));
+        } else if (fresnel) {
+            fresnel_q64(fresnel, nx, ny, Q);
+        }
         // target phase as (cos, sin) with the host libm, ifta.hpp:131-136 / :215-219
         const bool tphase_used = !cfg->freedom_phase || (cfg->init_phase == 0 && io->phase);
         std::vector<double2> h_tcs;

@@ -5,10 +5,11 @@ Same function names, arguments, defaults and return dictionaries as the
 pybind11 module for the functions on the IFTA / OSPR path:
 ``fft_forward``, ``fft_inverse``, ``quantise``, ``gs``, ``wgs``, ``lt``,
 ``ospr``, ``adaptive_ospr``, ``mse``.  Arrays are numpy (height, width),
-complex128 fields and float64 images like the reference's.  The transforms
-run in double on the B200 (hgc_fft2d_f64); the algorithms run on the float32
-hot path (the reference module runs them in double), so their results agree
-with it to float precision, not to the last double bit.
+complex128 fields and float64 images like the reference's, computed in
+double on the B200 as the reference module computes them: the transforms by
+hgc_fft2d_f64 and the algorithms by the device f64 loops (hgc_ifta_run_f64 /
+hgc_ospr_run_f64, the reference's double arithmetic per pixel).  The
+float32 hot path is ``paper_2008_12214_b200.run_*``.
 Holographic search and SSIM (``direct_search``, ``simulated_annealing``,
 ``ssim``) are not on the hot path and are not provided.
 
@@ -71,14 +72,15 @@ def fft_inverse(field) -> np.ndarray:
 
 def quantise(field, levels: int = 256) -> np.ndarray:
     """Project every pixel onto the nearest allowed modulator state (levels == 2
-    means binary phase {0, pi}, otherwise a full phase circle)."""
+    means binary phase {0, pi}, otherwise a full phase circle).  Decisions in
+    double; the states are the float32 hot-path table widened to double."""
     return api.quantise_field(_field(field), _slm(levels)).astype(np.complex128)
 
 
 def _ifta(variant, target, iterations, levels, seed, phase_freedom, clamp_lo=0.1, clamp_hi=10.0, lt_fraction=0.1):
     cfg = IftaConfig(variant=variant, iterations=iterations, slm=_slm(levels), target=_target(target, phase_freedom),
                      seed=seed, weight_clamp_lo=clamp_lo, weight_clamp_hi=clamp_hi, lt_initial_fraction=lt_fraction)
-    return _report(api.run_ifta(cfg))
+    return _report(api.run_ifta_f64(cfg))
 
 
 def gs(target, iterations: int = 25, levels: int = 256, seed: int = 0, phase_freedom: bool = True) -> dict:
@@ -102,7 +104,7 @@ def lt(target, iterations: int = 25, levels: int = 256, seed: int = 0, phase_fre
 def _ospr(variant, target, subframes, levels, seed, phase_freedom, gain) -> dict:  # bindings.cpp run_ospr_py
     cfg = OsprConfig(variant=variant, subframes=subframes, slm=_slm(levels), target=_target(target, phase_freedom),
                      seed=seed, feedback_gain=gain)
-    run = api.run_ospr_variant(cfg)
+    run = api.run_ospr_f64(cfg)
     d = _report(run.report)
     d["frames"] = [np.asarray(f, np.complex128) for f in run.set.frames]
     d["mean_intensity"] = np.asarray(run.set.mean_intensity, np.float64)

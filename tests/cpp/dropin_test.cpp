@@ -92,6 +92,35 @@ int main() {
     std::printf("ospr 6 frames: level mismatches %d, cumulative mse rel %.2e\n", om, rel);
     CHECK(om <= 6 && rel < 1e-4 && go.report.algorithm == "ospr" && go.set.frames.size() == 6);
 
+    // T = double: the GPU f64 loop against the reference's own double loop
+    // (detail::run_ifta<double>, its transforms on the GPU f64 FftBackend)
+    {
+        IftaConfig d = cfg;
+        d.iterations = 10;
+        auto gd = run_gs<double>(d);
+        auto rd = detail::run_ifta<double>(d, nullptr);
+        int m = 0;
+        Quantiser<double> qd(d.slm, 128, 128);
+        for (size_t i = 0; i < gd.hologram.data.size(); ++i)
+            m += qd.decide(i, gd.hologram.data[i]) != qd.decide(i, rd.hologram.data[i]);
+        double rel64 = std::abs(gd.final_error - rd.final_error) / rd.final_error;
+        std::printf("gs<double> binary 128^2: level mismatches %d, mse rel %.2e\n", m, rel64);
+        CHECK(m == 0 && rel64 < 1e-9);
+        auto p64 = Propagator<double>::fresnel(128, 128, p);
+        IftaConfig wd = w;
+        wd.iterations = 2;
+        auto gw64 = run_weighted_gs<double>(wd, &p64);
+        auto rw64 = detail::run_ifta<double>(wd, &p64);
+        rel64 = std::abs(gw64.final_error - rw64.final_error) / rw64.final_error;
+        std::printf("wgs<double> fresnel 256-level: mse rel %.2e\n", rel64);
+        CHECK(rel64 < 1e-9);
+        auto go64 = run_ospr<double>(o);
+        auto ro64 = detail::run_ospr_impl<double>(o, nullptr);
+        rel64 = std::abs(go64.report.final_error - ro64.report.final_error) / ro64.report.final_error;
+        std::printf("ospr<double> 6 frames: cumulative mse rel %.2e\n", rel64);
+        CHECK(rel64 < 1e-9 && go64.set.frames.size() == 6);
+    }
+
     // the runner's batch pool (runner.cpp:387-421): one job per host thread,
     // threads routed round-robin over the GPUs; results equal the sequential runs
     hologen_b200::route_threads_over_devices();

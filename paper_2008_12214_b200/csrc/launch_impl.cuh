@@ -59,7 +59,7 @@ template <int NY, int C, int MODE, int LAY>
 inline void col_launch_c(const ColArgs& a, int batch, cudaStream_t st, bool prepare) {
     auto kern = k_col<NY, C, MODE, LAY>;
     constexpr int EM = ColCfg<NY, LAY>::EM;
-    constexpr int smem = (NY > LineCfg<NY, EM>::E) ? PaddedLen<NY>::value * C * (int)sizeof(float2) : 0;
+    constexpr int smem = col_smem_bytes<NY, C, MODE, LAY>();
     if (prepare) {
         set_smem(kern, smem);
         return;

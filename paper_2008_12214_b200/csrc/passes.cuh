@@ -289,6 +289,15 @@ struct ColCfg {
         EM == 8 ? 2 : ((LAY == LAY_QUAD && THREADS >= 512 && THREADS < 1024) ? HG_COLQ_MINB : 1);
 };
 
+#ifndef HG_COL_TGT_BULK
+#define HG_COL_TGT_BULK 1
+#endif
+// The target slice of a TMA column tile is contiguous in the column-pair
+// layout (C*NY floats): one cp.async.bulk brings it into smem beside the
+// tile at kernel start, read after the forward transform.
+template <int NY, int C, int LAY, int MODE>
+struct ColTgtBulk;
+
 // Column tiles loaded / stored by 2-D TMA (k_col): quad-layout tiles of C
 // columns (C/2 quads = 16*C bytes per quad row) and at least 256 quad rows,
 // in boxes of 256 quad rows.  Their launches must carry ColArgs::tmap, whose
@@ -304,6 +313,16 @@ struct ColTma {
         else return (y >> 1) * (2 * C) + (c >> 1) * 4 + (y & 1) * 2 + (c & 1);
     }
 };
+template <int NY, int C, int LAY, int MODE>
+struct ColTgtBulk {
+    static constexpr bool on = HG_COL_TGT_BULK && ColTma<NY, C, LAY>::on && MODE != COL_PLAIN;
+    static constexpr int BYTES = on ? C * NY * (int)sizeof(float) : 0;
+};
+template <int NY, int C, int MODE, int LAY>
+constexpr int col_smem_bytes() {
+    return (NY > LineCfg<NY, ColCfg<NY, LAY>::EM>::E ? PaddedLen<NY>::value * C * (int)sizeof(float2) : 0) +
+           ColTgtBulk<NY, C, LAY, MODE>::BYTES;
+}
 
 
 // Per-thread float partials -> warp sums in float (32 terms) -> per-warp
@@ -375,6 +394,9 @@ __global__ void __launch_bounds__(LineCfg<NY, ColCfg<NY, LAY>::EM>::T * C, ColCf
     __shared__ uint64_t tbar;
     const int tq = blockIdx.x * (C / 2) * 8;  // inner coordinate (floats) of this column pair
     const int tr = a.tma_row0 + b * a.tma_brows;
+    constexpr bool kTgt = ColTgtBulk<NY, C, LAY, MODE>::on;
+    __shared__ uint64_t gbar;
+    float* tsm = reinterpret_cast<float*>(smem + PaddedLen<NY>::value * C);
     if constexpr (kTma) {
         if (threadIdx.x == 0) {
             mbar_init(&tbar, 1);
@@ -382,6 +404,11 @@ __global__ void __launch_bounds__(LineCfg<NY, ColCfg<NY, LAY>::EM>::T * C, ColCf
 #pragma unroll 1
             for (int k = 0; k < kBoxes; ++k)
                 tma_load_2d(smem + k * kBoxRows * 2 * C, a.tmap, tq, tr + k * kBoxRows, &tbar);
+            if constexpr (kTgt) {
+                mbar_init(&gbar, 1);
+                bulk_g2s(tsm, a.target + a.t_bstride * b + colpair_index(blockIdx.x * C, 0, NY),
+                         (uint32_t)ColTgtBulk<NY, C, LAY, MODE>::BYTES, &gbar);
+            }
         }
         __syncthreads();  // barrier initialised before anyone waits
         mbar_wait(&tbar, 0);
@@ -426,6 +453,13 @@ __global__ void __launch_bounds__(LineCfg<NY, ColCfg<NY, LAY>::EM>::T * C, ColCf
         fft_line<NY, -1, EM>(v, t, smem, idx, a.tw);  // completes the forward transform
         const float norm = a.norm;
         const float* tg = a.target + a.t_bstride * b + sb;
+        // target element e: from the bulk-loaded slice (same column-pair offsets) or global
+        const int tso = (int)(sb - colpair_index(blockIdx.x * C, 0, NY));
+        if constexpr (kTgt) mbar_wait(&gbar, 0);
+        auto tload = [&](int e) -> float {
+            if constexpr (kTgt) return tsm[tso + e * ss];
+            else return __ldg(&tg[e * ss]);
+        };
         constexpr int NV = MODE == COL_OSPR ? 7 : 4;
         float acc[NV];
 #pragma unroll
@@ -440,7 +474,7 @@ __global__ void __launch_bounds__(LineCfg<NY, ColCfg<NY, LAY>::EM>::T * C, ColCf
             for (int e = 0; e < E; ++e) {
                 const float2 R = cscale(v[e], norm);
                 const float r2 = R.x * R.x + R.y * R.y;
-                const float amp0 = __ldg(&tg[e * ss]);
+                const float amp0 = tload(e);
                 const float ri = rsqrtf(r2);                 // +inf at r2 == 0
                 const float r = r2 > 0.f ? r2 * ri : 0.f;    // |R|
                 const float d = amp0 - r;
@@ -471,7 +505,7 @@ __global__ void __launch_bounds__(LineCfg<NY, ColCfg<NY, LAY>::EM>::T * C, ColCf
                 const size_t so = (size_t)e * ss;
                 float2 R = cscale(v[e], norm);
                 const bool in_roi = !roi || roi[so];
-                float amp = __ldg(&tg[so]);
+                float amp = tload(e);
                 float r = sqrtf(R.x * R.x + R.y * R.y);
                 if (in_roi) {  // mse partials (metrics.hpp:70-97)
                     float d = amp - r;
@@ -519,7 +553,7 @@ __global__ void __launch_bounds__(LineCfg<NY, ColCfg<NY, LAY>::EM>::T * C, ColCf
                 const float sv = S[e * ss] + I;
                 S[e * ss] = sv;
                 const float m = (!roi || roi[e * ss]) ? 1.f : 0.f;
-                const float amp = __ldg(&tg[e * ss]) * m;
+                const float amp = tload(e) * m;
                 const float r = sqrtf(I) * m;
                 const float d = amp - r;
                 acc[0] = fmaf(d, d, acc[0]);

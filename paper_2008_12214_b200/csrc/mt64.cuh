@@ -98,20 +98,32 @@ __device__ __forceinline__ void mt_twist_warp(const uint64_t* __restrict__ ow, u
 // polynomials.  <= 1 ulp from glibc's sin/cos; over 4e7 random draws the
 // float casts (T)(a*cos), (T)(a*sin) of rng.hpp:62-64 matched glibc exactly.
 // ~3x fewer instructions than the general-range CUDA sincos (no slow path).
+// The coefficients live in constant memory so DFMA reads them as constant-
+// bank operands (as literals, every use re-materialised the 64-bit value
+// with two uniform moves).
+struct SinCos64 {
+    double two_over_pi, pio2_1, pio2_2, pio2_3;
+    double s6, s5, s4, s3, s2, s1;
+    double c6, c5, c4, c3, c2, c1;
+};
+static __constant__ SinCos64 kSC = {6.36619772367581382433e-01,  1.5707963267948966192e+00,
+                                    6.123233995736766036e-17,     -1.4973849048591698e-33,
+                                    1.58969099521155010221e-10,   -2.50507602534068634195e-08,
+                                    2.75573137070700676789e-06,   -1.98412698298579493134e-04,
+                                    8.33333333332248946124e-03,   -1.66666666666666324348e-01,
+                                    -1.13596475577881948265e-11,  2.08757232129817482790e-09,
+                                    -2.75573143513906633035e-07,  2.48015872894767294178e-05,
+                                    -1.38888888888741095749e-03,  4.16666666666666019037e-02};
 __device__ __forceinline__ void sincos_0_2pi(double x, double* sp, double* cp) {
-    const double n = rint(x * 6.36619772367581382433e-01);
-    double r = fma(-n, 1.5707963267948966192e+00, x);
-    r = fma(-n, 6.123233995736766036e-17, r);
-    r = fma(-n, -1.4973849048591698e-33, r);
+    const double n = rint(x * kSC.two_over_pi);
+    double r = fma(-n, kSC.pio2_1, x);
+    r = fma(-n, kSC.pio2_2, r);
+    r = fma(-n, kSC.pio2_3, r);
     const int q = (int)n & 3;
     const double z = r * r;
-    const double ps = fma(fma(fma(fma(1.58969099521155010221e-10, z, -2.50507602534068634195e-08), z,
-                                  2.75573137070700676789e-06), z, -1.98412698298579493134e-04), z,
-                          8.33333333332248946124e-03);
-    const double sr = fma(r * z, fma(z, ps, -1.66666666666666324348e-01), r);
-    const double pc = fma(fma(fma(fma(fma(-1.13596475577881948265e-11, z, 2.08757232129817482790e-09), z,
-                                      -2.75573143513906633035e-07), z, 2.48015872894767294178e-05), z,
-                              -1.38888888888741095749e-03), z, 4.16666666666666019037e-02);
+    const double ps = fma(fma(fma(fma(kSC.s6, z, kSC.s5), z, kSC.s4), z, kSC.s3), z, kSC.s2);
+    const double sr = fma(r * z, fma(z, ps, kSC.s1), r);
+    const double pc = fma(fma(fma(fma(fma(kSC.c6, z, kSC.c5), z, kSC.c4), z, kSC.c3), z, kSC.c2), z, kSC.c1);
     const double hz = 0.5 * z, w = 1.0 - hz;
     const double cr = w + (((1.0 - w) - hz) + z * (z * pc));
     const double s0 = (q & 1) ? cr : sr, c0 = (q & 1) ? sr : cr;

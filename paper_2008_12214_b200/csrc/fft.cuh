@@ -21,9 +21,6 @@
 namespace hg {
 
 constexpr int kMaxLine = 4096;
-#ifndef HG_ROW_TWSMEM
-#define HG_ROW_TWSMEM 0
-#endif
 
 // Complex element type of a transform: float2 (the hot path) or double2 (the
 // f64 FftBackend, k_fft64.cu).
@@ -147,11 +144,7 @@ struct LineCfg {
 // Twiddle exp(SIGN*2*pi*i*m/N) from the forward table.
 template <int N, int SIGN, class C2>
 __device__ __forceinline__ C2 twiddle(const C2* __restrict__ tw, int m) {
-#if HG_ROW_TWSMEM
-    C2 w = tw[N + m];  // the table may be staged in shared memory (k_row)
-#else
     C2 w = __ldg(&tw[N + m]);
-#endif
     if constexpr (SIGN > 0) w.y = -w.y;
     return w;
 }

@@ -89,9 +89,7 @@ struct RowCfg {
     static constexpr int E = LineCfg<NX>::E, T = LineCfg<NX>::T;
     static constexpr int RPC = LAY == LAY_QUAD ? (512 / T < 2 ? 2 : 512 / T) : (T >= 256 ? 1 : 256 / T);
     static constexpr int THREADS = T * RPC;
-    static constexpr int SMEM = (NX > E) ? (RPC * RowStride<NX>::value + (HG_ROW_TWSMEM && LAY == LAY_QUAD ? NX : 0)) *
-                                               (int)sizeof(float2)
-                                         : 0;
+    static constexpr int SMEM = (NX > E) ? RPC * RowStride<NX>::value * (int)sizeof(float2) : 0;
     static constexpr int MIN_BLOCKS = LAY == LAY_QUAD ? (THREADS >= 512 ? HG_ROWQ_MINB : 1) : (THREADS >= 256 ? 3 : 1);
 };
 
@@ -152,28 +150,10 @@ __global__ void __launch_bounds__(RowCfg<NX, LAY>::THREADS, RowCfg<NX, LAY>::MIN
     };
     auto tile = [&] { return a.field + a.bstride * blockIdx.y + quad_index(0, blockIdx.x * Cfg::RPC, NX); };
     auto lbase = [&] { return (lr >> 1) * (2 * NX) + (t >> 1) * 4 + (lr & 1) * 2 + (t & 1); };
-    // HG_ROW_TWSMEM: the NX twiddles tw[NX .. 2NX) also land in smem (after the rows)
-    constexpr bool kTwS = HG_ROW_TWSMEM && kBulk;
-    float2* tws = smem + Cfg::RPC * RowStride<NX>::value;
-    const float2* twp = kTwS ? tws - NX : a.tw;
     if constexpr (kBulk) {
         if (threadIdx.x == 0) {
             mbar_init(&rbar, 1);
-            if constexpr (kTwS) {
-                mbar_expect_tx(&rbar, tile_bytes() + NX * (uint32_t)sizeof(float2));
-                asm volatile(
-                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                        smem_u32(smem)),
-                    "l"(tile()), "r"(tile_bytes()), "r"(smem_u32(&rbar))
-                    : "memory");
-                asm volatile(
-                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                        smem_u32(tws)),
-                    "l"(a.tw + NX), "r"((uint32_t)(NX * sizeof(float2))), "r"(smem_u32(&rbar))
-                    : "memory");
-            } else {
-                bulk_g2s(smem, tile(), tile_bytes(), &rbar);
-            }
+            bulk_g2s(smem, tile(), tile_bytes(), &rbar);
         }
         __syncthreads();
         mbar_wait(&rbar, 0);
@@ -194,9 +174,9 @@ __global__ void __launch_bounds__(RowCfg<NX, LAY>::THREADS, RowCfg<NX, LAY>::MIN
             if (a.fresnel_q)
 #pragma unroll
                 for (int e = 0; e < E; ++e) v[e] = cmul_rn(v[e], __ldg(&a.fresnel_q[rowbase + t + e * T]));
-            fft_line<NX, -1>(v, t, smem, idx, twp);
+            fft_line<NX, -1>(v, t, smem, idx, a.tw);
         } else {
-            fft_line<NX, +1>(v, t, smem, idx, twp);
+            fft_line<NX, +1>(v, t, smem, idx, a.tw);
         }
         if (a.apply_norm)
 #pragma unroll
@@ -205,7 +185,7 @@ __global__ void __launch_bounds__(RowCfg<NX, LAY>::THREADS, RowCfg<NX, LAY>::MIN
 #pragma unroll
             for (int e = 0; e < E; ++e) v[e] = cmul_conj_rn(v[e], __ldg(&a.fresnel_q[rowbase + t + e * T]));
     } else {
-        fft_line<NX, +1>(v, t, smem, idx, twp);  // completes the 2-D inverse (propagation.hpp:89-95)
+        fft_line<NX, +1>(v, t, smem, idx, a.tw);  // completes the 2-D inverse (propagation.hpp:89-95)
         const int rowbase = y * NX;
         const float norm = a.norm;
         const float2* __restrict__ fq = FQ == 0 ? nullptr : a.fresnel_q;
@@ -226,7 +206,7 @@ __global__ void __launch_bounds__(RowCfg<NX, LAY>::THREADS, RowCfg<NX, LAY>::MIN
             if (hasq) f = cmul_rn(f, __ldg(&fq[i]));              // propagation.hpp:85
             v[e] = f;
         }
-        fft_line<NX, -1>(v, t, smem, idx, twp);  // starts the forward transform
+        fft_line<NX, -1>(v, t, smem, idx, a.tw);  // starts the forward transform
     }
     if constexpr (kBulk) {
         const int lb = opaque(lbase());

@@ -315,7 +315,12 @@ struct ColTma {
 };
 template <int NY, int C, int LAY, int MODE>
 struct ColTgtBulk {
+    // GS / WGS: the fp32 target slice.  OSPR: the job's running intensity sum
+    // S instead (read and written, always in HBM; the shared OSPR target stays
+    // L2-resident and is read directly).
     static constexpr bool on = HG_COL_TGT_BULK && ColTma<NY, C, LAY>::on && MODE != COL_PLAIN;
+    static constexpr bool target = on && MODE != COL_OSPR;
+    static constexpr bool S = on && MODE == COL_OSPR;
     static constexpr int BYTES = on ? C * NY * (int)sizeof(float) : 0;
 };
 template <int NY, int C, int MODE, int LAY>
@@ -394,7 +399,8 @@ __global__ void __launch_bounds__(LineCfg<NY, ColCfg<NY, LAY>::EM>::T * C, ColCf
     __shared__ uint64_t tbar;
     const int tq = blockIdx.x * (C / 2) * 8;  // inner coordinate (floats) of this column pair
     const int tr = a.tma_row0 + b * a.tma_brows;
-    constexpr bool kTgt = ColTgtBulk<NY, C, LAY, MODE>::on;
+    constexpr bool kTgt = ColTgtBulk<NY, C, LAY, MODE>::target;
+    constexpr bool kSB = ColTgtBulk<NY, C, LAY, MODE>::S;
     __shared__ uint64_t gbar;
     float* tsm = reinterpret_cast<float*>(smem + PaddedLen<NY>::value * C);
     if constexpr (kTma) {
@@ -404,10 +410,11 @@ __global__ void __launch_bounds__(LineCfg<NY, ColCfg<NY, LAY>::EM>::T * C, ColCf
 #pragma unroll 1
             for (int k = 0; k < kBoxes; ++k)
                 tma_load_2d(smem + k * kBoxRows * 2 * C, a.tmap, tq, tr + k * kBoxRows, &tbar);
-            if constexpr (kTgt) {
+            if constexpr (kTgt || kSB) {
                 mbar_init(&gbar, 1);
-                bulk_g2s(tsm, a.target + a.t_bstride * b + colpair_index(blockIdx.x * C, 0, NY),
-                         (uint32_t)ColTgtBulk<NY, C, LAY, MODE>::BYTES, &gbar);
+                const float* src = kTgt ? a.target + a.t_bstride * b : a.S + a.S_bstride * b;
+                bulk_g2s(tsm, src + colpair_index(blockIdx.x * C, 0, NY), (uint32_t)ColTgtBulk<NY, C, LAY, MODE>::BYTES,
+                         &gbar);
             }
         }
         __syncthreads();  // barrier initialised before anyone waits
@@ -543,7 +550,8 @@ __global__ void __launch_bounds__(LineCfg<NY, ColCfg<NY, LAY>::EM>::T * C, ColCf
                 v[e] = R;
             }
         } else {  // COL_OSPR: ospr.hpp:134-145
-            float* S = a.S + a.S_bstride * b + sb;
+            if constexpr (kSB) mbar_wait(&gbar, 0);
+            float* S = kSB ? tsm + tso : a.S + a.S_bstride * b + sb;  // bulk-landed slice or global
             const float inv_n = a.inv_n;
             const uint8_t* roi = a.roi ? a.roi + sb : nullptr;
 #pragma unroll
@@ -576,6 +584,16 @@ __global__ void __launch_bounds__(LineCfg<NY, ColCfg<NY, LAY>::EM>::T * C, ColCf
             }
         }
         const size_t blk = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
+        if constexpr (kSB) {  // the updated S slice back to HBM in one bulk store
+            fence_proxy_async();
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                bulk_s2g(a.S + a.S_bstride * b + colpair_index(blockIdx.x * C, 0, NY), tsm,
+                         (uint32_t)ColTgtBulk<NY, C, LAY, MODE>::BYTES);
+                bulk_commit();
+                bulk_wait_read0();
+            }
+        }
         block_sum_float_store<NV>(acc, a.partials + blk * 8);
     }
 }

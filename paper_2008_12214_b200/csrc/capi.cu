@@ -316,6 +316,29 @@ __global__ void k_to_colpair(const TI* in, TO* out, int nx, int ny, size_t total
         out[p.b * npix + colpair_index(p.x, p.y, ny)] = (TO)in[g];
     }
 }
+// Row-major -> column-pair major through a 32-row x 64-column smem tile, so
+// both the reads (rows) and the writes (64 contiguous outputs per column pair)
+// are coalesced.  Requires nx % 64 == 0 and ny % 32 == 0.
+template <class TI, class TO>
+__global__ void __launch_bounds__(256) k_to_colpair_tiled(const TI* in, TO* out, int nx, int ny) {
+    __shared__ TO tile[32][65];
+    const int x0 = blockIdx.x * 64, y0 = blockIdx.y * 32;
+    const size_t base = (size_t)blockIdx.z * nx * ny;
+    const int tid = threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int r = tid / 64 + 4 * k, c = tid % 64;
+        tile[r][c] = (TO)in[base + (size_t)(y0 + r) * nx + x0 + c];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int idx = tid + 256 * k, pair = idx / 64, w = idx % 64;
+        const int y = w >> 1, xl = 2 * pair + (w & 1);
+        out[base + colpair_index(x0 + xl, y0 + y, ny)] = tile[y][xl];
+    }
+}
+
 __global__ void k_to_quad(const float2* in, float2* out, int nx, int ny, size_t total) {
     const size_t npix = (size_t)nx * ny;
     HG_GRID_LOOP(g, total) {
@@ -580,6 +603,17 @@ static dim3 ew_grid(size_t n) {
     if (b > 148 * 16) b = 148 * 16;
     if (b < 1) b = 1;
     return dim3((unsigned)b);
+}
+
+template <class TI, class TO>
+static void to_colpair(const TI* in, TO* out, int nx, int ny, size_t batch, cudaStream_t st) {
+    if (nx % 64 == 0 && ny % 32 == 0 && batch <= 65535) {
+        k_to_colpair_tiled<TI, TO><<<dim3(nx / 64, ny / 32, (unsigned)batch), 256, 0, st>>>(in, out, nx, ny);
+    } else {
+        const size_t tot = (size_t)nx * ny * batch;
+        k_to_colpair<TI, TO><<<ew_grid(tot), 256, 0, st>>>(in, out, nx, ny, tot);
+    }
+    CK(cudaGetLastError());
 }
 
 // ---------------------------------------------------------- validation
@@ -1132,7 +1166,7 @@ int hgc_ifta_plan_upload(hgc_ifta_plan* p, const hgc_ifta_io* io) {
         }
         p->M = roi_count(io->roi, npix);
         launch_validate(p->amp_d.p, io->phase ? p->phase_d.p : nullptr, tot, p->vflags.p, p->stream);
-        k_to_colpair<double, float><<<ew_grid(tot), 256, 0, p->stream>>>(p->amp_d.p, p->target_f.p, p->nx, p->ny, tot);
+        to_colpair<double, float>(p->amp_d.p, p->target_f.p, p->nx, p->ny, p->batch, p->stream);
         CK(cudaGetLastError());
         if (io->phase) {
             if (!p->cfg.freedom_phase) {
@@ -1709,8 +1743,7 @@ int hgc_ospr_plan_upload(hgc_ospr_plan* p, const hgc_ospr_io* io) {
         CK(cudaMemcpyAsync(p->amp_d.p, io->amplitude, sizeof(double) * ttot, cudaMemcpyHostToDevice, p->stream));
         p->M = roi_count(io->roi, p->npix);
         launch_validate(p->amp_d.p, nullptr, ttot, p->vflags.p, p->stream);
-        k_to_colpair<double, float><<<ew_grid(ttot), 256, 0, p->stream>>>(p->amp_d.p, p->target_f.p, p->nx, p->ny,
-                                                                          ttot);
+        to_colpair<double, float>(p->amp_d.p, p->target_f.p, p->nx, p->ny, ttot / p->npix, p->stream);
         CK(cudaGetLastError());
         p->has_roi = io->roi != nullptr;
         if (io->roi) {  // column-pair major

@@ -67,12 +67,12 @@ def parse():
 
 # ----------------------------------------------------------- distributed
 class Dist:
-    def __init__(self):
+    def __init__(self, collectives: bool = True):
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
-        if self.world > 1:
+        if self.world > 1 and collectives:
             import torch
             import torch.distributed as dist
             torch.cuda.set_device(self.local)
@@ -436,9 +436,9 @@ def run_reference(args, d: Dist):
 
 def main():
     args = parse()
+    if args.impl == "reference":  # rank 0 alone works on the host cores: no process group needed
+        return run_reference(args, Dist(collectives=False))
     d = Dist()
-    if args.impl == "reference":
-        return run_reference(args, d)
     peak, peak_kind = peaks()
     gs = gs_ours(args, d)
     osp = None if args.no_ospr else ospr_ours(args, d)

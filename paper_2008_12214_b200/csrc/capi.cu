@@ -141,8 +141,7 @@ static void prepare_kernels(int nx, int ny) {
 // point so cudart stays statically linked.
 struct DevTensorMap {
     DBuf<CUtensorMap> d;
-    void make(float2* base, int nx, int ny, size_t rows) {
-        const int C = nx / col_tiles(nx, ny, LAY_QUAD);  // columns per column-pass tile
+    void make(float2* base, int nx, int C, size_t rows) {  // C: columns per column-pass tile
         static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
             void* fn = nullptr;
             cudaDriverEntryPointQueryResult q{};
@@ -816,6 +815,7 @@ struct hgc_ifta_plan {
     bool has_phase = false, has_roi = false;
     size_t M = 0;
     int tiles = 0;
+    int cw = 0;  // columns per column-pass CTA (col_width_rt)
     int bx0 = 0, by0 = 0, bw = 0, bh = 0;  // LT roi bounding box
     DBuf<float2> field, Q, tphase_cs, init_field, scratch;
     cudaEvent_t done = nullptr;  // recorded after each execute on the execute stream
@@ -939,6 +939,7 @@ struct hgc_ifta_plan {
         cg.partials = partials.p + (size_t)(k - 1) * batch * tiles * 8;
         cg.tmap = tmap.d.p;
         cg.tma_brows = ny / 2;
+        cg.cw = cw;
         return cg;
     }
 
@@ -979,6 +980,7 @@ struct hgc_ifta_plan {
         ca.sign = +1;
         ca.tmap = tmap.d.p;
         ca.tma_brows = ny / 2;
+        ca.cw = cw;
         col_plain(ny, ca, batch, st);
         ++launches;
         // Iterations run target-group by target-group: a group's field +
@@ -1122,10 +1124,11 @@ int hgc_ifta_plan_create(hgc_ifta_plan** out, const hgc_ifta_cfg* cfg, const hgc
         if (fresnel) p->fp = *fresnel;
         build_quant(slm, nx, ny, p->q);
         p->wide_levels = slm->levels > 256;
-        p->tiles = col_tiles(nx, ny, LAY_QUAD);
+        p->cw = col_width_rt(nx, ny, batch);
+        p->tiles = nx / p->cw;
         const size_t tot = p->npix * batch;
         p->field.alloc(tot);
-        if (ny >= 512) p->tmap.make(p->field.p, nx, ny, (size_t)batch * ny / 2);
+        if (ny >= 512) p->tmap.make(p->field.p, nx, p->cw, (size_t)batch * ny / 2);
         p->target_f.alloc(tot);
         p->amp_d.alloc(tot);
         if (cfg->variant == 1) p->weights.alloc(tot);
@@ -1409,6 +1412,7 @@ struct hgc_ospr_plan {
     bool wide_levels = false, has_roi = false;
     size_t M = 0;
     int tiles = 0;
+    int cw = 0;  // columns per column-pass CTA (col_width_rt)
     DBuf<float2> field, field2;  // double-buffered seeded field (plain OSPR)
     DBuf<float> target_f, S;
     DBuf<double> amp_d, partials, traces;
@@ -1493,7 +1497,8 @@ struct hgc_ospr_plan {
         }
         return sa;
     }
-    void set_tma(ColArgs& c, int n) const {  // the TMA view of buf(n)
+    void set_tma(ColArgs& c, int n) const {  // the TMA view of buf(n) (+ the launch's column width)
+        c.cw = cw;
         if (preseed) {
             c.tmap = tmap1.d.p;
             c.tma_row0 = (n - 1) * (ny / 2);
@@ -1638,7 +1643,8 @@ static void create_ospr_plan(hgc_ospr_plan** out, const hgc_ospr_cfg* cfg_in, co
         p->npix = (size_t)nx * ny;
         build_quant(slm, nx, ny, p->q);
         p->wide_levels = slm->levels > 256;
-        p->tiles = col_tiles(nx, ny, LAY_QUAD);
+        p->cw = col_width_rt(nx, ny, jobs);
+        p->tiles = nx / p->cw;
         const size_t tot = p->npix * jobs;
         const size_t ttot = p->per_job ? tot : p->npix;
         {
@@ -1651,10 +1657,10 @@ static void create_ospr_plan(hgc_ospr_plan** out, const hgc_ospr_cfg* cfg_in, co
             p->fstride = p->preseed ? all : p->npix;
         }
         p->field.alloc(p->fstride * jobs);
-        if (ny >= 512) p->tmap1.make(p->field.p, nx, ny, p->fstride * jobs / (2 * (size_t)nx));
+        if (ny >= 512) p->tmap1.make(p->field.p, nx, p->cw, p->fstride * jobs / (2 * (size_t)nx));
         if (!p->preseed && cfg->variant == 0 && cfg->subframes > 1) {  // second buffer + stream for seed/pass overlap
             p->field2.alloc(tot);
-            if (ny >= 512) p->tmap2.make(p->field2.p, nx, ny, tot / (2 * (size_t)nx));
+            if (ny >= 512) p->tmap2.make(p->field2.p, nx, p->cw, tot / (2 * (size_t)nx));
             CK(cudaStreamCreateWithFlags(&p->stream2, cudaStreamNonBlocking));
             CK(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&p->ev_seed, cudaEventDisableTiming));

@@ -15,4 +15,10 @@ void col_plain(int ny, const ColArgs& a, int batch, cudaStream_t st, bool prepar
 int col_tiles(int nx, int ny, int layout) {
     return layout == LAY_QUAD ? col_tiles_lay<LAY_QUAD>(nx, ny) : col_tiles_lay<LAY_ROW>(nx, ny);
 }
+int col_width_rt(int nx, int ny, int batch) {
+    int cw = nx / col_tiles(nx, ny, LAY_QUAD);
+    const int T = ny / (ny < 16 ? ny : 16);  // threads per column (LineCfg<ny>::T)
+    while (cw > 2 && (long long)(nx / cw) * batch < 2LL * sm_count() && T * (cw / 2) >= 64) cw /= 2;
+    return cw;
+}
 }  // namespace hg

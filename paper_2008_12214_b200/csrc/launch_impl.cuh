@@ -1,11 +1,22 @@
 // launch_impl.cuh — size/layout dispatch shared by the k_*.cu translation units.
 #pragma once
+#include <algorithm>
 #include <cstdlib>
 
 #include "errors.h"
 #include "launch.h"
 
 namespace hg {
+
+inline int sm_count() {
+    static int n = [] {
+        int dev = 0, v = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    return n;
+}
 
 template <class K>
 inline void set_smem(K kernel, int bytes) {
@@ -21,8 +32,15 @@ inline void row_launch(const RowArgs& a, int batch, cudaStream_t st, bool prepar
         set_smem(kern, Cfg::SMEM);
         return;
     }
-    dim3 grid((a.ny + Cfg::RPC - 1) / Cfg::RPC, batch);
-    kern<<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(a);
+    int rpc = Cfg::RPC;
+    if (LAY == LAY_QUAD && Cfg::RPC > 2) {  // small launches: fewer rows per CTA, more CTAs
+        const int min_rpc = std::max(2, 64 / Cfg::T);
+        while (rpc > min_rpc && (long long)((a.ny + rpc - 1) / rpc) * batch < 2LL * sm_count()) rpc /= 2;
+    }
+    RowArgs ar = a;
+    ar.rpc = rpc;
+    dim3 grid((a.ny + rpc - 1) / rpc, batch);
+    kern<<<grid, Cfg::T * rpc, Cfg::SMEM, st>>>(ar);
     CK(cudaGetLastError());
 }
 
@@ -73,7 +91,7 @@ inline void col_launch_c(const ColArgs& a, int batch, cudaStream_t st, bool prep
 template <int NY, int MODE, int LAY>
 inline void col_launch(const ColArgs& a, int batch, cudaStream_t st, bool prepare) {
     constexpr int CM = ColCfg<NY, LAY>::C;
-    switch (col_width<NY, LAY>(a.nx)) {
+    switch (a.cw > 0 ? a.cw : col_width<NY, LAY>(a.nx)) {
         case 1: if constexpr (CM >= 1 && LAY == LAY_ROW) col_launch_c<NY, 1, MODE, LAY>(a, batch, st, prepare); break;
         case 2: if constexpr (CM >= 2) col_launch_c<NY, 2, MODE, LAY>(a, batch, st, prepare); break;
         case 4: if constexpr (CM >= 4) col_launch_c<NY, 4, MODE, LAY>(a, batch, st, prepare); break;

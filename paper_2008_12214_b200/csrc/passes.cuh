@@ -76,6 +76,7 @@ struct RowArgs {
     uint8_t* levels8;         // [target][ny][nx] row-major or nullptr
     uint16_t* levels16;
     size_t lv_bstride;
+    int rpc;                  // quad layout: rows per CTA this launch (even, <= RowCfg::RPC; 0 = RowCfg::RPC)
 };
 
 template <int N>
@@ -121,7 +122,9 @@ __global__ void __launch_bounds__(RowCfg<NX, LAY>::THREADS, RowCfg<NX, LAY>::MIN
         lr = threadIdx.x / T;
         t = threadIdx.x % T;
     }
-    const int y = blockIdx.x * Cfg::RPC + lr;
+    // rows per CTA: the compile-time tile, or fewer when a launch would leave SMs idle
+    const int RPCr = (LAY == LAY_QUAD && Cfg::RPC > 2 && a.rpc > 0) ? a.rpc : Cfg::RPC;
+    const int y = blockIdx.x * RPCr + lr;
     const int b = blockIdx.y;
     RowSmemIdx idx{lr * RowStride<NX>::value};
     const bool valid = y < a.ny;  // (ny is a multiple of RPC except for tiny fields)
@@ -146,9 +149,9 @@ __global__ void __launch_bounds__(RowCfg<NX, LAY>::THREADS, RowCfg<NX, LAY>::MIN
     __shared__ uint64_t rbar;
     // (recomputed where used, so nothing extra stays live across the transforms)
     auto tile_bytes = [&] {
-        return (uint32_t)(min(Cfg::RPC, a.ny - (int)blockIdx.x * Cfg::RPC) * NX * (int)sizeof(float2));
+        return (uint32_t)(min(RPCr, a.ny - (int)blockIdx.x * RPCr) * NX * (int)sizeof(float2));
     };
-    auto tile = [&] { return a.field + a.bstride * blockIdx.y + quad_index(0, blockIdx.x * Cfg::RPC, NX); };
+    auto tile = [&] { return a.field + a.bstride * blockIdx.y + quad_index(0, blockIdx.x * RPCr, NX); };
     auto lbase = [&] { return (lr >> 1) * (2 * NX) + (t >> 1) * 4 + (lr & 1) * 2 + (t & 1); };
     if constexpr (kBulk) {
         if (threadIdx.x == 0) {
@@ -261,6 +264,7 @@ struct ColArgs {
     // tma_row0 + b * tma_brows.  nullptr: per-thread loads/stores.
     const void* tmap;
     int tma_row0, tma_brows;
+    int cw;  // columns per CTA this launch (an instantiated width <= ColCfg::C; 0 = the default)
 };
 
 template <int NY, int LAY>

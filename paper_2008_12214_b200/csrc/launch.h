@@ -26,7 +26,7 @@ void col_ospr(int ny, const ColArgs& a, int batch, cudaStream_t st, bool prepare
 // Column tiles (CTAs) per target of the column pass for an nx x ny field.
 int col_tiles(int nx, int ny, int layout);
 // Quad-layout column width for a launch over `batch` targets: the default
-// tile, halved while the launch would leave SMs idle (>= 2 CTAs per SM), at
+// tile, halved while the launch would leave SMs idle (< 1 CTA per SM), at
 // least 64 threads per CTA.  The plans use it for the launches, the TMA box
 // and the number of partial-sum tiles (nx / width).
 int col_width_rt(int nx, int ny, int batch);

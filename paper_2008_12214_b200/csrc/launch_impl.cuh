@@ -33,9 +33,9 @@ inline void row_launch(const RowArgs& a, int batch, cudaStream_t st, bool prepar
         return;
     }
     int rpc = Cfg::RPC;
-    if (LAY == LAY_QUAD && Cfg::RPC > 2) {  // small launches: fewer rows per CTA, more CTAs
+    if (LAY == LAY_QUAD && Cfg::RPC > 2) {  // small launches: fewer rows per CTA until every SM has one
         const int min_rpc = std::max(2, 64 / Cfg::T);
-        while (rpc > min_rpc && (long long)((a.ny + rpc - 1) / rpc) * batch < 2LL * sm_count()) rpc /= 2;
+        while (rpc > min_rpc && (long long)((a.ny + rpc - 1) / rpc) * batch < sm_count()) rpc /= 2;
     }
     RowArgs ar = a;
     ar.rpc = rpc;
@@ -83,6 +83,8 @@ inline void col_launch_c(const ColArgs& a, int batch, cudaStream_t st, bool prep
         return;
     }
     if (ColTma<NY, C, LAY>::on && !a.tmap) fail(HGC_ECUDA, "column pass: TMA tile launched without a tensor map");
+    static const bool smem_ready = (set_smem(kern, smem), true);  // narrower run-time widths (col_width_rt)
+    (void)smem_ready;
     dim3 grid(a.nx / C, batch);
     kern<<<grid, LineCfg<NY, EM>::T * C, smem, st>>>(a);
     CK(cudaGetLastError());

@@ -222,7 +222,9 @@ def test_batch_equals_single():
     for t in range(3):
         single = hg.run_gs(cfg_for(amps[t], slm, 6, seed=1 + t))
         assert np.array_equal(reps[t].levels, single.levels)
-        assert reps[t].final_error == single.final_error
+        # the launch's column width may differ between batch and single runs
+        # (col_width_rt), which only reorders the MSE partial sums
+        assert abs(reps[t].final_error - single.final_error) <= 1e-12 * single.final_error
 
 
 def test_validation_errors():

@@ -28,7 +28,8 @@ def test_plan_shapes_match_oracle(oracle, ny, nx):
 @pytest.mark.parametrize("batch,n", [(1, 256), (3, 256), (5, 1024), (17, 128)])
 def test_batch_groups_match_single_runs(batch, n):
     """Batched plans (incl. L2-resident target groups at small sizes) equal
-    independent single-target runs bit for bit."""
+    independent single-target runs: identical levels; MSE traces equal up to
+    the summation order (the launch's column width can differ, col_width_rt)."""
     amps = np.stack([np.roll(hg.patterns.bench_target(n), 11 * t, axis=1) for t in range(batch)])
     slm = hg.SlmSpec.full_circle_phase(8)
     cfg = hg.IftaConfig(iterations=4, slm=slm, target=hg.TargetSpec(amps[0]), seed=1)
@@ -37,7 +38,7 @@ def test_batch_groups_match_single_runs(batch, n):
         c = hg.IftaConfig(iterations=4, slm=slm, target=hg.TargetSpec(amps[t]), seed=1 + t)
         single = hg.run_gs(c)
         assert np.array_equal(reps[t].levels, single.levels)
-        assert np.array_equal(reps[t].trace.values(), single.trace.values())
+        assert np.max(np.abs(reps[t].trace.values() - single.trace.values()) / single.trace.values()) < 1e-12
 
 
 @pytest.mark.parametrize("ny,nx,N", [(2, 2, 3), (4096, 2, 2), (512, 64, 4)])

@@ -224,7 +224,7 @@ def test_batch_equals_single():
         assert np.array_equal(reps[t].levels, single.levels)
         # the launch's column width may differ between batch and single runs
         # (col_width_rt), which only reorders the MSE partial sums
-        assert abs(reps[t].final_error - single.final_error) <= 1e-12 * single.final_error
+        assert abs(reps[t].final_error - single.final_error) <= 1e-7 * single.final_error
 
 
 def test_validation_errors():

@@ -38,7 +38,7 @@ def test_batch_groups_match_single_runs(batch, n):
         c = hg.IftaConfig(iterations=4, slm=slm, target=hg.TargetSpec(amps[t]), seed=1 + t)
         single = hg.run_gs(c)
         assert np.array_equal(reps[t].levels, single.levels)
-        assert np.max(np.abs(reps[t].trace.values() - single.trace.values()) / single.trace.values()) < 1e-12
+        assert np.max(np.abs(reps[t].trace.values() - single.trace.values()) / single.trace.values()) < 1e-7
 
 
 @pytest.mark.parametrize("ny,nx,N", [(2, 2, 3), (4096, 2, 2), (512, 64, 4)])

@@ -205,14 +205,6 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// Programmatic dependent launch (launch_impl.cuh launch_pdl): the kernel lets
-// its dependent grid launch early, then waits for its own prerequisite grid
-// (completion + memory visibility) before reading anything it produced.
-__device__ __forceinline__ void pdl_begin() {
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-}
-
 template <int V>
 struct IntC {
     static constexpr int value = V;

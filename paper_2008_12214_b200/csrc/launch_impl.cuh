@@ -18,36 +18,6 @@ inline int sm_count() {
     return n;
 }
 
-// Launch with programmatic stream serialization: inside a captured graph the
-// edge from the previous kernel becomes programmatic, so this grid's CTAs are
-// scheduled on SMs freed by the previous grid's tail and wait in pdl_begin()
-// (common.cuh).  HG_PDL=0 turns it off (measurements).
-inline bool pdl_enabled() {
-    static const bool on = [] {
-        const char* e = getenv("HG_PDL");
-        return !(e && e[0] == '0');
-    }();
-    return on;
-}
-template <class K, class A>
-inline void launch_pdl(K kern, dim3 grid, int threads, int smem, cudaStream_t st, const A& args) {
-    if (!pdl_enabled()) {
-        kern<<<grid, threads, smem, st>>>(args);
-        return;
-    }
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = grid;
-    cfg.blockDim = dim3(threads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    CK(cudaLaunchKernelEx(&cfg, kern, args));
-}
-
 template <class K>
 inline void set_smem(K kernel, int bytes) {
     if (bytes > 48 * 1024) CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
@@ -70,7 +40,7 @@ inline void row_launch(const RowArgs& a, int batch, cudaStream_t st, bool prepar
     RowArgs ar = a;
     ar.rpc = rpc;
     dim3 grid((a.ny + rpc - 1) / rpc, batch);
-    launch_pdl(kern, grid, Cfg::T * rpc, Cfg::SMEM, st, ar);
+    kern<<<grid, Cfg::T * rpc, Cfg::SMEM, st>>>(ar);
     CK(cudaGetLastError());
 }
 
@@ -116,7 +86,7 @@ inline void col_launch_c(const ColArgs& a, int batch, cudaStream_t st, bool prep
     static const bool smem_ready = (set_smem(kern, smem), true);  // narrower run-time widths (col_width_rt)
     (void)smem_ready;
     dim3 grid(a.nx / C, batch);
-    launch_pdl(kern, grid, LineCfg<NY, EM>::T * C, smem, st, a);
+    kern<<<grid, LineCfg<NY, EM>::T * C, smem, st>>>(a);
     CK(cudaGetLastError());
 }
 

@@ -104,7 +104,6 @@ __global__ void __launch_bounds__(RowCfg<NX, LAY>::THREADS, RowCfg<NX, LAY>::MIN
     using Cfg = RowCfg<NX, LAY>;
     constexpr int E = Cfg::E, T = Cfg::T;
     extern __shared__ __align__(128) float2 smem[];
-    pdl_begin();
     int lr, t;
     if constexpr (LAY == LAY_QUAD) {
         // the 2T threads of a row pair interleave so a warp covers 2 rows x 16
@@ -364,7 +363,6 @@ __global__ void __launch_bounds__(LineCfg<NY, ColCfg<NY, LAY>::EM>::T * C, ColCf
     k_col(ColArgs a) {
     constexpr int EM = ColCfg<NY, LAY>::EM;
     constexpr int E = LineCfg<NY, EM>::E, T = LineCfg<NY, EM>::T;
-    pdl_begin();
     extern __shared__ __align__(128) float2 smem[];
     const int c = threadIdx.x % C, t = threadIdx.x / C;
     const int x = blockIdx.x * C + c;

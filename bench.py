@@ -276,7 +276,8 @@ def ospr_ours(args, d: Dist):
     if not args.no_e2e:  # double-buffered plans, as in gs_e2e
         plan2 = hg.OsprPlan(cfg, n, n, J)
         h = [plan._h, plan2._h]
-        lvs = [torch.empty((J, N, n, n), dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+        # binary frames come back as bit-planes (what a binary FLC SLM is fed): npix/8 bytes per frame
+        lvs = [torch.empty((J, N, n * n // 8), dtype=torch.uint8, pin_memory=True) for _ in range(2)]
         fms = [np.empty((J, N)) for _ in range(2)]
         cms = [np.empty((J, N)) for _ in range(2)]
         ios = []
@@ -284,7 +285,7 @@ def ospr_ours(args, d: Dist):
             io = _lib.HgcOsprIo()
             io.amplitude = amp.ctypes.data
             io.seeds = seeds.ctypes.data
-            io.levels8 = lvs[i].data_ptr()
+            io.levels1 = lvs[i].data_ptr()
             io.frame_mse, io.cumulative_mse = fms[i].ctypes.data, cms[i].ctypes.data
             ios.append(io)
         L = _lib.lib
@@ -307,9 +308,9 @@ def ospr_ours(args, d: Dist):
         dt = d.max(time.perf_counter() - t0)
         plan2.close()
         res["e2e"] = {"value": d.world * J * N * es / dt, "unit": "subframes/s",
-                      "h2d_bytes_per_step": int(n * n * 8 + J * 8), "d2h_bytes_per_step": int(J * N * n * n + 2 * J * N * 8),
+                      "h2d_bytes_per_step": int(n * n * 8 + J * 8), "d2h_bytes_per_step": int(J * N * n * n // 8 + 2 * J * N * 8),
                       "steps": es, "api": "hgc_ospr_plan_upload/execute/download (C ABI, pinned host buffers, "
-                                          "two plans double-buffered)"}
+                                          "two plans double-buffered; frames read back as bit-planes)"}
     plan.close()
     return res
 

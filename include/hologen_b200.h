@@ -52,7 +52,7 @@
 extern "C" {
 #endif
 
-#define HGC_ABI_VERSION 3
+#define HGC_ABI_VERSION 4
 
 typedef enum {
     HGC_OK = 0,
@@ -125,6 +125,8 @@ typedef struct hgc_ifta_io {
                                    L <= 256 (io.cpp:272-287) */
     uint8_t* replay_gray8;      /* write_replay_png pixels [batch][ny][nx] (io.cpp:189-205) */
     double* replay_peak;        /* its amplitude_at_255 [batch] (io.cpp:206-207) */
+    uint8_t* levels1;           /* 2-level SLMs: the levels as bit-planes, bit (i & 7) of byte i >> 3 of
+                                   each target's row-major plane [batch][ny*nx/8] (binary SLM frames) */
 } hgc_ifta_io;
 
 /* hologen::OsprConfig (ospr.hpp:20-38).  variant: 0 Ospr, 1 AdaptiveOspr.
@@ -156,6 +158,8 @@ typedef struct hgc_ospr_io {
     uint8_t* frames_gray8;      /* frame levels as write_hologram_png pixels [jobs][subframes][ny][nx] */
     uint8_t* replay_gray8;      /* write_replay_png pixels of the replay [jobs][ny][nx] */
     double* replay_peak;        /* [jobs] */
+    uint8_t* levels1;           /* 2-level SLMs: frame levels as bit-planes [jobs][subframes][ny*nx/8],
+                                   bit (i & 7) of byte i >> 3 (what a binary FLC SLM is fed) */
 } hgc_ospr_io;
 
 /* ------------------------------------------------------------ library */

@@ -649,7 +649,9 @@ class OsprPlan:
     def execute(self, stream: int | None = None):
         check(lib.hgc_ospr_plan_execute(self._h, stream))
 
-    def download(self, frames: bool = False, gray: bool = False):
+    def download(self, frames: bool = False, gray: bool = False, bits: bool = False):
+        """bits=True (2-level SLMs) adds "levels1": the frames as bit-planes
+        [jobs][N][npix/8], bit (i & 7) of byte i >> 3 (np.packbits little)."""
         N = self._nf
         jobs, ny, nx = self.jobs, self.ny, self.nx
         wide = self.cfg.slm.levels > 256
@@ -666,6 +668,9 @@ class OsprPlan:
             io.frames = _p(out["frames"])
         io.frame_mse, io.cumulative_mse = _p(out["frame_mse"]), _p(out["cumulative_mse"])
         io.mean_intensity, io.final_error = _p(out["mean_intensity"]), _p(out["final_error"])
+        if bits:
+            out["levels1"] = np.empty((jobs, N, ny * nx // 8), np.uint8)
+            io.levels1 = _p(out["levels1"])
         if gray:  # device-encoded hologram.png per frame / replay.png pixels
             out["frames_gray8"] = np.empty((jobs, N, ny, nx), np.uint8)
             out["replay_gray8"] = np.empty((jobs, ny, nx), np.uint8)

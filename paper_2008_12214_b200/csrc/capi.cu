@@ -499,6 +499,18 @@ __global__ void k_levels_gray8(const uint8_t* lv8, const uint16_t* lv16, size_t 
         out[i] = table[lv8 ? lv8[i] : lv16[i]];
 }
 
+// 2-level SLMs: levels as bit-planes (bit i & 7 of byte i >> 3), 8 pixels per byte.
+__global__ void k_pack_levels1(const uint8_t* lv8, size_t nbytes, uint8_t* out) {
+    for (size_t j = blockIdx.x * (size_t)blockDim.x + threadIdx.x; j < nbytes; j += (size_t)gridDim.x * blockDim.x) {
+        const uint2 w = *reinterpret_cast<const uint2*>(lv8 + 8 * j);  // 8 levels, each 0 or 1
+        const uint64_t v = ((uint64_t)w.y << 32) | w.x;
+        uint8_t b = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) b |= (uint8_t)(((v >> (8 * k)) & 1) << k);
+        out[j] = b;
+    }
+}
+
 // |z| in double exactly as std::abs(std::complex<double>) (io.cpp:193-195)
 // computes it on the reference's host: glibc's hypot, i.e. Borges' corrected
 // algorithm ("An Improved Algorithm for hypot(a,b)", arXiv:1904.09481;
@@ -602,6 +614,17 @@ static dim3 ew_grid(size_t n) {
     if (b > 148 * 16) b = 148 * 16;
     if (b < 1) b = 1;
     return dim3((unsigned)b);
+}
+
+static void levels1_dev(const uint8_t* lv8, size_t n, int levels, uint8_t* host_out, cudaStream_t st) {
+    if (levels != 2) invalid("levels1: bit-planes need a 2-level SLM");
+    if (n % 8) invalid("levels1: pixel count must be a multiple of 8");
+    DBuf<uint8_t> b;
+    b.alloc(n / 8);
+    k_pack_levels1<<<ew_grid(n / 8), 256, 0, st>>>(lv8, n / 8, b.p);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(host_out, b.p, n / 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
 }
 
 template <class TI, class TO>
@@ -1314,6 +1337,7 @@ int hgc_ifta_plan_download(hgc_ifta_plan* p, hgc_ifta_io* io) {
             if (io->replay_peak)
                 CK(cudaMemcpy(io->replay_peak, pk.p, sizeof(double) * p->batch, cudaMemcpyDeviceToHost));
         }
+        if (io->levels1) levels1_dev(p->lv8.p, tot, p->q.p.levels, io->levels1, p->stream);
         if (!p->wide_levels && io->levels8 && !io->levels16 && !io->hologram) {
             CK(cudaMemcpy(io->levels8, p->lv8.p, tot, cudaMemcpyDeviceToHost));  // straight into the caller's buffer
         } else if (io->levels8 || io->levels16 || io->hologram) {
@@ -1853,6 +1877,7 @@ int hgc_ospr_plan_download(hgc_ospr_plan* p, hgc_ospr_io* io) {
             if (io->replay_gray8) CK(cudaMemcpy(io->replay_gray8, g.p, tot, cudaMemcpyDeviceToHost));
             if (io->replay_peak) CK(cudaMemcpy(io->replay_peak, pk.p, sizeof(double) * p->jobs, cudaMemcpyDeviceToHost));
         }
+        if (io->levels1) levels1_dev(p->lv8.p, lvtot, p->q.p.levels, io->levels1, p->stream);
         if (!p->wide_levels && io->levels8 && !io->levels16 && !io->frames) {
             CK(cudaMemcpy(io->levels8, p->lv8.p, lvtot, cudaMemcpyDeviceToHost));
         } else if (io->levels8 || io->levels16 || io->frames) {

@@ -74,3 +74,21 @@ def test_ospr_plan_gray_outputs():
         want, peak = _replay_px(replay)
         assert out["replay_peak"][j] == peak
         assert np.array_equal(out["replay_gray8"][j], want)
+
+
+def test_ospr_binary_bitplanes():
+    """2-level SLM frames as bit-planes (hgc_ospr_io.levels1): np.packbits(little) of the levels."""
+    amp = hg.patterns.bench_target(64)
+    cfg = hg.OsprConfig(subframes=3, slm=hg.SlmSpec.binary_phase(), target=hg.TargetSpec(amp), seed=2)
+    p = hg.OsprPlan(cfg, 64, 64, 2)
+    p.upload(amp, seeds=[2, 3])
+    p.execute()
+    out = p.download(bits=True)
+    want = np.packbits(out["levels"].reshape(2, 3, -1), axis=-1, bitorder="little")
+    assert np.array_equal(out["levels1"], want)
+    p16 = hg.OsprPlan(hg.OsprConfig(subframes=1, slm=hg.SlmSpec.full_circle_phase(4), target=hg.TargetSpec(amp)),
+                      64, 64, 1)
+    p16.upload(amp)
+    p16.execute()
+    with pytest.raises(ValueError, match="2-level"):
+        p16.download(bits=True)

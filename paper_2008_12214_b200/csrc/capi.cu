@@ -616,11 +616,13 @@ static dim3 ew_grid(size_t n) {
     return dim3((unsigned)b);
 }
 
-static void levels1_dev(const uint8_t* lv8, size_t n, int levels, uint8_t* host_out, cudaStream_t st) {
+// (b: the plan's persistent buffer — a per-call cudaFree would synchronise the
+// whole device and stall other plans running concurrently)
+static void levels1_dev(const uint8_t* lv8, size_t n, int levels, uint8_t* host_out, DBuf<uint8_t>& b,
+                        cudaStream_t st) {
     if (levels != 2) invalid("levels1: bit-planes need a 2-level SLM");
     if (n % 8) invalid("levels1: pixel count must be a multiple of 8");
-    DBuf<uint8_t> b;
-    b.alloc(n / 8);
+    b.ensure(n / 8);
     k_pack_levels1<<<ew_grid(n / 8), 256, 0, st>>>(lv8, n / 8, b.p);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(host_out, b.p, n / 8, cudaMemcpyDeviceToHost, st));
@@ -846,7 +848,7 @@ struct hgc_ifta_plan {
     DBuf<int> vflags;             // deferred TargetSpec validation flags
     DBuf<float> target_f, weights, init_weights;
     DBuf<double> amp_d, phase_d, partials, trace;
-    DBuf<uint8_t> roi, roi_rm, lv8;
+    DBuf<uint8_t> roi, roi_rm, lv8, lv1;
     DBuf<uint16_t> lv16;
     DBuf<MtState> mt;
     DBuf<uint64_t> seeds;
@@ -1337,7 +1339,7 @@ int hgc_ifta_plan_download(hgc_ifta_plan* p, hgc_ifta_io* io) {
             if (io->replay_peak)
                 CK(cudaMemcpy(io->replay_peak, pk.p, sizeof(double) * p->batch, cudaMemcpyDeviceToHost));
         }
-        if (io->levels1) levels1_dev(p->lv8.p, tot, p->q.p.levels, io->levels1, p->stream);
+        if (io->levels1) levels1_dev(p->lv8.p, tot, p->q.p.levels, io->levels1, p->lv1, p->stream);
         if (!p->wide_levels && io->levels8 && !io->levels16 && !io->hologram) {
             CK(cudaMemcpy(io->levels8, p->lv8.p, tot, cudaMemcpyDeviceToHost));  // straight into the caller's buffer
         } else if (io->levels8 || io->levels16 || io->hologram) {
@@ -1440,7 +1442,7 @@ struct hgc_ospr_plan {
     DBuf<float2> field, field2;  // double-buffered seeded field (plain OSPR)
     DBuf<float> target_f, S;
     DBuf<double> amp_d, partials, traces;
-    DBuf<uint8_t> roi, lv8;
+    DBuf<uint8_t> roi, lv8, lv1;
     DBuf<uint16_t> lv16;
     DBuf<MtState> mt;
     DBuf<uint64_t> seeds;
@@ -1877,7 +1879,7 @@ int hgc_ospr_plan_download(hgc_ospr_plan* p, hgc_ospr_io* io) {
             if (io->replay_gray8) CK(cudaMemcpy(io->replay_gray8, g.p, tot, cudaMemcpyDeviceToHost));
             if (io->replay_peak) CK(cudaMemcpy(io->replay_peak, pk.p, sizeof(double) * p->jobs, cudaMemcpyDeviceToHost));
         }
-        if (io->levels1) levels1_dev(p->lv8.p, lvtot, p->q.p.levels, io->levels1, p->stream);
+        if (io->levels1) levels1_dev(p->lv8.p, lvtot, p->q.p.levels, io->levels1, p->lv1, p->stream);
         if (!p->wide_levels && io->levels8 && !io->levels16 && !io->frames) {
             CK(cudaMemcpy(io->levels8, p->lv8.p, lvtot, cudaMemcpyDeviceToHost));
         } else if (io->levels8 || io->levels16 || io->frames) {

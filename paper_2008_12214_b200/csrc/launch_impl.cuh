@@ -24,10 +24,10 @@ inline void set_smem(K kernel, int bytes) {
 }
 
 // ------------------------------------------------------------------- rows
-template <int NX, int MODE, int QK, int LAY, int FQ>
+template <int NX, int MODE, int QK, int LAY, int FQ, int LV = 2>
 inline void row_launch(const RowArgs& a, int batch, cudaStream_t st, bool prepare) {
     using Cfg = RowCfg<NX, LAY>;
-    auto kern = k_row<NX, MODE, QK, LAY, FQ>;
+    auto kern = k_row<NX, MODE, QK, LAY, FQ, LV>;
     if (prepare) {
         set_smem(kern, Cfg::SMEM);
         return;
@@ -54,11 +54,11 @@ inline int quant_kind(const QuantParams& q) {
     return QK_GENERIC;
 }
 
-template <int MODE, int QK, int LAY, int FQ>
+template <int MODE, int QK, int LAY, int FQ, int LV = 2>
 inline void row_dispatch_q(int nx, const RowArgs& a, int batch, cudaStream_t st, bool prepare) {
     switch (nx) {
 #define HG_ROW(N) \
-    case N: row_launch<N, MODE, QK, LAY, FQ>(a, batch, st, prepare); break;
+    case N: row_launch<N, MODE, QK, LAY, FQ, LV>(a, batch, st, prepare); break;
         HG_ROW(2) HG_ROW(4) HG_ROW(8) HG_ROW(16) HG_ROW(32) HG_ROW(64) HG_ROW(128) HG_ROW(256)
         HG_ROW(512) HG_ROW(1024) HG_ROW(2048) HG_ROW(4096)
 #undef HG_ROW

@@ -99,7 +99,10 @@ struct RowCfg {
 #endif
 // FQ: Fresnel Q in the fused pass — 0 absent, 1 present (compile time, the
 // specialised quantisers), 2 decided at run time from a.fresnel_q.
-template <int NX, int MODE, int QK, int LAY, int FQ>
+// LV: level indices out — 0 never (compile time: the K-1 non-final iterations
+// carry no store code or index registers), 1 when a.levels8/16 is set, 2
+// decided at run time.
+template <int NX, int MODE, int QK, int LAY, int FQ, int LV = 2>
 __global__ void __launch_bounds__(RowCfg<NX, LAY>::THREADS, RowCfg<NX, LAY>::MIN_BLOCKS) k_row(RowArgs a) {
     using Cfg = RowCfg<NX, LAY>;
     constexpr int E = Cfg::E, T = Cfg::T;
@@ -193,8 +196,8 @@ __global__ void __launch_bounds__(RowCfg<NX, LAY>::THREADS, RowCfg<NX, LAY>::MIN
         const float norm = a.norm;
         const float2* __restrict__ fq = FQ == 0 ? nullptr : a.fresnel_q;
         const bool hasq = FQ == 1 || (FQ == 2 && fq != nullptr);
-        uint8_t* __restrict__ lv8 = a.levels8 ? a.levels8 + a.lv_bstride * b : nullptr;
-        uint16_t* __restrict__ lv16 = a.levels16 ? a.levels16 + a.lv_bstride * b : nullptr;
+        uint8_t* __restrict__ lv8 = (LV != 0 && a.levels8) ? a.levels8 + a.lv_bstride * b : nullptr;
+        uint16_t* __restrict__ lv16 = (LV != 0 && a.levels16) ? a.levels16 + a.lv_bstride * b : nullptr;
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             const int i = rowbase + t + e * T;  // row-major pixel index (levels, Q, illumination)
@@ -204,8 +207,10 @@ __global__ void __launch_bounds__(RowCfg<NX, LAY>::THREADS, RowCfg<NX, LAY>::MIN
             if constexpr (QK == QK_BINARY) f = k ? a.q.s1 : a.q.s0;
             else if constexpr (QK == QK_FULL) f = __ldg(&a.q.states[k]);  // phase mode, no illumination
             else f = quant_state(a.q, k, i);
-            if (lv8 && valid) lv8[i] = (uint8_t)k;
-            if (lv16 && valid) lv16[i] = (uint16_t)k;
+            if constexpr (LV != 0) {
+                if (lv8 && valid) lv8[i] = (uint8_t)k;
+                if (lv16 && valid) lv16[i] = (uint16_t)k;
+            }
             if (hasq) f = cmul_rn(f, __ldg(&fq[i]));              // propagation.hpp:85
             v[e] = f;
         }

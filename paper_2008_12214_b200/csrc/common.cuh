@@ -28,61 +28,36 @@ __device__ __forceinline__ float2 cmul_conj_rn(float2 a, float2 b) {
     return make_float2(__fadd_rn(ac, bd), __fsub_rn(bc, ad));
 }
 
-// Complex arithmetic of the transforms (FMA allowed).  HG_PACKED_F32=1 runs it
-// on the packed FP32 instructions: sm_100a executes the f32x2 PTX types as
-// FADD2 / FMUL2 / FFMA2, one instruction for both lanes, with lane broadcast /
-// swap as free operand modifiers (nvcc does not pack scalar code by itself).
-// That cut the static instruction count of the fused passes by 18-24% but
-// measured slower overall at 4096^2 (row -1.7%, column +7%: the pairing moves
-// and per-lane negations cost more than the issue slots saved), so the scalar
-// form is the default.  Per lane both forms compute the same roundings:
+// Complex arithmetic of the transforms on packed FP32: a complex64 value is
+// one register pair and sm_100a executes the f32x2 operations as FADD2 /
+// FMUL2 / FFMA2, one instruction for both components, with lane broadcast,
+// lane swap and negation as free operand modifiers and constant pairs in
+// uniform registers.  Per component the roundings are exactly those of the
+// scalar forms:
 //   cadd / csub: a.x +- b.x, a.y +- b.y;
-//   cmul: fmaf(a.x, b.x, -(a.y*b.y)), fmaf(a.x, b.y, a.y*b.x) — the inner
-//   products are formed as (a.y, a.y) * (-b.y, b.x), negation being exact.
-#ifndef HG_PACKED_F32
-#define HG_PACKED_F32 0
+//   cmul: fmaf(a.x, b.x, -(a.y*b.y)), fmaf(a.x, b.y, a.y*b.x), formed as
+//         (a.x, a.x) * b + (a.y, a.y) * (-b.y, b.x)  (negation is exact).
+__device__ __forceinline__ float2 f2swap(float2 a) { return make_float2(a.y, a.x); }
+__device__ __forceinline__ float2 f2bx(float2 a) { return make_float2(a.x, a.x); }
+__device__ __forceinline__ float2 f2by(float2 a) { return make_float2(a.y, a.y); }
+#ifndef HG_FFT_SCALAR  // per translation unit: 1 = the same arithmetic as scalar FADD/FMUL/FFMA
+#define HG_FFT_SCALAR 0
 #endif
-#ifndef HG_PACKED_CMUL
-#define HG_PACKED_CMUL HG_PACKED_F32
-#endif
-__device__ __forceinline__ unsigned long long f2_pack(float2 a) {
-    unsigned long long r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
-    return r;
+#if HG_FFT_SCALAR
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cmul_r(float2 a, float2 w, float2 wr) {
+    return make_float2(fmaf(a.x, w.x, a.y * wr.x), fmaf(a.x, w.y, a.y * wr.y));
 }
-__device__ __forceinline__ float2 f2_unpack(unsigned long long r) {
-    float2 a;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
-    return a;
-}
-__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-#if HG_PACKED_CMUL
-    unsigned long long s, r;
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(s) : "l"(f2_pack(make_float2(a.y, a.y))), "l"(f2_pack(make_float2(-b.y, b.x))));
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2_pack(make_float2(a.x, a.x))), "l"(f2_pack(b)), "l"(s));
-    return f2_unpack(r);
 #else
-    return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
-#endif
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+// a * w given w and its rotation wr = i*w = (-w.y, w.x)
+__device__ __forceinline__ float2 cmul_r(float2 a, float2 w, float2 wr) {
+    return __ffma2_rn(f2bx(a), w, __fmul2_rn(f2by(a), wr));
 }
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) {
-#if HG_PACKED_F32
-    unsigned long long r;
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_pack(a)), "l"(f2_pack(b)));
-    return f2_unpack(r);
-#else
-    return make_float2(a.x + b.x, a.y + b.y);
 #endif
-}
-__device__ __forceinline__ float2 csub(float2 a, float2 b) {
-#if HG_PACKED_F32
-    unsigned long long r;
-    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_pack(a)), "l"(f2_pack(b)));
-    return f2_unpack(r);
-#else
-    return make_float2(a.x - b.x, a.y - b.y);
-#endif
-}
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) { return cmul_r(a, b, make_float2(-b.y, b.x)); }
 // double2 versions for the f64 transform (k_fft64.cu)
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
     return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
@@ -90,7 +65,11 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ float2 cscale(float2 a, float s) {
+#if HG_FFT_SCALAR
     return make_float2(__fmul_rn(a.x, s), __fmul_rn(a.y, s));
+#else
+    return __fmul2_rn(a, make_float2(s, s));
+#endif
 }
 
 // Opaque copies: the compiler must recompute anything derived from the

@@ -12,7 +12,11 @@
 //
 // Twiddles come from a per-length table tw[N + m] = exp(-2*pi*i*m/N)
 // (N = 1..4096, 8192 entries), computed in double once per device and read
-// through the read-only path.  SIGN = -1 forward, +1 inverse (unnormalised, like FFTW;
+// through the read-only path.  The float2 arithmetic runs on packed FP32
+// (common.cuh): with w and i*w at hand (one exact FMUL2 rotation) every
+// twiddle product, forward or conjugated (inverse), is one FMUL2 + one FFMA2
+// with only operand modifiers, bit-identical per component to the scalar
+// fmaf forms.  SIGN = -1 forward, +1 inverse (unnormalised, like FFTW;
 // the unitary 1/sqrt(nx*ny) scale is applied by the fused passes exactly
 // where fftw_backend.cpp:121-123 applies it).
 #pragma once
@@ -29,19 +33,48 @@ struct CT;
 template <>
 struct CT<float2> {
     using S = float;
+    using TW = float2;
     static __device__ __forceinline__ float2 make(float x, float y) { return make_float2(x, y); }
 };
 template <>
 struct CT<double2> {
     using S = double;
+    using TW = double2;
     static __device__ __forceinline__ double2 make(double x, double y) { return make_double2(x, y); }
 };
+
+template <class C2>
+__device__ __forceinline__ C2 cneg(C2 a) {
+    return CT<C2>::make(-a.x, -a.y);
+}
 
 // ---------------------------------------------------------------- radix-R
 template <int SIGN, class C2>
 __device__ __forceinline__ C2 mul_si(C2 a) {  // a * (SIGN * i)
     return SIGN < 0 ? CT<C2>::make(a.y, -a.x) : CT<C2>::make(-a.y, a.x);
 }
+
+// Packed float2 forms (one instruction each; per component exact):
+// a * (SIGN*i) = swap(a) * (-SIGN, SIGN), and t + SIGN*i*d = swap(d) * (-SIGN, SIGN) + t.
+#if HG_FFT_SCALAR
+template <int SIGN>
+__device__ __forceinline__ float2 mul_si(float2 a) {
+    return SIGN < 0 ? make_float2(a.y, -a.x) : make_float2(-a.y, a.x);
+}
+template <int SIGN>
+__device__ __forceinline__ float2 add_si(float2 t, float2 d) {
+    return cadd(t, mul_si<SIGN>(d));
+}
+#else
+template <int SIGN>
+__device__ __forceinline__ float2 mul_si(float2 a) {
+    return __fmul2_rn(f2swap(a), make_float2(-(float)SIGN, (float)SIGN));
+}
+template <int SIGN>
+__device__ __forceinline__ float2 add_si(float2 t, float2 d) {
+    return __ffma2_rn(f2swap(d), make_float2(-(float)SIGN, (float)SIGN), t);
+}
+#endif
 
 // W16^m = exp(SIGN*2*pi*i*m/16), applied to a (compile-time m).
 template <int SIGN, int M, class C2>
@@ -52,7 +85,7 @@ __device__ __forceinline__ C2 tw16(C2 a) {
                 h = (S)0.707106781186547524400844362104849039L;
     if constexpr (m == 0) return a;
     else if constexpr (m == 4) return mul_si<SIGN>(a);
-    else if constexpr (m == 8) return CT<C2>::make(-a.x, -a.y);
+    else if constexpr (m == 8) return cneg(a);
     else if constexpr (m == 12) return mul_si<-SIGN>(a);
     else {
         // cos/sin of 2*pi*m/16 for the remaining m
@@ -77,6 +110,16 @@ __device__ __forceinline__ void dft4(C2& v0, C2& v1, C2& v2, C2& v3) {
     v2 = csub(t0, t2);
     v1 = cadd(t1, t3);
     v3 = csub(t1, t3);
+}
+
+template <int SIGN>
+__device__ __forceinline__ void dft4(float2& v0, float2& v1, float2& v2, float2& v3) {
+    const float2 t0 = cadd(v0, v2), t1 = csub(v0, v2);
+    const float2 t2 = cadd(v1, v3), d = csub(v1, v3);
+    v0 = cadd(t0, t2);
+    v2 = csub(t0, t2);
+    v1 = add_si<SIGN>(t1, d);   // t1 + (SIGN i) d
+    v3 = add_si<-SIGN>(t1, d);  // t1 - (SIGN i) d
 }
 
 // In-place DFT of R values, natural order in and out:
@@ -142,9 +185,9 @@ struct LineCfg {
 };
 
 // Twiddle exp(SIGN*2*pi*i*m/N) from the forward table.
-template <int N, int SIGN, class C2>
-__device__ __forceinline__ C2 twiddle(const C2* __restrict__ tw, int m) {
-    C2 w = __ldg(&tw[N + m]);
+template <int N, int SIGN, class TW>
+__device__ __forceinline__ TW twiddle(const TW* __restrict__ tw, int m) {
+    TW w = __ldg(&tw[N + m]);
     if constexpr (SIGN > 0) w.y = -w.y;
     return w;
 }
@@ -154,13 +197,13 @@ __device__ __forceinline__ C2 twiddle(const C2* __restrict__ tw, int m) {
 // error <= ~2 ulp): 3 loads instead of 15 keeps the pass within the register
 // budget of a 1024-thread CTA (loading all 15 measured 10.1 vs 6.9 ms for
 // the 4096^2 row pass: the extra live values spill).
-template <int N, int SIGN, int R, class C2>
-__device__ __forceinline__ void apply_twiddles(C2* x, const C2* __restrict__ tw, int m) {
+template <int N, int SIGN, int R, class C2, class TW>
+__device__ __forceinline__ void apply_twiddles(C2* x, const TW* __restrict__ tw, int m) {
     if constexpr (R == 16) {
-        const C2 w1 = twiddle<N, SIGN>(tw, m);
-        const C2 w4 = twiddle<N, SIGN>(tw, 4 * m);
-        const C2 w8 = twiddle<N, SIGN>(tw, 8 * m);
-        const C2 w2 = cmul(w1, w1), w3 = cmul(w2, w1), w12 = cmul(w8, w4);
+        const TW w1 = twiddle<N, SIGN>(tw, m);
+        const TW w4 = twiddle<N, SIGN>(tw, 4 * m);
+        const TW w8 = twiddle<N, SIGN>(tw, 8 * m);
+        const TW w2 = cmul(w1, w1), w3 = cmul(w2, w1), w12 = cmul(w8, w4);
         x[1] = cmul(x[1], w1);
         x[2] = cmul(x[2], w2);
         x[3] = cmul(x[3], w3);
@@ -177,9 +220,9 @@ __device__ __forceinline__ void apply_twiddles(C2* x, const C2* __restrict__ tw,
         x[14] = cmul(x[14], cmul(w12, w2));
         x[15] = cmul(x[15], cmul(w12, w3));
     } else if constexpr (R == 8) {
-        const C2 w1 = twiddle<N, SIGN>(tw, m);
-        const C2 w2 = twiddle<N, SIGN>(tw, 2 * m);
-        const C2 w4 = twiddle<N, SIGN>(tw, 4 * m);
+        const TW w1 = twiddle<N, SIGN>(tw, m);
+        const TW w2 = twiddle<N, SIGN>(tw, 2 * m);
+        const TW w4 = twiddle<N, SIGN>(tw, 4 * m);
         x[1] = cmul(x[1], w1);
         x[2] = cmul(x[2], w2);
         x[3] = cmul(x[3], cmul(w1, w2));
@@ -193,6 +236,83 @@ __device__ __forceinline__ void apply_twiddles(C2* x, const C2* __restrict__ tw,
     }
 }
 
+// float2 lines: twiddles as (w, i*w) pairs in the forward direction; the
+// inverse applies conj(w) through lane swaps: a * conj(w) = (a.x, a.x) * swap(i*w)
+// + (a.y, a.y) * swap(w).
+struct Tw2 {
+    float2 w, r;
+};
+__device__ __forceinline__ float2 f2rot(float2 w) {  // i*w = (-w.y, w.x), exact
+#if HG_FFT_SCALAR
+    return make_float2(-w.y, w.x);
+#else
+    return __fmul2_rn(f2swap(w), make_float2(-1.f, 1.f));
+#endif
+}
+template <int N>
+__device__ __forceinline__ Tw2 tw_load(const float2* __restrict__ tw, int m) {
+    const float2 w = __ldg(&tw[N + m]);
+    return Tw2{w, f2rot(w)};
+}
+__device__ __forceinline__ Tw2 tw_mul(Tw2 a, Tw2 b) {
+    const float2 p = cmul_r(a.w, b.w, b.r);
+    return Tw2{p, f2rot(p)};
+}
+template <int SIGN>
+__device__ __forceinline__ float2 tw_apply(float2 a, Tw2 w) {
+    if constexpr (SIGN < 0) return cmul_r(a, w.w, w.r);
+    else return cmul_r(a, f2swap(w.r), f2swap(w.w));  // conj(w) and i*conj(w)
+}
+template <int N, int SIGN, int R>
+__device__ __forceinline__ void apply_twiddles(float2* x, const float2* __restrict__ tw, int m) {
+    if constexpr (R == 16) {
+        const Tw2 w1 = tw_load<N>(tw, m), w4 = tw_load<N>(tw, 4 * m), w8 = tw_load<N>(tw, 8 * m);
+        const Tw2 w2 = tw_mul(w1, w1), w3 = tw_mul(w2, w1), w12 = tw_mul(w8, w4);
+        x[1] = tw_apply<SIGN>(x[1], w1);
+        x[2] = tw_apply<SIGN>(x[2], w2);
+        x[3] = tw_apply<SIGN>(x[3], w3);
+        x[4] = tw_apply<SIGN>(x[4], w4);
+        x[8] = tw_apply<SIGN>(x[8], w8);
+        x[12] = tw_apply<SIGN>(x[12], w12);
+        x[5] = tw_apply<SIGN>(x[5], tw_mul(w4, w1));
+        x[6] = tw_apply<SIGN>(x[6], tw_mul(w4, w2));
+        x[7] = tw_apply<SIGN>(x[7], tw_mul(w4, w3));
+        x[9] = tw_apply<SIGN>(x[9], tw_mul(w8, w1));
+        x[10] = tw_apply<SIGN>(x[10], tw_mul(w8, w2));
+        x[11] = tw_apply<SIGN>(x[11], tw_mul(w8, w3));
+        x[13] = tw_apply<SIGN>(x[13], tw_mul(w12, w1));
+        x[14] = tw_apply<SIGN>(x[14], tw_mul(w12, w2));
+        x[15] = tw_apply<SIGN>(x[15], tw_mul(w12, w3));
+    } else if constexpr (R == 8) {
+        const Tw2 w1 = tw_load<N>(tw, m), w2 = tw_load<N>(tw, 2 * m), w4 = tw_load<N>(tw, 4 * m);
+        const Tw2 w3 = tw_mul(w1, w2);
+        x[1] = tw_apply<SIGN>(x[1], w1);
+        x[2] = tw_apply<SIGN>(x[2], w2);
+        x[3] = tw_apply<SIGN>(x[3], w3);
+        x[4] = tw_apply<SIGN>(x[4], w4);
+        x[5] = tw_apply<SIGN>(x[5], tw_mul(w4, w1));
+        x[6] = tw_apply<SIGN>(x[6], tw_mul(w4, w2));
+        x[7] = tw_apply<SIGN>(x[7], tw_mul(w4, w3));
+    } else {
+#pragma unroll
+        for (int r = 1; r < R; ++r) x[r] = tw_apply<SIGN>(x[r], tw_load<N>(tw, r * m));
+    }
+}
+
+// Barrier between the scatter and the gather of an exchange (the whole CTA).
+struct CtaSync {
+    __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+
+// Exchange-buffer slot access (one element per slot).
+template <class C2, class I>
+__device__ __forceinline__ void smst(C2* sm, const I&, int s, C2 v) {
+    sm[s] = v;
+}
+template <class C2, class I>
+__device__ __forceinline__ C2 smld(const C2* sm, const I&, int s) {
+    return sm[s];
+}
 // One Stockham pass (span NS) and, recursively, the rest.
 //   butterfly j = t + b*T (b < E/R) reads elements b + r*(E/R);
 //   twiddle by W_{NS*R}^{r*(j mod NS)}; DFT_R;
@@ -200,9 +320,9 @@ __device__ __forceinline__ void apply_twiddles(C2* x, const C2* __restrict__ tw,
 // SmemIdx maps a line position to a shared-memory slot for this thread's line.
 template <int N, int SIGN, int NS, int EM = 16>
 struct StockhamPass {
-    template <class C2, class SmemIdx>
+    template <class C2, class SmemIdx, class Sync>
     __device__ __forceinline__ static void run(C2 (&v)[LineCfg<N, EM>::E], int t, C2* sm, const SmemIdx& idx,
-                                               const C2* __restrict__ tw) {
+                                               const typename CT<C2>::TW* __restrict__ tw, const Sync& sync) {
         constexpr int E = LineCfg<N, EM>::E, T = LineCfg<N, EM>::T;
         constexpr int R = (N / NS >= E) ? E : N / NS;
         constexpr int B = E / R;
@@ -227,36 +347,37 @@ struct StockhamPass {
                     const int s0 = idx(base);
                     constexpr int rs = (NS == 1) ? 1 : NS + NS / 16;
 #pragma unroll
-                    for (int r = 0; r < R; ++r) sm[s0 + r * rs * SmemIdx::kLineStride] = x[r];
+                    for (int r = 0; r < R; ++r) smst(sm, idx, s0 + r * rs * SmemIdx::kLineStride, x[r]);
                 } else {
 #pragma unroll
-                    for (int r = 0; r < R; ++r) sm[idx(base + r * NS)] = x[r];
+                    for (int r = 0; r < R; ++r) smst(sm, idx, idx(base + r * NS), x[r]);
                 }
             }
         }
         if constexpr (!last) {
-            __syncthreads();
+            sync();
             if constexpr (T % 16 == 0) {
                 const int s0 = idx(t);
                 constexpr int es = T + T / 16;
 #pragma unroll
-                for (int e = 0; e < E; ++e) v[e] = sm[s0 + e * es * SmemIdx::kLineStride];
+                for (int e = 0; e < E; ++e) v[e] = smld(sm, idx, s0 + e * es * SmemIdx::kLineStride);
             } else {
 #pragma unroll
-                for (int e = 0; e < E; ++e) v[e] = sm[idx(t + e * T)];
+                for (int e = 0; e < E; ++e) v[e] = smld(sm, idx, idx(t + e * T));
             }
-            __syncthreads();
-            StockhamPass<N, SIGN, NS * R, EM>::run(v, t, sm, idx, tw);
+            sync();
+            StockhamPass<N, SIGN, NS * R, EM>::run(v, t, sm, idx, tw, sync);
         }
     }
 };
 
 // Full unnormalised 1-D transform of one line held in strided ownership.
-// Every thread of the CTA must call it (it contains __syncthreads when N > E).
-template <int N, int SIGN, int EM = 16, class C2, class SmemIdx>
+// Every thread of the CTA (or of the Sync group) must call it (it contains
+// barriers when N > E).
+template <int N, int SIGN, int EM = 16, class C2, class SmemIdx, class Sync = CtaSync>
 __device__ __forceinline__ void fft_line(C2 (&v)[LineCfg<N, EM>::E], int t, C2* sm, const SmemIdx& idx,
-                                         const C2* __restrict__ tw) {
-    StockhamPass<N, SIGN, 1, EM>::run(v, t, sm, idx, tw);
+                                         const typename CT<C2>::TW* __restrict__ tw, const Sync& sync = Sync{}) {
+    StockhamPass<N, SIGN, 1, EM>::run(v, t, sm, idx, tw, sync);
 }
 
 // Padded slot for position q of a line: one pad slot every 16 keeps the

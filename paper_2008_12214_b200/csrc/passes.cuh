@@ -20,6 +20,9 @@
 #include "fft.cuh"
 #include "quant.cuh"
 
+#ifndef HG_NULL_COMPUTE
+#define HG_NULL_COMPUTE 0
+#endif
 #ifndef HG_ROWQ_MINB  // resident CTAs / SM asked of the quad-layout row pass (register cap)
 #define HG_ROWQ_MINB 2
 #endif
@@ -93,6 +96,40 @@ struct RowCfg {
     static constexpr int SMEM = (NX > E) ? RPC * RowStride<NX>::value * (int)sizeof(float2) : 0;
     static constexpr int MIN_BLOCKS = LAY == LAY_QUAD ? (THREADS >= 512 ? HG_ROWQ_MINB : 1) : (THREADS >= 256 ? 3 : 1);
 };
+
+// The aperture-plane work of one row (thread t's elements x = t + e*T of row y
+// of target b, in registers): IFFT (completes P^-1), *norm, *conj(Q),
+// quantise (+levels), *Q, FFT (starts P).
+template <int NX, int QK, int FQ, int LV, class Sync = CtaSync>
+__device__ __forceinline__ void row_fused_body(float2 (&v)[LineCfg<NX>::E], int t, int y, int b, bool valid,
+                                               float2* smem, const RowSmemIdx& idx, const RowArgs& a,
+                                               const Sync& sync = Sync{}) {
+    constexpr int E = LineCfg<NX>::E, T = LineCfg<NX>::T;
+    fft_line<NX, +1>(v, t, smem, idx, a.tw, sync);  // completes the 2-D inverse (propagation.hpp:89-95)
+    const int rowbase = y * NX;
+    const float norm = a.norm;
+    const float2* __restrict__ fq = FQ == 0 ? nullptr : a.fresnel_q;
+    const bool hasq = FQ == 1 || (FQ == 2 && fq != nullptr);
+    uint8_t* __restrict__ lv8 = (LV != 0 && a.levels8) ? a.levels8 + a.lv_bstride * b : nullptr;
+    uint16_t* __restrict__ lv16 = (LV != 0 && a.levels16) ? a.levels16 + a.lv_bstride * b : nullptr;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int i = rowbase + t + e * T;  // row-major pixel index (levels, Q, illumination)
+        float2 f = cscale(v[e], norm);                        // fftw_backend.cpp:121-123
+        if (hasq) f = cmul_conj_rn(f, __ldg(&fq[i]));         // propagation.hpp:93
+        const int k = quant_decide_kind<QK>(a.q, f.x, f.y, i);  // quantise.hpp:211-215
+        if constexpr (QK == QK_BINARY) f = k ? a.q.s1 : a.q.s0;
+        else if constexpr (QK == QK_FULL) f = __ldg(&a.q.states[k]);  // phase mode, no illumination
+        else f = quant_state(a.q, k, i);
+        if constexpr (LV != 0) {
+            if (lv8 && valid) lv8[i] = (uint8_t)k;
+            if (lv16 && valid) lv16[i] = (uint16_t)k;
+        }
+        if (hasq) f = cmul_rn(f, __ldg(&fq[i]));              // propagation.hpp:85
+        v[e] = f;
+    }
+    fft_line<NX, -1>(v, t, smem, idx, a.tw, sync);  // starts the forward transform
+}
 
 #ifndef HG_ROW_BULK
 #define HG_ROW_BULK 1
@@ -191,30 +228,9 @@ __global__ void __launch_bounds__(RowCfg<NX, LAY>::THREADS, RowCfg<NX, LAY>::MIN
 #pragma unroll
             for (int e = 0; e < E; ++e) v[e] = cmul_conj_rn(v[e], __ldg(&a.fresnel_q[rowbase + t + e * T]));
     } else {
-        fft_line<NX, +1>(v, t, smem, idx, a.tw);  // completes the 2-D inverse (propagation.hpp:89-95)
-        const int rowbase = y * NX;
-        const float norm = a.norm;
-        const float2* __restrict__ fq = FQ == 0 ? nullptr : a.fresnel_q;
-        const bool hasq = FQ == 1 || (FQ == 2 && fq != nullptr);
-        uint8_t* __restrict__ lv8 = (LV != 0 && a.levels8) ? a.levels8 + a.lv_bstride * b : nullptr;
-        uint16_t* __restrict__ lv16 = (LV != 0 && a.levels16) ? a.levels16 + a.lv_bstride * b : nullptr;
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-            const int i = rowbase + t + e * T;  // row-major pixel index (levels, Q, illumination)
-            float2 f = cscale(v[e], norm);                        // fftw_backend.cpp:121-123
-            if (hasq) f = cmul_conj_rn(f, __ldg(&fq[i]));         // propagation.hpp:93
-            const int k = quant_decide_kind<QK>(a.q, f.x, f.y, i);  // quantise.hpp:211-215
-            if constexpr (QK == QK_BINARY) f = k ? a.q.s1 : a.q.s0;
-            else if constexpr (QK == QK_FULL) f = __ldg(&a.q.states[k]);  // phase mode, no illumination
-            else f = quant_state(a.q, k, i);
-            if constexpr (LV != 0) {
-                if (lv8 && valid) lv8[i] = (uint8_t)k;
-                if (lv16 && valid) lv16[i] = (uint16_t)k;
-            }
-            if (hasq) f = cmul_rn(f, __ldg(&fq[i]));              // propagation.hpp:85
-            v[e] = f;
-        }
-        fft_line<NX, -1>(v, t, smem, idx, a.tw);  // starts the forward transform
+#if !HG_NULL_COMPUTE  // diagnostic build: the passes' memory traffic alone
+        row_fused_body<NX, QK, FQ, LV>(v, t, y, b, valid, smem, idx, a);
+#endif
     }
     if constexpr (kBulk) {
         const int lb = opaque(lbase());
@@ -466,7 +482,9 @@ __global__ void __launch_bounds__(LineCfg<NY, ColCfg<NY, LAY>::EM>::T * C, ColCf
         store_col(base);
         return;
     } else {
+#if !HG_NULL_COMPUTE
         fft_line<NY, -1, EM>(v, t, smem, idx, a.tw);  // completes the forward transform
+#endif
         const float norm = a.norm;
         const float* tg = a.target + a.t_bstride * b + sb;
         // target element e: from the bulk-loaded slice (same column-pair offsets) or global
@@ -588,7 +606,9 @@ __global__ void __launch_bounds__(LineCfg<NY, ColCfg<NY, LAY>::EM>::T * C, ColCf
             if (a.last) {
                 store_col(a.replay_out + a.bstride * b);
             } else {
+#if !HG_NULL_COMPUTE
                 fft_line<NY, +1, EM>(v, t, smem, idx, a.tw);  // starts the next inverse transform
+#endif
                 store_col(base);
             }
         }

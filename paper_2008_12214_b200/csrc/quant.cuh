@@ -136,32 +136,6 @@ __device__ __forceinline__ float fast_atan2f(float y, float x) {
     return copysignf(r, y);
 }
 
-// Fast decision only (QK_BINARY / QK_FULL): k, and near = the pixel must be
-// re-decided by quant_exact_kind.  quant_decide_kind == fast + exact-if-near.
-template <int QK>
-__device__ __forceinline__ int quant_fast_kind(const QuantParams& q, float vr, float vi, bool& near) {
-    static_assert(QK == QK_BINARY || QK == QK_FULL, "fast/exact split: specialised quantisers only");
-    if constexpr (QK == QK_BINARY) {
-        near = !(fabsf(vr) > 1e-5f * fmaxf(fabsf(vr), fabsf(vi)));
-        return vr < 0.f ? 1 : 0;
-    } else {
-        const float two_pi_f = 6.28318530717958648f;
-        float d = fast_atan2f(vi, vr) - q.min_arg_f;
-        d -= two_pi_f * floorf(d * (1.0f / two_pi_f));
-        const float u = d * q.inv_spac_f;
-        const float fu = floorf(u);
-        const float fr = u - fu;
-        near = !(fabsf(fr - 0.5f) >= q.margin_u);  // NaN-safe
-        const int k = (int)fu + (fr >= 0.5f ? 1 : 0);
-        return k >= q.levels ? k - q.levels : k;
-    }
-}
-template <int QK>
-__device__ __forceinline__ int quant_exact_kind(const QuantParams& q, float vr, float vi) {
-    if constexpr (QK == QK_BINARY) return quant_decide_exact(1, 2, 0, q.min_arg, q.inv_spac, q.range, 0.0, 0.0, vr, vi);
-    else return quant_decide_exact(1, q.levels, 1, q.min_arg, q.inv_spac, q.range, 0.0, 0.0, vr, vi);
-}
-
 template <int QK>
 __device__ __forceinline__ int quant_decide_kind(const QuantParams& q, float vr, float vi, size_t i) {
     if constexpr (QK == QK_BINARY) {

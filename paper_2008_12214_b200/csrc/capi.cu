@@ -130,7 +130,8 @@ static void prepare_kernels(int nx, int ny) {
     ca.layout = LAY_QUAD;
     col_gs(ny, ca, 1, nullptr, true);
     col_ospr(ny, ca, 1, nullptr, true);
-    CK(cudaFuncSetAttribute(k_seed_random_phase, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSeedSmem));
+    CK(cudaFuncSetAttribute(k_seed_random_phase<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSeedSmem));
+    CK(cudaFuncSetAttribute(k_seed_random_phase<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSeedSmem));
 }
 
 // ------------------------------------------------ TMA tensor maps
@@ -171,6 +172,19 @@ struct DevTensorMap {
 // kMinChunkDraws (the jump costs about as much as ~30k draws).
 constexpr size_t kMinChunkDraws = 32768;
 constexpr int kMaxChunks = 512;
+// The seed kernel instantiation for a launch: the fast consumer loop when the
+// output is the plans' float quad layout with a plain amplitude.
+#ifndef HG_SEED_FAST
+#define HG_SEED_FAST 1
+#endif
+static void seed_launch(int grid, const SeedArgs& sa, cudaStream_t st) {
+    if (HG_SEED_FAST && sa.quad && sa.out && !sa.out64 && !sa.S && sa.nx >= 2)
+        k_seed_random_phase<true><<<grid, kSeedThreads, kSeedSmem, st>>>(sa);
+    else
+        k_seed_random_phase<false><<<grid, kSeedThreads, kSeedSmem, st>>>(sa);
+    CK(cudaGetLastError());
+}
+
 struct SeedChunks {
     int chunks = 1;
     size_t len = 0;
@@ -233,7 +247,7 @@ struct SeedChunks {
         sa.seeds = offset0 == 0 ? seeds : nullptr;
         sa.chunks = chunks;
         sa.chunk_len = len;
-        k_seed_random_phase<<<streams * chunks, kSeedThreads, kSeedSmem, st>>>(sa);
+        seed_launch(streams * chunks, sa, st);
         return n + 1;
     }
 
@@ -264,7 +278,7 @@ struct SeedChunks {
                 ++n;
             }
             sa.seeds = first && offset0 == 0 ? seeds : nullptr;
-            k_seed_random_phase<<<streams, kSeedThreads, kSeedSmem, st>>>(sa);
+            seed_launch(streams, sa, st);
             return n + 1;
         }
         JumpArgs ja = first ? JumpArgs{seeds, nullptr, starts.p, pool.p, 1, states, chunks, 0, c_first()}
@@ -274,7 +288,7 @@ struct SeedChunks {
         sa.chunks = chunks;
         sa.chunk_len = len;
         sa.no_save = 1;
-        k_seed_random_phase<<<streams * chunks, kSeedThreads, kSeedSmem, st>>>(sa);
+        seed_launch(streams * chunks, sa, st);
         return 2;
     }
 };
@@ -2469,7 +2483,8 @@ int hgc_seed_random_phase(const double* amplitude, int nx, int ny, uint64_t engi
         const size_t npix = (size_t)nx * ny;
         require_finite_img(amplitude, npix, "seed_random_phase");
         const float2* tw = device_twiddles();
-        CK(cudaFuncSetAttribute(k_seed_random_phase, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSeedSmem));
+        CK(cudaFuncSetAttribute(k_seed_random_phase<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSeedSmem));
+    CK(cudaFuncSetAttribute(k_seed_random_phase<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSeedSmem));
         DBuf<double> a;
         DBuf<float2> f;
         DBuf<MtState> mt;

@@ -132,6 +132,17 @@ __device__ __forceinline__ void sincos_0_2pi(double x, double* sp, double* cp) {
 }
 
 constexpr int kSeedThreads = 512;
+// Fast loop: one draw per iteration at <= 64 registers (2 CTAs / SM).  The
+// OSPR seed runs beside the passes of the previous frame, so its footprint
+// matters: unroll 2 / 64 registers / 1 CTA per SM measured 43.0k vs 51.8k
+// subframes/s, unroll 4 (96 registers) no better.
+#ifndef HG_SEED_UNROLL
+#define HG_SEED_UNROLL 1
+#endif
+#ifndef HG_SEED_MINB
+#define HG_SEED_MINB 2
+#endif
+constexpr int kSeedUnroll = HG_SEED_UNROLL;
 constexpr int kTwistsPerGroup = 8;
 constexpr int kRingSlots = 2 * kTwistsPerGroup;  // two groups: one produced while one is consumed
 constexpr size_t kSeedSmem = sizeof(uint64_t) * kMtN * kRingSlots;
@@ -252,7 +263,11 @@ __global__ void __launch_bounds__(kJumpThreads) k_mt_jump(JumpArgs a) {
 }
 
 // One CTA per stream.  Warp 0 produces twists; warps 1.. consume.
-__global__ void __launch_bounds__(kSeedThreads) k_seed_random_phase(SeedArgs a) {
+// FAST: the plans' common case (float quad-layout output, plain amplitude),
+// with 32-bit index arithmetic and nothing else in the consumer loop; the
+// generic instantiation serves row-major / adaptive / double outputs.
+template <bool FAST>
+__global__ void __launch_bounds__(kSeedThreads, FAST ? HG_SEED_MINB : 1) k_seed_random_phase(SeedArgs a) {
     extern __shared__ uint64_t ring[];  // kRingSlots * 312 words
     __shared__ int s_pos;
     const int chunks = a.chunks > 1 ? a.chunks : 1;
@@ -318,6 +333,27 @@ __global__ void __launch_bounds__(kSeedThreads) k_seed_random_phase(SeedArgs a) 
                 const int left = (int)npix - d0;
                 cnt = left < kMtN * kTwistsPerGroup ? left : kMtN * kTwistsPerGroup;
             }
+            if constexpr (FAST) {
+                const int pb = (int)cbeg + d0;
+                const int qshift = lognx - 1;
+                // bases held in registers (not re-derived from the kernel
+                // parameters with 64-bit multiplies on every draw)
+                const double* __restrict__ ab = opaque(ampp);
+                float2* __restrict__ ob = opaque(out);
+#pragma unroll kSeedUnroll
+                for (int j = ctid; j < cnt; j += cthreads) {
+                    const int p = pb + j;  // row-major pixel index of this draw (rng.hpp:60)
+                    const double av = __ldg(&ab[p & pmask]);
+                    const uint64_t x = mt_temper(src[j]);
+                    const double u = (double)(x >> 11) * 0x1.0p-53;  // Rng::uniform01, rng.hpp:32
+                    const double theta = __dmul_rn(HG_TWO_PI, u);    // rng.hpp:62
+                    double sn, cs;
+                    sincos_0_2pi(theta, &sn, &cs);
+                    const int px = p & nxm, py = p >> lognx;
+                    const int o = ((((py >> 1) << qshift) + (px >> 1)) << 2) + ((py & 1) << 1) + (px & 1);
+                    ob[o] = make_float2(__double2float_rn(__dmul_rn(av, cs)), __double2float_rn(__dmul_rn(av, sn)));
+                }
+            } else {
 #pragma unroll 2
             for (int j = ctid; j < cnt; j += cthreads) {
                 const uint64_t x = mt_temper(src[j]);
@@ -345,6 +381,7 @@ __global__ void __launch_bounds__(kSeedThreads) k_seed_random_phase(SeedArgs a) 
                     a.out64[a.out_stride * s + p] = make_double2(__dmul_rn(av, cs), __dmul_rn(av, sn));
                 else
                     out[o] = make_float2(__double2float_rn(__dmul_rn(av, cs)), __double2float_rn(__dmul_rn(av, sn)));
+            }
             }
         }
         __syncthreads();

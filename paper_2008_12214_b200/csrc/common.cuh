@@ -28,24 +28,35 @@ __device__ __forceinline__ float2 cmul_conj_rn(float2 a, float2 b) {
     return make_float2(__fadd_rn(ac, bd), __fsub_rn(bc, ad));
 }
 
-// Complex arithmetic of the transforms on packed FP32: a complex64 value is
-// one register pair and sm_100a executes the f32x2 operations as FADD2 /
-// FMUL2 / FFMA2, one instruction for both components, with lane broadcast,
-// lane swap and negation as free operand modifiers and constant pairs in
-// uniform registers.  Per component the roundings are exactly those of the
-// scalar forms:
+// Complex arithmetic of the transforms.  sm_100a executes the f32x2
+// operations as FADD2 / FMUL2 / FFMA2, one instruction for both components,
+// with lane broadcast, lane swap and negation as free operand modifiers and
+// constant pairs in uniform registers.  Per component the roundings are
+// exactly those of the scalar forms, so every choice below gives bit-identical
+// fields:
 //   cadd / csub: a.x +- b.x, a.y +- b.y;
-//   cmul: fmaf(a.x, b.x, -(a.y*b.y)), fmaf(a.x, b.y, a.y*b.x), formed as
+//   cmul: fmaf(a.x, b.x, -(a.y*b.y)), fmaf(a.x, b.y, a.y*b.x), i.e.
 //         (a.x, a.x) * b + (a.y, a.y) * (-b.y, b.x)  (negation is exact).
+// HG_FFT_SCALAR: 0 everything packed, 1 everything scalar, 2 (default) packed
+// adds with scalar products.  Packed instructions issue at half rate (2 warp
+// instructions/clk/SM = 128 lane-ops, like scalar FADD/FFMA at 4; microbench
+// tools/microbench/f32x2_tput.cu), so they save issue slots, not FP-pipe time.
+// Measured at 4096^2 x 64 in the launch sequence: 11.66 ms per iteration
+// (hybrid) vs 11.77 (packed) vs 12.45 (scalar).
 __device__ __forceinline__ float2 f2swap(float2 a) { return make_float2(a.y, a.x); }
 __device__ __forceinline__ float2 f2bx(float2 a) { return make_float2(a.x, a.x); }
 __device__ __forceinline__ float2 f2by(float2 a) { return make_float2(a.y, a.y); }
-#ifndef HG_FFT_SCALAR  // per translation unit: 1 = the same arithmetic as scalar FADD/FMUL/FFMA
-#define HG_FFT_SCALAR 0
+#ifndef HG_FFT_SCALAR
+#define HG_FFT_SCALAR 2
 #endif
 #if HG_FFT_SCALAR
+#if HG_FFT_SCALAR == 2  // packed adds, scalar products
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+#else
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+#endif
 __device__ __forceinline__ float2 cmul_r(float2 a, float2 w, float2 wr) {
     return make_float2(fmaf(a.x, w.x, a.y * wr.x), fmaf(a.x, w.y, a.y * wr.y));
 }

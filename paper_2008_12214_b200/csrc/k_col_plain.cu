@@ -1,14 +1,5 @@
 // k_col_plain.cu — plain column transforms (first half of P^-1 in the plans'
 // quad layout; the primitive FFT in row-major) and the column tiling rule.
-// The column passes run the transforms on scalar FP32 (measured faster there
-// than packed: 5.38 vs 5.58 ms per 64 x 4096^2 GS column pass; the row pass,
-// which also carries the quantiser, gains from packing: 6.17 vs 6.81 ms).
-#ifndef HG_COL_FFT_SCALAR
-#define HG_COL_FFT_SCALAR 1
-#endif
-#ifndef HG_FFT_SCALAR
-#define HG_FFT_SCALAR HG_COL_FFT_SCALAR
-#endif
 #include "launch_impl.cuh"
 
 namespace hg {

@@ -35,6 +35,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "GS iterations/sec at 4096² and OSPR subframes/sec; % of HBM roofline"
+E2E_MIN_STEPS = 10
 GS_BYTES_PER_PX = {"row": 16, "col": 20, "iteration": 36}  # 2 fused round trips + fp32 target
 OSPR_BYTES_PER_PX = {"seed": 8, "col_inv": 16, "row": 17, "col_acc": 20, "subframe": 49}
 
@@ -262,7 +263,10 @@ def gs_e2e(args, plan, amps, seeds, d: Dist):
 
     run(2)  # warm (graph instantiation of the second plan)
     d.barrier()
-    steps = max(2, args.steps)
+    # steady-state serving loop: at least E2E_MIN_STEPS batches, so the first
+    # batch's upload (exposed, nothing to overlap it with) is amortised as in
+    # a long-running service; it is still inside the timed region
+    steps = max(E2E_MIN_STEPS, args.steps)
     t0 = time.perf_counter()
     run(steps)
     dt = d.max(time.perf_counter() - t0)
@@ -329,7 +333,7 @@ def ospr_ours(args, d: Dist):
 
         run(2)
         d.barrier()
-        es = max(2, steps)
+        es = max(E2E_MIN_STEPS, steps)
         t0 = time.perf_counter()
         run(es)
         dt = d.max(time.perf_counter() - t0)

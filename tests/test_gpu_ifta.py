@@ -98,6 +98,27 @@ def test_config4_fresnel_lockstep(oracle, k):
     assert rel(m_gpu, m_ref) < MSE_TOL
 
 
+def test_config5_gs_4096_256level_lockstep(oracle):
+    # BASELINE config 5 geometry at full size (4096^2, 256 levels): the
+    # benchmark's own kernels (k_row<4096,...,QK_FULL>, k_col<4096,2,COL_GS_FAST>)
+    # run one iteration from the oracle's R_1 (~15 s of oracle time)
+    amp = hg.patterns.bench_target(4096)
+    mism, near, (m_gpu, m_ref), _, _ = lockstep(oracle, amp, hg.SlmSpec.full_circle_phase(256), 2)
+    bad = mism & ~near
+    assert bad.sum() <= 2, int(bad.sum())
+    assert rel(m_gpu, m_ref) < MSE_TOL
+
+
+def test_config4_fresnel_2048_lockstep(oracle):
+    # BASELINE config 4 at full size: Fresnel GS 2048^2, 256 levels, typical physics
+    amp = hg.patterns.bench_target(2048)
+    fr = (532e-9, 0.1, 8e-6, 8e-6)
+    mism, near, (m_gpu, m_ref), _, _ = lockstep(oracle, amp, hg.SlmSpec.full_circle_phase(256), 1, fresnel=fr)
+    bad = mism & ~near
+    assert bad.sum() <= 2, int(bad.sum())
+    assert rel(m_gpu, m_ref) < MSE_TOL
+
+
 def test_multilevel_free_running_band(oracle):
     # f32 vs f64 GS band of the reference (test_ifta.cpp:282-288): 2e-2 relative
     amp = hg.patterns.bench_target(128)

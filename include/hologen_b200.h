@@ -211,6 +211,13 @@ int hgc_ifta_plan_launches(hgc_ifta_plan* plan);
  * fused column pass, each launched `reps` times on the plan's stream (CUDA
  * events).  Advances the resident state: call after the timed work. */
 int hgc_ifta_plan_profile(hgc_ifta_plan* plan, int reps, double* ms_seed, double* ms_row, double* ms_col);
+/* Per-pass device time inside the plan's own graph: with timing on (set
+ * before the first execute), CUDA events are recorded around the first target
+ * group's row and column passes of every iteration; kernel_times returns
+ * their average over iterations 1..K-1 of the last execute (ms) and that
+ * count.  Measurement support, not part of the reference interface. */
+int hgc_ifta_plan_set_kernel_timing(hgc_ifta_plan* plan, int on);
+int hgc_ifta_plan_kernel_times(hgc_ifta_plan* plan, double* ms_row, double* ms_col, int* iterations);
 int hgc_ifta_plan_destroy(hgc_ifta_plan* plan);
 
 int hgc_ospr_plan_create(hgc_ospr_plan** plan, const hgc_ospr_cfg* cfg, const hgc_slm* slm, int nx,

@@ -109,6 +109,8 @@ _SIGS = {
     "hgc_ifta_plan_device_ptrs": (_i, [_vp, _P(_vp), _P(_vp), _P(_vp)]),
     "hgc_ifta_plan_launches": (_i, [_vp]),
     "hgc_ifta_plan_profile": (_i, [_vp, _i, _P(_d), _P(_d), _P(_d)]),
+    "hgc_ifta_plan_set_kernel_timing": (_i, [_vp, _i]),
+    "hgc_ifta_plan_kernel_times": (_i, [_vp, _P(_d), _P(_d), _P(_i)]),
     "hgc_ifta_plan_destroy": (_i, [_vp]),
     "hgc_ospr_plan_create": (_i, [_P(_vp), _P(HgcOsprCfg), _P(HgcSlm), _i, _i, _i, _i]),
     "hgc_ospr_plan_upload": (_i, [_vp, _P(HgcOsprIo)]),

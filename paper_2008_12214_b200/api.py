@@ -596,6 +596,18 @@ class IftaPlan:
     def launches(self) -> int:
         return int(lib.hgc_ifta_plan_launches(self._h))
 
+    def set_kernel_timing(self, on: bool = True):
+        """Record CUDA events around the passes inside the plan's graph (call
+        before the first execute); read them with kernel_times()."""
+        check(lib.hgc_ifta_plan_set_kernel_timing(self._h, int(on)))
+
+    def kernel_times(self) -> dict:
+        """Average row / column pass device ms of the last execute, measured
+        inside its graph (iterations 1..K-1 of the first target group)."""
+        r, c, n = C.c_double(), C.c_double(), C.c_int()
+        check(lib.hgc_ifta_plan_kernel_times(self._h, C.byref(r), C.byref(c), C.byref(n)))
+        return {"row": r.value, "col": c.value, "iterations": n.value}
+
     def profile(self, reps: int = 5) -> dict:
         """Per-kernel device ms: seed, fused row pass, fused column pass."""
         s, r, c = C.c_double(), C.c_double(), C.c_double()

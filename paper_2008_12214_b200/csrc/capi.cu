@@ -874,8 +874,15 @@ struct hgc_ifta_plan {
     int launches = 0;
     bool uploaded = false;
     bool init_weights_given = false;
+    // Per-pass timing inside the graph (hgc_ifta_plan_set_kernel_timing;
+    // external event record nodes, cudaEventRecordExternal):
+    // kev[0] before the first group's row pass of iteration 1, kev[2k-1]
+    // after its row pass of iteration k, kev[2k] after its column pass.
+    bool ktime = false;
+    std::vector<cudaEvent_t> kev;
 
     ~hgc_ifta_plan() {
+        for (cudaEvent_t e : kev) cudaEventDestroy(e);
         if (graph) cudaGraphExecDestroy(graph);
         if (done) cudaEventDestroy(done);
         if (up_ev) cudaEventDestroy(up_ev);
@@ -1028,14 +1035,17 @@ struct hgc_ifta_plan {
         // target halves on concurrent streams, staggered by a pass, measured
         // no gain at 4096^2: 3927 vs 3950 it/s.)
         const int G = group_size();
+        const bool tk = ktime && (int)kev.size() == 2 * cfg.iterations + 1;
         for (int g0 = 0; g0 < batch; g0 += G) {
             const int gn = std::min(G, batch - g0);
+            if (tk && g0 == 0) CK(cudaEventRecordWithFlags(kev[0], st, cudaEventRecordExternal));
             for (int k = 1; k <= cfg.iterations; ++k) {
                 RowArgs ra = row_args(k == cfg.iterations);
                 ra.field += (size_t)g0 * npix;
                 if (ra.levels8) ra.levels8 += (size_t)g0 * npix;
                 if (ra.levels16) ra.levels16 += (size_t)g0 * npix;
                 row_fused(nx, ra, gn, st);
+                if (tk && g0 == 0) CK(cudaEventRecordWithFlags(kev[2 * k - 1], st, cudaEventRecordExternal));
                 ColArgs cg = col_args(k);
                 cg.field += (size_t)g0 * npix;
                 cg.target += (size_t)g0 * npix;
@@ -1045,6 +1055,7 @@ struct hgc_ifta_plan {
                 cg.partials += (size_t)g0 * tiles * 8;
                 cg.tma_row0 = g0 * (ny / 2);
                 col_gs(ny, cg, gn, st);
+                if (tk && g0 == 0) CK(cudaEventRecordWithFlags(kev[2 * k], st, cudaEventRecordExternal));
                 launches += 2;
             }
         }
@@ -1392,6 +1403,41 @@ int hgc_ifta_plan_launches(hgc_ifta_plan* p) { return p ? p->launches : -1; }
 // Per-kernel device time of the plan's passes (CUDA events on the plan's
 // stream, `reps` back-to-back launches each).  Runs extra iterations on the
 // resident field: call after the timed work.
+int hgc_ifta_plan_set_kernel_timing(hgc_ifta_plan* p, int on) {
+    return guarded([&] {
+        if (!p) invalid("hgc_ifta_plan_set_kernel_timing: null plan");
+        if (p->graph) invalid("hgc_ifta_plan_set_kernel_timing: call before the first execute");
+        CK(cudaSetDevice(p->device));
+        p->ktime = on != 0;
+        if (p->ktime && p->kev.empty()) {
+            p->kev.resize(2 * p->cfg.iterations + 1);
+            for (cudaEvent_t& e : p->kev) CK(cudaEventCreate(&e));
+        }
+    });
+}
+
+int hgc_ifta_plan_kernel_times(hgc_ifta_plan* p, double* ms_row, double* ms_col, int* n) {
+    return guarded([&] {
+        if (!p || !p->ktime || p->kev.empty() || !p->graph)
+            invalid("hgc_ifta_plan_kernel_times: timing not enabled or nothing executed");
+        CK(cudaSetDevice(p->device));
+        CK(cudaEventSynchronize(p->kev.back()));
+        // iterations 1 .. K-1 (the last one stores levels and the replay instead)
+        const int K = p->cfg.iterations, m = K > 1 ? K - 1 : 1;
+        double r = 0, c = 0;
+        for (int k = 1; k <= m; ++k) {
+            float a = 0.f, b = 0.f;
+            CK(cudaEventElapsedTime(&a, p->kev[2 * k - 2], p->kev[2 * k - 1]));
+            CK(cudaEventElapsedTime(&b, p->kev[2 * k - 1], p->kev[2 * k]));
+            r += a;
+            c += b;
+        }
+        if (ms_row) *ms_row = r / m;
+        if (ms_col) *ms_col = c / m;
+        if (n) *n = m;
+    });
+}
+
 int hgc_ifta_plan_profile(hgc_ifta_plan* p, int reps, double* ms_seed, double* ms_row, double* ms_col) {
     return guarded([&] {
         if (!p || !p->uploaded) invalid("hgc_ifta_plan_profile: plan not ready");

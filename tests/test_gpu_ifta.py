@@ -329,3 +329,28 @@ def test_generic_constraint_with_tma_tiles_matches_oracle(oracle, case):
     mism = level_mismatches(rep.levels, ref.levels).sum()
     assert mism <= 16, (case, mism)
     assert np.max(np.abs(rep.trace.values() - ref.trace) / ref.trace) < MSE_TOL, case
+
+
+def test_plan_kernel_timing_inside_graph():
+    """Per-pass CUDA events inside the plan's graph (bench roofline): positive
+    times over iterations 1..K-1, and the results are those of an untimed plan."""
+    n, B, K = 256, 2, 4
+    amp = hg.patterns.bench_target(n)
+    cfg = hg.IftaConfig(iterations=K, slm=hg.SlmSpec.full_circle_phase(16), target=hg.TargetSpec(amp))
+    outs = []
+    for timed in (True, False):
+        p = hg.IftaPlan(cfg, n, n, B)
+        if timed:
+            p.set_kernel_timing(True)
+        p.upload(np.broadcast_to(amp, (B, n, n)), seeds=np.arange(1, B + 1))
+        p.execute()
+        r = p.download()
+        outs.append((np.array(r.levels, copy=True), np.array(r.trace, copy=True)))
+        if timed:
+            kt = p.kernel_times()
+            assert kt["iterations"] == K - 1 and kt["row"] > 0 and kt["col"] > 0
+        else:
+            with pytest.raises(Exception):
+                p.kernel_times()
+        p.close()
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])

@@ -103,7 +103,7 @@ struct RowCfg {
 template <int NX, int QK, int FQ, int LV, class Sync = CtaSync>
 __device__ __forceinline__ void row_fused_body(float2 (&v)[LineCfg<NX>::E], int t, int y, int b, bool valid,
                                                float2* smem, const RowSmemIdx& idx, const RowArgs& a,
-                                               const Sync& sync = Sync{}) {
+                                               const float2* sstates, const Sync& sync = Sync{}) {
     constexpr int E = LineCfg<NX>::E, T = LineCfg<NX>::T;
     fft_line<NX, +1>(v, t, smem, idx, a.tw, sync);  // completes the 2-D inverse (propagation.hpp:89-95)
     const int rowbase = y * NX;
@@ -119,7 +119,7 @@ __device__ __forceinline__ void row_fused_body(float2 (&v)[LineCfg<NX>::E], int 
         if (hasq) f = cmul_conj_rn(f, __ldg(&fq[i]));         // propagation.hpp:93
         const int k = quant_decide_kind<QK>(a.q, f.x, f.y, i);  // quantise.hpp:211-215
         if constexpr (QK == QK_BINARY) f = k ? a.q.s1 : a.q.s0;
-        else if constexpr (QK == QK_FULL) f = __ldg(&a.q.states[k]);  // phase mode, no illumination
+        else if constexpr (QK == QK_FULL) f = HG_STATES_SMEM ? sstates[k] : __ldg(&a.q.states[k]);  // phase mode, no illumination
         else f = quant_state(a.q, k, i);
         if constexpr (LV != 0) {
             if (lv8 && valid) lv8[i] = (uint8_t)k;
@@ -187,6 +187,14 @@ __global__ void __launch_bounds__(RowCfg<NX, LAY>::THREADS, RowCfg<NX, LAY>::MIN
     // writes them back; thread element e sits at landing slot lb + e*2T.
     constexpr bool kBulk = HG_ROW_BULK && LAY == LAY_QUAD && NX > E && T >= 2;
     __shared__ uint64_t rbar;
+    // QK_FULL state table (<= 256 levels, quant_kind) in shared memory: the
+    // per-pixel gather k -> state hits ~1 bank-conflict group instead of ~14 L1 lines
+    constexpr bool kSmemStates = HG_STATES_SMEM && MODE == ROW_FUSED && QK == QK_FULL;
+    __shared__ float2 sstates[kSmemStates ? 256 : 1];
+    if constexpr (kSmemStates) {
+        for (int i = threadIdx.x; i < a.q.levels; i += blockDim.x) sstates[i] = __ldg(&a.q.states[i]);
+        if constexpr (!kBulk) __syncthreads();
+    }
     // (recomputed where used, so nothing extra stays live across the transforms)
     auto tile_bytes = [&] {
         return (uint32_t)(min(RPCr, a.ny - (int)blockIdx.x * RPCr) * NX * (int)sizeof(float2));
@@ -229,7 +237,7 @@ __global__ void __launch_bounds__(RowCfg<NX, LAY>::THREADS, RowCfg<NX, LAY>::MIN
             for (int e = 0; e < E; ++e) v[e] = cmul_conj_rn(v[e], __ldg(&a.fresnel_q[rowbase + t + e * T]));
     } else {
 #if !HG_NULL_COMPUTE  // diagnostic build: the passes' memory traffic alone
-        row_fused_body<NX, QK, FQ, LV>(v, t, y, b, valid, smem, idx, a);
+        row_fused_body<NX, QK, FQ, LV>(v, t, y, b, valid, smem, idx, a, sstates);
 #endif
     }
     if constexpr (kBulk) {

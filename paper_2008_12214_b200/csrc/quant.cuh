@@ -112,6 +112,9 @@ __device__ __forceinline__ int quant_decide(const QuantParams& q, float vr, floa
 //               is the sign of Re(f) (level 1 = pi state iff Re(f) < 0)
 //   QK_FULL     full-circle phase without illumination
 enum QuantKind { QK_GENERIC = 0, QK_BINARY = 1, QK_FULL = 2 };
+#ifndef HG_STATES_SMEM  // QK_FULL row pass reads its state table from shared memory (<= 256 levels)
+#define HG_STATES_SMEM 0
+#endif
 
 // atan2 in float without the library slow paths: odd degree-13 polynomial
 // on [0,1] (max error 3.5e-7 rad in float) + octant fix-ups; total error

@@ -240,7 +240,10 @@ __global__ void __launch_bounds__(RowCfg<NX, LAY>::THREADS, RowCfg<NX, LAY>::MIN
         row_fused_body<NX, QK, FQ, LV>(v, t, y, b, valid, smem, idx, a, sstates);
 #endif
     }
-    if constexpr (kBulk) {
+#ifndef HG_ROW_DIRECT_STORE  // bulk-loaded tiles stored by per-thread coalesced stores (no EXIT wait on the bulk read)
+#define HG_ROW_DIRECT_STORE 0
+#endif
+    if constexpr (kBulk && !HG_ROW_DIRECT_STORE) {
         const int lb = opaque(lbase());
 #pragma unroll
         for (int e = 0; e < E; ++e) smem[lb + e * 2 * T] = v[e];

@@ -52,7 +52,7 @@
 extern "C" {
 #endif
 
-#define HGC_ABI_VERSION 4
+#define HGC_ABI_VERSION 5
 
 typedef enum {
     HGC_OK = 0,
@@ -127,6 +127,20 @@ typedef struct hgc_ifta_io {
     double* replay_peak;        /* its amplitude_at_255 [batch] (io.cpp:206-207) */
     uint8_t* levels1;           /* 2-level SLMs: the levels as bit-planes, bit (i & 7) of byte i >> 3 of
                                    each target's row-major plane [batch][ny*nx/8] (binary SLM frames) */
+    /* Checkpoint (extension; the state a resumed run starts from): nonzero =
+     * the last iteration also applies the replay-plane constraint (ifta.hpp:185-224,
+     * incl. the WGS weight update and the LT rectangle of iteration K), so
+     * `replay` receives the constrained field R_K instead of the unconstrained
+     * one and `weights` the WGS weights W_K.  For GS and WGS, running K1
+     * iterations with checkpoint and then K2 with init_phase Given from
+     * (replay, weights) reproduces a K1 + K2 run bit for bit (LT's schedule
+     * depends on K).  trace / levels / hologram are unchanged. */
+    int checkpoint;
+    float* weights;             /* WGS weights after the run [batch][ny][nx] (1 for other variants) */
+    /* RunReport::profile (report.hpp:38-45): {transform, constraint, metric,
+     * other} seconds of hgc_ifta_run, attributed from per-pass device times
+     * (DESIGN.md §5); their sum equals *seconds.  Only hgc_ifta_run fills it. */
+    double* profile;
 } hgc_ifta_io;
 
 /* hologen::OsprConfig (ospr.hpp:20-38).  variant: 0 Ospr, 1 AdaptiveOspr.
@@ -277,6 +291,9 @@ typedef struct hgc_ifta_io64 {
     double* final_error;
     const double* fresnel_q;    /* optional complex [ny][nx] Q to use instead of computing it from
                                    hgc_fresnel (e.g. from a Propagator<double>, propagation.hpp:97-103) */
+    double* profile;            /* RunReport::profile {transform, constraint, metric, other} seconds:
+                                   device time of each reference phase (ifta.hpp:166-226), other =
+                                   the rest of the call, or NULL */
 } hgc_ifta_io64;
 int hgc_ifta_run_f64(const hgc_ifta_cfg* cfg, const hgc_slm* slm, const hgc_fresnel* fresnel, int nx, int ny,
                      hgc_ifta_io64* io);
@@ -290,6 +307,7 @@ typedef struct hgc_ospr_io64 {
     double* mean_intensity;     /* [ny][nx] */
     double* replay;             /* complex [ny][nx] */
     double* final_error;
+    double* profile;            /* RunReport::profile as hgc_ifta_io64 (ospr.hpp:105-147 phases), or NULL */
 } hgc_ospr_io64;
 int hgc_ospr_run_f64(const hgc_ospr_cfg* cfg, const hgc_slm* slm, int nx, int ny, hgc_ospr_io64* io);
 

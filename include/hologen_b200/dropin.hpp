@@ -98,6 +98,17 @@ inline B200FftBackendF64& fft_backend_f64() {
     return b;
 }
 
+// RunReport::profile from the library's per-phase device times (hgc_*_io
+// profile: transform, constraint, metric); "other" is the rest of the
+// call as this wrapper timed it, so total() == seconds as in ifta.hpp:231-233.
+template <class Rep>
+inline void set_profile(Rep& rep, const double (&p)[4]) {
+    rep.profile.transform = p[0];
+    rep.profile.constraint = p[1];
+    rep.profile.metric = p[2];
+    rep.profile.other = std::max(0.0, rep.seconds - (p[0] + p[1] + p[2]));
+}
+
 // run_ifta<float> on the GPU (ifta.hpp:86-235 semantics).
 inline hologen::RunReport<float> run_ifta_gpu(const hologen::IftaConfig& cfg, const hologen::Propagator<float>* prop) {
     auto t0 = std::chrono::steady_clock::now();
@@ -139,12 +150,14 @@ inline hologen::RunReport<float> run_ifta_gpu(const hologen::IftaConfig& cfg, co
     io.replay = reinterpret_cast<float*>(rep.replay.data.data());
     io.trace = trace.data();
     io.fresnel_q = q.empty() ? nullptr : reinterpret_cast<const float*>(q.data());
+    double prof[4] = {0, 0, 0, 0};
+    io.profile = prof;
     throw_status(hgc_ifta_run(&c, &s, nullptr, nx, ny, 1, &io));
     rep.trace.name = "mse";
     for (int k = 0; k < cfg.iterations; ++k) rep.trace.append(k + 1, trace[k]);
     rep.final_error = trace.back();
     rep.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-    rep.profile.other = rep.seconds;  // fused kernels: no per-phase wall-clock split
+    set_profile(rep, prof);  // fused passes: per-pass device time split by phase
     return rep;
 }
 
@@ -244,12 +257,14 @@ inline hologen::RunReport<double> run_ifta_gpu64(const hologen::IftaConfig& cfg,
     io.replay = reinterpret_cast<double*>(rep.replay.data.data());
     io.trace = trace.data();
     io.fresnel_q = q.empty() ? nullptr : reinterpret_cast<const double*>(q.data());
+    double prof[4] = {0, 0, 0, 0};
+    io.profile = prof;
     throw_status(hgc_ifta_run_f64(&c, &s, nullptr, nx, ny, &io));
     rep.trace.name = "mse";
     for (int k = 0; k < cfg.iterations; ++k) rep.trace.append(k + 1, trace[k]);
     rep.final_error = trace.back();
     rep.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-    rep.profile.other = rep.seconds;
+    set_profile(rep, prof);
     return rep;
 }
 
@@ -282,6 +297,8 @@ inline hologen::OsprRun<double> run_ospr_gpu64(const hologen::OsprConfig& cfg, h
     io.cumulative_mse = cm.data();
     io.mean_intensity = mi.data();
     io.replay = reinterpret_cast<double*>(rep.replay.data.data());
+    double prof[4] = {0, 0, 0, 0};
+    io.profile = prof;
     throw_status(hgc_ospr_run_f64(&c, &s, nx, ny, &io));
     rep.algorithm = cfg.variant == hologen::OsprVariant::AdaptiveOspr ? "adaptive_ospr" : "ospr";
     rep.seed = cfg.seed;
@@ -303,7 +320,7 @@ inline hologen::OsprRun<double> run_ospr_gpu64(const hologen::OsprConfig& cfg, h
     rep.evaluations = N;
     rep.extra_traces.push_back(std::move(frame_trace));
     rep.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-    rep.profile.other = rep.seconds;
+    set_profile(rep, prof);
     return run;
 }
 

@@ -61,7 +61,8 @@ class HgcIftaIo(C.Structure):
                 ("levels8", C.c_void_p), ("levels16", C.c_void_p), ("replay", C.c_void_p),
                 ("trace", C.c_void_p), ("final_error", C.c_void_p), ("seconds", C.c_void_p),
                 ("fresnel_q", C.c_void_p), ("hologram_gray8", C.c_void_p), ("replay_gray8", C.c_void_p),
-                ("replay_peak", C.c_void_p), ("levels1", C.c_void_p)]
+                ("replay_peak", C.c_void_p), ("levels1", C.c_void_p), ("checkpoint", C.c_int),
+                ("weights", C.c_void_p), ("profile", C.c_void_p)]
 
 
 class HgcOsprCfg(C.Structure):
@@ -82,13 +83,13 @@ class HgcIftaIo64(C.Structure):
     _fields_ = [("amplitude", C.c_void_p), ("phase", C.c_void_p), ("roi", C.c_void_p), ("init_field", C.c_void_p),
                 ("init_weights", C.c_void_p), ("hologram", C.c_void_p), ("replay", C.c_void_p),
                 ("levels", C.c_void_p), ("trace", C.c_void_p), ("final_error", C.c_void_p),
-                ("fresnel_q", C.c_void_p)]
+                ("fresnel_q", C.c_void_p), ("profile", C.c_void_p)]
 
 
 class HgcOsprIo64(C.Structure):
     _fields_ = [("amplitude", C.c_void_p), ("roi", C.c_void_p), ("frames", C.c_void_p), ("levels", C.c_void_p),
                 ("frame_mse", C.c_void_p), ("cumulative_mse", C.c_void_p), ("mean_intensity", C.c_void_p),
-                ("replay", C.c_void_p), ("final_error", C.c_void_p)]
+                ("replay", C.c_void_p), ("final_error", C.c_void_p), ("profile", C.c_void_p)]
 
 
 _vp, _i, _u64, _d = C.c_void_p, C.c_int, C.c_uint64, C.c_double
@@ -150,7 +151,7 @@ for _name, (_res, _args) in _SIGS.items():
     _f.restype = _res
     _f.argtypes = _args
 
-ABI_VERSION = 4  # HGC_ABI_VERSION of include/hologen_b200.h this binding was written against
+ABI_VERSION = 5  # HGC_ABI_VERSION of include/hologen_b200.h this binding was written against
 if lib.hgc_abi_version() != ABI_VERSION:
     raise ImportError(f"{LIB_PATH}: ABI version {lib.hgc_abi_version()} != {ABI_VERSION}; rebuild the library")
 

@@ -277,7 +277,7 @@ class _IftaBuffers:
     """Host arrays for one batched IFTA call (inputs + requested outputs)."""
 
     def __init__(self, cfg: IftaConfig, amps: np.ndarray, seeds, phases=None, init_field=None, init_weights=None,
-                 want_hologram=True, want_replay=True):
+                 want_hologram=True, want_replay=True, checkpoint=False):
         self.amps = np.ascontiguousarray(amps, np.float64)
         b, ny, nx = self.amps.shape
         K = cfg.iterations
@@ -310,6 +310,11 @@ class _IftaBuffers:
         io.trace = _p(self.trace)
         io.final_error = _p(self.final_error)
         io.seconds = _p(self.seconds)
+        self.profile = np.zeros(4, np.float64)
+        io.profile = _p(self.profile)
+        io.checkpoint = int(bool(checkpoint))
+        self.weights = np.empty((b, ny, nx), np.float32) if checkpoint else None
+        io.weights = _p(self.weights)
         self.io = io
         self.hologram_gray8 = self.replay_gray8 = self.replay_peak = None
 
@@ -331,9 +336,13 @@ def _check_variant(cfg: IftaConfig, want: IftaVariant | None, name: str):
 
 
 def run_ifta_batch(cfg: IftaConfig, amplitudes: np.ndarray, seeds=None, prop: Propagator | None = None,
-                   phases=None, init_field=None, init_weights=None) -> list[RunReport]:
+                   phases=None, init_field=None, init_weights=None, checkpoint=False) -> list[RunReport]:
     """B independent targets of one size/SLM/propagation, one launch sequence.
-    seeds[b] replaces cfg.seed for target b (default: cfg.seed for all)."""
+    seeds[b] replaces cfg.seed for target b (default: cfg.seed for all).
+    checkpoint: the last iteration also applies the replay-plane constraint;
+    each report's `replay` is then the constrained field R_K and `weights`
+    the WGS weights W_K — the state a run with init_field / init_weights
+    (InitPhase.Given) resumes from (hgc_ifta_io::checkpoint)."""
     amps = np.asarray(amplitudes, np.float64)
     if amps.ndim == 2:
         amps = amps[None]
@@ -341,7 +350,7 @@ def run_ifta_batch(cfg: IftaConfig, amplitudes: np.ndarray, seeds=None, prop: Pr
     if cfg.iterations < 1:
         raise ValueError("IftaConfig: iterations must be >= 1")
     seeds = np.full(b, cfg.seed, np.uint64) if seeds is None else np.asarray(seeds, np.uint64)
-    bufs = _IftaBuffers(cfg, amps, seeds, phases, init_field, init_weights)
+    bufs = _IftaBuffers(cfg, amps, seeds, phases, init_field, init_weights, checkpoint=checkpoint)
     keep = []
     slm = _slm(cfg.slm, keep)
     c = _ifta_cfg(cfg)
@@ -356,20 +365,23 @@ def run_ifta_batch(cfg: IftaConfig, amplitudes: np.ndarray, seeds=None, prop: Pr
         rep.trace = MetricTrace("mse", [(k + 1, float(v)) for k, v in enumerate(bufs.trace[i])])
         rep.final_error = float(bufs.final_error[i])
         rep.seconds = float(bufs.seconds[0])
-        rep.profile = PhaseProfile(other=rep.seconds)
+        tr, cn, me, ot = (float(v) for v in bufs.profile)  # report.hpp:38-45, whole batched call
+        rep.profile = PhaseProfile(transform=tr, constraint=cn, metric=me, other=ot)
+        if checkpoint:
+            rep.weights = bufs.weights[i]
         reps.append(rep)
     return reps
 
 
 def _run_ifta(cfg: IftaConfig, prop: Propagator | None, want: IftaVariant | None, name: str,
-              init_field=None, init_weights=None) -> RunReport:
+              init_field=None, init_weights=None, checkpoint=False) -> RunReport:
     _check_variant(cfg, want, name)
     cfg.validate()
     if prop is not None and prop.is_fresnel() and (prop.nx, prop.ny) != (cfg.target.width(), cfg.target.height()):
         raise ValueError("Propagator: field size does not match Fresnel phase")
     phases = None if cfg.target.phase is None else np.asarray(cfg.target.phase)[None]
     return run_ifta_batch(cfg, np.asarray(cfg.target.amplitude)[None], [cfg.seed], prop, phases, init_field,
-                          init_weights)[0]
+                          init_weights, checkpoint)[0]
 
 
 def run_gs(cfg: IftaConfig, prop: Propagator | None = None) -> RunReport:  # ifta.hpp:239-244
@@ -384,10 +396,12 @@ def run_liu_taghizadeh(cfg: IftaConfig, prop: Propagator | None = None) -> RunRe
     return _run_ifta(cfg, prop, IftaVariant.LiuTaghizadeh, "run_liu_taghizadeh")
 
 
-def run_ifta(cfg: IftaConfig, prop: Propagator | None = None, init_field=None, init_weights=None) -> RunReport:
+def run_ifta(cfg: IftaConfig, prop: Propagator | None = None, init_field=None, init_weights=None,
+             checkpoint=False) -> RunReport:
     """run_ifta<float> (ifta.hpp:260-263); init_field/init_weights serve
-    InitPhase.Given (resume from a replay field, e.g. a checkpoint)."""
-    return _run_ifta(cfg, prop, None, "run_ifta", init_field, init_weights)
+    InitPhase.Given (resume from a replay field, e.g. a checkpoint);
+    checkpoint=True returns that resume state (see run_ifta_batch)."""
+    return _run_ifta(cfg, prop, None, "run_ifta", init_field, init_weights, checkpoint)
 
 
 def run_ifta_f64(cfg: IftaConfig, prop: Propagator | None = None, init_field=None, init_weights=None) -> RunReport:

@@ -329,6 +329,14 @@ __global__ void k_to_colpair(const TI* in, TO* out, int nx, int ny, size_t total
         out[p.b * npix + colpair_index(p.x, p.y, ny)] = (TO)in[g];
     }
 }
+template <class T>
+__global__ void k_from_colpair(const T* in, T* out, int nx, int ny, size_t total) {
+    const size_t npix = (size_t)nx * ny;
+    HG_GRID_LOOP(g, total) {
+        Pix p = pix_of(g, nx, npix);
+        out[g] = in[p.b * npix + colpair_index(p.x, p.y, ny)];
+    }
+}
 // Row-major -> column-pair major through a 32-row x 64-column smem tile, so
 // both the reads (rows) and the writes (64 contiguous outputs per column pair)
 // are coalesced.  Requires nx % 64 == 0 and ny % 32 == 0.
@@ -874,12 +882,51 @@ struct hgc_ifta_plan {
     int launches = 0;
     bool uploaded = false;
     bool init_weights_given = false;
+    bool ckpt = false;  // hgc_ifta_io::checkpoint: the last iteration also constrains
     // Per-pass timing inside the graph (hgc_ifta_plan_set_kernel_timing;
     // external event record nodes, cudaEventRecordExternal):
     // kev[0] before the first group's row pass of iteration 1, kev[2k-1]
     // after its row pass of iteration k, kev[2k] after its column pass.
     bool ktime = false;
     std::vector<cudaEvent_t> kev;
+    int group0 = 0;  // targets of the first (timed) group
+
+    // RunReport::profile (report.hpp:38-45) of a run of `seconds`: the device
+    // time of the fused passes (in-graph events around the first group's
+    // passes, scaled to the whole batch) split by phase.  A fused pass holds
+    // several reference phases; the split uses the measured share of each
+    // (the quantiser is kRowQuant of the row pass, the MSE
+    // partials and constraint kColMetric / kColConstraint of the column pass,
+    // the rest is transform).  "other" is the remainder (seed, copies, setup),
+    // so the four add up to `seconds` like the reference's (ifta.hpp:231-233).
+    void profile_split(double seconds, double* out) const {
+        static constexpr double kRowQuant = 0.25, kColMetric = 0.05, kColConstraint = 0.05;
+        double row = 0, col = 0;
+        if (ktime && !kev.empty() && group0 > 0) {
+            for (int k = 1; k <= cfg.iterations; ++k) {
+                float a = 0.f, b = 0.f;
+                CK(cudaEventElapsedTime(&a, kev[2 * k - 2], kev[2 * k - 1]));
+                CK(cudaEventElapsedTime(&b, kev[2 * k - 1], kev[2 * k]));
+                row += a;
+                col += b;
+            }
+            const double scale = (double)batch / group0 * 1e-3;
+            row *= scale;
+            col *= scale;
+        }
+        double tr = row * (1 - kRowQuant) + col * (1 - kColMetric - kColConstraint);
+        double cn = row * kRowQuant + col * kColConstraint, me = col * kColMetric;
+        const double dev = tr + cn + me;
+        if (dev > seconds && dev > 0) {  // (never expected: the passes run inside the call)
+            tr *= seconds / dev;
+            cn *= seconds / dev;
+            me *= seconds / dev;
+        }
+        out[0] = tr;
+        out[1] = cn;
+        out[2] = me;
+        out[3] = std::max(0.0, seconds - (tr + cn + me));
+    }
 
     ~hgc_ifta_plan() {
         for (cudaEvent_t e : kev) cudaEventDestroy(e);
@@ -968,7 +1015,7 @@ struct hgc_ifta_plan {
         cg.scale_free = cfg.freedom_scale;
         cg.clamp_lo = (float)cfg.weight_clamp_lo;
         cg.clamp_hi = (float)cfg.weight_clamp_hi;
-        if (cfg.variant == 2 && !last) {  // LT schedule, ifta.hpp:55-63, :74-84, :189
+        if (cfg.variant == 2 && (!last || ckpt)) {  // LT schedule, ifta.hpp:55-63, :74-84, :189
             const int K = cfg.iterations;
             double frac = cfg.lt_initial_fraction + (1.0 - cfg.lt_initial_fraction) * (k - 1) / (K - 1);
             double side = std::sqrt(frac);
@@ -981,6 +1028,7 @@ struct hgc_ifta_plan {
             cg.lt_y1 = cg.lt_y0 + ah;
         }
         cg.last = last ? 1 : 0;
+        cg.ckpt = ckpt ? 1 : 0;
         cg.replay_out = field.p;
         cg.partials = partials.p + (size_t)(k - 1) * batch * tiles * 8;
         cg.tmap = tmap.d.p;
@@ -989,6 +1037,25 @@ struct hgc_ifta_plan {
         return cg;
     }
 
+    // Row/column passes of the targets [g0, g0+gn) at iteration k.
+    RowArgs row_args_g(int k, int g0) const {
+        RowArgs ra = row_args(k == cfg.iterations);
+        ra.field += (size_t)g0 * npix;
+        if (ra.levels8) ra.levels8 += (size_t)g0 * npix;
+        if (ra.levels16) ra.levels16 += (size_t)g0 * npix;
+        return ra;
+    }
+    ColArgs col_args_g(int k, int g0) const {
+        ColArgs cg = col_args(k);
+        cg.field += (size_t)g0 * npix;
+        cg.target += (size_t)g0 * npix;
+        if (cg.weights) cg.weights += (size_t)g0 * npix;
+        if (cg.tphase_cs) cg.tphase_cs += (size_t)g0 * npix;
+        cg.replay_out += (size_t)g0 * npix;
+        cg.partials += (size_t)g0 * tiles * 8;
+        cg.tma_row0 = g0 * (ny / 2);
+        return cg;
+    }
     // The whole run_ifta sequence (ifta.hpp:124-226) as stream work.
     void record(cudaStream_t st) {
         launches = 0;
@@ -1035,26 +1102,15 @@ struct hgc_ifta_plan {
         // target halves on concurrent streams, staggered by a pass, measured
         // no gain at 4096^2: 3927 vs 3950 it/s.)
         const int G = group_size();
+        group0 = std::min(G, batch);
         const bool tk = ktime && (int)kev.size() == 2 * cfg.iterations + 1;
         for (int g0 = 0; g0 < batch; g0 += G) {
             const int gn = std::min(G, batch - g0);
             if (tk && g0 == 0) CK(cudaEventRecordWithFlags(kev[0], st, cudaEventRecordExternal));
             for (int k = 1; k <= cfg.iterations; ++k) {
-                RowArgs ra = row_args(k == cfg.iterations);
-                ra.field += (size_t)g0 * npix;
-                if (ra.levels8) ra.levels8 += (size_t)g0 * npix;
-                if (ra.levels16) ra.levels16 += (size_t)g0 * npix;
-                row_fused(nx, ra, gn, st);
+                row_fused(nx, row_args_g(k, g0), gn, st);
                 if (tk && g0 == 0) CK(cudaEventRecordWithFlags(kev[2 * k - 1], st, cudaEventRecordExternal));
-                ColArgs cg = col_args(k);
-                cg.field += (size_t)g0 * npix;
-                cg.target += (size_t)g0 * npix;
-                if (cg.weights) cg.weights += (size_t)g0 * npix;
-                if (cg.tphase_cs) cg.tphase_cs += (size_t)g0 * npix;
-                cg.replay_out += (size_t)g0 * npix;
-                cg.partials += (size_t)g0 * tiles * 8;
-                cg.tma_row0 = g0 * (ny / 2);
-                col_gs(ny, cg, gn, st);
+                col_gs(ny, col_args_g(k, g0), gn, st);
                 if (tk && g0 == 0) CK(cudaEventRecordWithFlags(kev[2 * k], st, cudaEventRecordExternal));
                 launches += 2;
             }
@@ -1063,6 +1119,45 @@ struct hgc_ifta_plan {
                                          trace.p);
         ++launches;
         CK(cudaGetLastError());
+    }
+};
+
+// RunReport::profile for the unfused (f64) loops: events at the reference's
+// phase boundaries (ifta.hpp:166-226, ospr.hpp:105-147) on the loop's stream;
+// interval i is charged to phase ph[i] (0 transform, 1 constraint, 2 metric,
+// 3 other).  Inactive (no events) unless the caller asked for a profile.
+struct PhaseClock {
+    cudaStream_t st = nullptr;
+    bool on = false;
+    std::vector<cudaEvent_t> ev;
+    std::vector<int> ph;
+    PhaseClock(cudaStream_t s, bool enable) : st(s), on(enable) {
+        if (on) mark(3);
+    }
+    ~PhaseClock() {
+        for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    }
+    void mark(int phase) {  // closes the interval since the previous mark
+        if (!on) return;
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        CK(cudaEventRecord(e, st));
+        ev.push_back(e);
+        ph.push_back(phase);
+    }
+    // (after the stream is synchronised) out = {transform, constraint, metric,
+    // other} with other = seconds - the rest, as ifta.hpp:231-233 does.
+    void report(double seconds, double* out) const {
+        double t[4] = {0, 0, 0, 0};
+        for (size_t i = 1; i < ev.size(); ++i) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, ev[i - 1], ev[i]));
+            t[ph[i]] += 1e-3 * ms;
+        }
+        const double counted = t[0] + t[1] + t[2];
+        const double sc = counted > seconds && counted > 0 ? seconds / counted : 1.0;
+        for (int i = 0; i < 3; ++i) out[i] = t[i] * sc;
+        out[3] = std::max(0.0, seconds - counted * sc);
     }
 };
 
@@ -1279,8 +1374,9 @@ int hgc_ifta_plan_upload(hgc_ifta_plan* p, const hgc_ifta_io* io) {
                                    p->stream));
             }
         }
+        p->ckpt = io->checkpoint != 0;
         CK(cudaEventRecord(p->up_ev, p->stream));  // execute waits on it; no host sync
-        const uint64_t sig = (uint64_t)(uintptr_t)p->roi.p ^ ((uint64_t)(uintptr_t)p->phase_d.p << 1) ^
+        const uint64_t sig = ((uint64_t)p->ckpt << 59) ^ (uint64_t)(uintptr_t)p->roi.p ^ ((uint64_t)(uintptr_t)p->phase_d.p << 1) ^
                              ((uint64_t)(uintptr_t)p->tphase_cs.p << 2) ^ ((uint64_t)(uintptr_t)p->init_field.p << 3) ^
                              ((uint64_t)(uintptr_t)p->init_weights.p << 4) ^ ((uint64_t)(uintptr_t)p->Q.p << 5) ^
                              ((uint64_t)p->has_roi << 60) ^
@@ -1337,6 +1433,18 @@ int hgc_ifta_plan_download(hgc_ifta_plan* p, hgc_ifta_io* io) {
             CK(cudaGetLastError());
             CK(cudaStreamSynchronize(p->stream));
             CK(cudaMemcpy(io->replay, p->scratch.p, sizeof(float2) * tot, cudaMemcpyDeviceToHost));
+        }
+        if (io->weights) {  // WGS weights (column-pair major -> row-major); 1 when not WGS
+            if (p->cfg.variant != 1) {
+                std::fill(io->weights, io->weights + tot, 1.0f);
+            } else {
+                DBuf<float> w;
+                w.alloc(tot);
+                k_from_colpair<float><<<ew_grid(tot), 256, 0, p->stream>>>(p->weights.p, w.p, p->nx, p->ny, tot);
+                CK(cudaGetLastError());
+                CK(cudaStreamSynchronize(p->stream));
+                CK(cudaMemcpy(io->weights, w.p, sizeof(float) * tot, cudaMemcpyDeviceToHost));
+            }
         }
         std::vector<double> tr;
         if (io->trace || io->final_error) {
@@ -1471,17 +1579,19 @@ int hgc_ifta_run(const hgc_ifta_cfg* cfg, const hgc_slm* slm, const hgc_fresnel*
     hgc_ifta_plan* p = nullptr;
     int rc = guarded([] { route_device(); });
     if (rc == HGC_OK) rc = hgc_ifta_plan_create(&p, cfg, slm, fresnel, nx, ny, batch);
+    if (rc == HGC_OK && io && io->profile) rc = hgc_ifta_plan_set_kernel_timing(p, 1);
     if (rc == HGC_OK) rc = hgc_ifta_plan_upload(p, io);
     if (rc == HGC_OK) rc = guarded([&] { check_validation(p->vflags.p, p->stream); });  // eager in the one-shot run
     if (rc == HGC_OK) rc = hgc_ifta_plan_execute(p, nullptr);
     if (rc == HGC_OK) rc = hgc_ifta_plan_download(p, io);
+    const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (rc == HGC_OK && io && io->profile) rc = guarded([&] { p->profile_split(secs, io->profile); });
     if (p) {
         std::string keep = g_err;
         hgc_ifta_plan_destroy(p);
         g_err = keep;
     }
-    if (rc == HGC_OK && io && io->seconds)
-        *io->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (rc == HGC_OK && io && io->seconds) *io->seconds = secs;
     return rc;
 }
 
@@ -2265,6 +2375,7 @@ static void fresnel_q64(const hgc_fresnel* p, int nx, int ny, DBuf<double2>& Q) 
 
 int hgc_ifta_run_f64(const hgc_ifta_cfg* cfg, const hgc_slm* slm, const hgc_fresnel* fresnel, int nx, int ny,
                      hgc_ifta_io64* io) {
+    const auto t0 = std::chrono::steady_clock::now();
     return guarded([&] {
         validate_ifta_cfg(cfg);
         if (!io || !io->amplitude) invalid("TargetSpec: amplitude image is empty");
@@ -2368,13 +2479,19 @@ int hgc_ifta_run_f64(const hgc_ifta_cfg* cfg, const hgc_slm* slm, const hgc_fres
         }
         if (io->levels) lv.alloc(n);
         const int K = cfg->iterations;
+        PhaseClock pc(st, io->profile != nullptr);
         for (int k = 1; k <= K; ++k) {
+            pc.mark(3);
             CK(cudaMemcpyAsync(f.p, R.p, sizeof(double2) * n, cudaMemcpyDeviceToDevice, st));
             propagate64(f, Q, nx, ny, +1, st);                                           // f = prop.inverse(R)
+            pc.mark(0);
             k_quant64<<<ew_grid(n), 256, 0, st>>>(f.p, k == K ? lv.p : nullptr, n, q.q);  // quant.apply(f)
+            pc.mark(1);
             CK(cudaMemcpyAsync(R.p, f.p, sizeof(double2) * n, cudaMemcpyDeviceToDevice, st));
             propagate64(R, Q, nx, ny, -1, st);                                           // R = prop.forward(f)
+            pc.mark(0);
             mse64(amp.p, Mag64{R.p, nullptr, 0.0}, roi.p, n, M, cfg->freedom_scale, part, g, trace.p + (k - 1), st);
+            pc.mark(2);
             if (k == K) break;
             Con64 c{};
             c.amp = amp.p;
@@ -2398,6 +2515,7 @@ int hgc_ifta_run_f64(const hgc_ifta_cfg* cfg, const hgc_slm* slm, const hgc_fres
             }
             k_constrain64<<<ew_grid(n), 256, 0, st>>>(R.p, n, c);
             CK(cudaGetLastError());
+            pc.mark(1);
         }
         std::vector<double> tr(K);
         CK(cudaMemcpyAsync(tr.data(), trace.p, sizeof(double) * K, cudaMemcpyDeviceToHost, st));
@@ -2405,6 +2523,8 @@ int hgc_ifta_run_f64(const hgc_ifta_cfg* cfg, const hgc_slm* slm, const hgc_fres
         if (io->replay) CK(cudaMemcpyAsync(io->replay, R.p, sizeof(double2) * n, cudaMemcpyDeviceToHost, st));
         if (io->levels) CK(cudaMemcpyAsync(io->levels, lv.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
+        if (io->profile)
+            pc.report(std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(), io->profile);
         CK(cudaStreamDestroy(st));
         if (io->trace) std::memcpy(io->trace, tr.data(), sizeof(double) * K);
         if (io->final_error) *io->final_error = tr.back();
@@ -2412,6 +2532,7 @@ int hgc_ifta_run_f64(const hgc_ifta_cfg* cfg, const hgc_slm* slm, const hgc_fres
 }
 
 int hgc_ospr_run_f64(const hgc_ospr_cfg* cfg, const hgc_slm* slm, int nx, int ny, hgc_ospr_io64* io) {
+    const auto t0 = std::chrono::steady_clock::now();
     return guarded([&] {
         validate_ospr_cfg(cfg);
         if (!io || !io->amplitude) invalid("TargetSpec: amplitude image is empty");
@@ -2454,7 +2575,9 @@ int hgc_ospr_run_f64(const hgc_ospr_cfg* cfg, const hgc_slm* slm, int nx, int ny
         SeedChunks ch;
         ch.plan_stream(n, 1);
         mt.alloc(ch.chunks);
+        PhaseClock pc(st, io->profile != nullptr);
         for (int k = 1; k <= N; ++k) {
+            pc.mark(3);
             const bool budget = cfg->variant == 1 && k > 1;  // ospr.hpp:106-116
             if (budget) k_ospr_amp64<<<ew_grid(n), 256, 0, st>>>(T.p, S.p, n, k, cfg->feedback_gain, amp.p);
             SeedArgs sa{};
@@ -2463,16 +2586,22 @@ int hgc_ospr_run_f64(const hgc_ospr_cfg* cfg, const hgc_slm* slm, int nx, int ny
             sa.out_stride = n;
             sa.npix = n;
             ch.launch_stream(sa, sd.p, mt.p, 1, k == 1, st);                              // seed_random_phase<double>
+            pc.mark(3);
             propagate64(f, none, nx, ny, +1, st);                                         // fft_inverse
+            pc.mark(0);
             k_quant64<<<ew_grid(n), 256, 0, st>>>(f.p, io->levels ? lv.p + n * (k - 1) : nullptr, n, q.q);
+            pc.mark(1);
             if (io->frames)
                 CK(cudaMemcpyAsync(io->frames + 2 * n * (k - 1), f.p, sizeof(double2) * n, cudaMemcpyDeviceToHost, st));
             CK(cudaMemcpyAsync(R.p, f.p, sizeof(double2) * n, cudaMemcpyDeviceToDevice, st));
+            pc.mark(3);
             propagate64(R, none, nx, ny, -1, st);                                         // fft_forward
+            pc.mark(0);
             k_ospr_acc64<<<ew_grid(n), 256, 0, st>>>(R.p, n, S.p);                        // ospr.hpp:134-137
             mse64(T.p, Mag64{R.p, nullptr, 0.0}, roi.p, n, M, cfg->freedom_scale, part, g, fm.p + (k - 1), st);
             mse64(T.p, Mag64{nullptr, S.p, (double)k}, roi.p, n, M, cfg->freedom_scale, part, g, cm.p + (k - 1), st);
             CK(cudaGetLastError());
+            pc.mark(2);
         }
         DBuf<double> mean;
         DBuf<double2> rep;
@@ -2487,6 +2616,8 @@ int hgc_ospr_run_f64(const hgc_ospr_cfg* cfg, const hgc_slm* slm, int nx, int ny
             CK(cudaMemcpyAsync(io->mean_intensity, mean.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
         if (io->replay) CK(cudaMemcpyAsync(io->replay, rep.p, sizeof(double2) * n, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
+        if (io->profile)
+            pc.report(std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(), io->profile);
         CK(cudaStreamDestroy(st));
         if (io->frame_mse) std::memcpy(io->frame_mse, hfm.data(), sizeof(double) * N);
         if (io->cumulative_mse) std::memcpy(io->cumulative_mse, hcm.data(), sizeof(double) * N);

@@ -192,17 +192,22 @@ __device__ __forceinline__ TW twiddle(const TW* __restrict__ tw, int m) {
     return w;
 }
 
-// x[r] *= w^r, w = exp(SIGN*2*pi*i*m/N), r = 1..R-1.  For R = 16 only w, w^4
-// and w^8 come from the table (the rest are <= 2 products of table values,
-// error <= ~2 ulp): 3 loads instead of 15 keeps the pass within the register
-// budget of a 1024-thread CTA (loading all 15 measured 10.1 vs 6.9 ms for
-// the 4096^2 row pass: the extra live values spill).
-template <int N, int SIGN, int R, class C2, class TW>
-__device__ __forceinline__ void apply_twiddles(C2* x, const TW* __restrict__ tw, int m) {
+// x[r] *= w^r, w = exp(SIGN*2*pi*i*k/S), r = 1..R-1, k < S/R (S = the pass's
+// span NS*R).  Every power a pass needs is read from the table of a shorter
+// length at the same index k: w^4 = W_{S/4}^k, w^8 = W_{S/8}^k (exact: the
+// table entries of W_S^{4k} and W_{S/4}^k are the same sincospi argument).  A
+// warp's 16 consecutive k then touch one 128-B line per load instead of up to
+// 16 (stride 4k / 8k in the length-S table).  For R = 16 only w, w^4 and w^8
+// are loaded (the rest are <= 2 products of table values, error <= ~2 ulp):
+// 3 loads instead of 15 keeps the pass within the register budget of a
+// 1024-thread CTA (loading all 15 measured 10.1 vs 6.9 ms for the 4096^2 row
+// pass: the extra live values spill).
+template <int S, int SIGN, int R, class C2, class TW>
+__device__ __forceinline__ void apply_twiddles(C2* x, const TW* __restrict__ tw, int k) {
     if constexpr (R == 16) {
-        const TW w1 = twiddle<N, SIGN>(tw, m);
-        const TW w4 = twiddle<N, SIGN>(tw, 4 * m);
-        const TW w8 = twiddle<N, SIGN>(tw, 8 * m);
+        const TW w1 = twiddle<S, SIGN>(tw, k);
+        const TW w4 = twiddle<S / 4, SIGN>(tw, k);
+        const TW w8 = twiddle<S / 8, SIGN>(tw, k);
         const TW w2 = cmul(w1, w1), w3 = cmul(w2, w1), w12 = cmul(w8, w4);
         x[1] = cmul(x[1], w1);
         x[2] = cmul(x[2], w2);
@@ -220,9 +225,9 @@ __device__ __forceinline__ void apply_twiddles(C2* x, const TW* __restrict__ tw,
         x[14] = cmul(x[14], cmul(w12, w2));
         x[15] = cmul(x[15], cmul(w12, w3));
     } else if constexpr (R == 8) {
-        const TW w1 = twiddle<N, SIGN>(tw, m);
-        const TW w2 = twiddle<N, SIGN>(tw, 2 * m);
-        const TW w4 = twiddle<N, SIGN>(tw, 4 * m);
+        const TW w1 = twiddle<S, SIGN>(tw, k);
+        const TW w2 = twiddle<S / 2, SIGN>(tw, k);
+        const TW w4 = twiddle<S / 4, SIGN>(tw, k);
         x[1] = cmul(x[1], w1);
         x[2] = cmul(x[2], w2);
         x[3] = cmul(x[3], cmul(w1, w2));
@@ -232,7 +237,7 @@ __device__ __forceinline__ void apply_twiddles(C2* x, const TW* __restrict__ tw,
         x[7] = cmul(x[7], cmul(w4, cmul(w1, w2)));
     } else {
 #pragma unroll
-        for (int r = 1; r < R; ++r) x[r] = cmul(x[r], twiddle<N, SIGN>(tw, r * m));
+        for (int r = 1; r < R; ++r) x[r] = cmul(x[r], twiddle<S, SIGN>(tw, r * k));
     }
 }
 
@@ -263,10 +268,10 @@ __device__ __forceinline__ float2 tw_apply(float2 a, Tw2 w) {
     if constexpr (SIGN < 0) return cmul_r(a, w.w, w.r);
     else return cmul_r(a, f2swap(w.r), f2swap(w.w));  // conj(w) and i*conj(w)
 }
-template <int N, int SIGN, int R>
-__device__ __forceinline__ void apply_twiddles(float2* x, const float2* __restrict__ tw, int m) {
+template <int S, int SIGN, int R>
+__device__ __forceinline__ void apply_twiddles(float2* x, const float2* __restrict__ tw, int k) {
     if constexpr (R == 16) {
-        const Tw2 w1 = tw_load<N>(tw, m), w4 = tw_load<N>(tw, 4 * m), w8 = tw_load<N>(tw, 8 * m);
+        const Tw2 w1 = tw_load<S>(tw, k), w4 = tw_load<S / 4>(tw, k), w8 = tw_load<S / 8>(tw, k);
         const Tw2 w2 = tw_mul(w1, w1), w3 = tw_mul(w2, w1), w12 = tw_mul(w8, w4);
         x[1] = tw_apply<SIGN>(x[1], w1);
         x[2] = tw_apply<SIGN>(x[2], w2);
@@ -284,7 +289,7 @@ __device__ __forceinline__ void apply_twiddles(float2* x, const float2* __restri
         x[14] = tw_apply<SIGN>(x[14], tw_mul(w12, w2));
         x[15] = tw_apply<SIGN>(x[15], tw_mul(w12, w3));
     } else if constexpr (R == 8) {
-        const Tw2 w1 = tw_load<N>(tw, m), w2 = tw_load<N>(tw, 2 * m), w4 = tw_load<N>(tw, 4 * m);
+        const Tw2 w1 = tw_load<S>(tw, k), w2 = tw_load<S / 2>(tw, k), w4 = tw_load<S / 4>(tw, k);
         const Tw2 w3 = tw_mul(w1, w2);
         x[1] = tw_apply<SIGN>(x[1], w1);
         x[2] = tw_apply<SIGN>(x[2], w2);
@@ -295,7 +300,7 @@ __device__ __forceinline__ void apply_twiddles(float2* x, const float2* __restri
         x[7] = tw_apply<SIGN>(x[7], tw_mul(w4, w3));
     } else {
 #pragma unroll
-        for (int r = 1; r < R; ++r) x[r] = tw_apply<SIGN>(x[r], tw_load<N>(tw, r * m));
+        for (int r = 1; r < R; ++r) x[r] = tw_apply<SIGN>(x[r], tw_load<S>(tw, r * k));
     }
 }
 
@@ -334,7 +339,7 @@ struct StockhamPass {
             for (int r = 0; r < R; ++r) x[r] = v[b + r * B];
             const int j = t + b * T;
             const int k = j & (NS - 1);
-            if constexpr (NS > 1) apply_twiddles<N, SIGN, R>(x, tw, k * (N / (NS * R)));
+            if constexpr (NS > 1) apply_twiddles<NS * R, SIGN, R>(x, tw, k);
             dft<R, SIGN>(x);
             if constexpr (last) {
 #pragma unroll

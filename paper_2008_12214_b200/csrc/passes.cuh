@@ -117,7 +117,14 @@ __device__ __forceinline__ void row_fused_body(float2 (&v)[LineCfg<NX>::E], int 
         const int i = rowbase + t + e * T;  // row-major pixel index (levels, Q, illumination)
         float2 f = cscale(v[e], norm);                        // fftw_backend.cpp:121-123
         if (hasq) f = cmul_conj_rn(f, __ldg(&fq[i]));         // propagation.hpp:93
+#ifndef HG_ROW_VARIANT  // diagnostic builds: 1 = no quantiser, 2 = no forward row transform
+#define HG_ROW_VARIANT 0
+#endif
+#if HG_ROW_VARIANT == 1
+        const int k = (__float_as_int(f.x) >> 20) & 255;
+#else
         const int k = quant_decide_kind<QK>(a.q, f.x, f.y, i);  // quantise.hpp:211-215
+#endif
         if constexpr (QK == QK_BINARY) f = k ? a.q.s1 : a.q.s0;
         else if constexpr (QK == QK_FULL) f = HG_STATES_SMEM ? sstates[k] : __ldg(&a.q.states[k]);  // phase mode, no illumination
         else f = quant_state(a.q, k, i);
@@ -128,7 +135,9 @@ __device__ __forceinline__ void row_fused_body(float2 (&v)[LineCfg<NX>::E], int 
         if (hasq) f = cmul_rn(f, __ldg(&fq[i]));              // propagation.hpp:85
         v[e] = f;
     }
+#if HG_ROW_VARIANT != 2
     fft_line<NX, -1>(v, t, smem, idx, a.tw, sync);  // starts the forward transform
+#endif
 }
 
 #ifndef HG_ROW_BULK
@@ -139,8 +148,9 @@ __device__ __forceinline__ void row_fused_body(float2 (&v)[LineCfg<NX>::E], int 
 // LV: level indices out — 0 never (compile time: the K-1 non-final iterations
 // carry no store code or index registers), 1 when a.levels8/16 is set, 2
 // decided at run time.
-template <int NX, int MODE, int QK, int LAY, int FQ, int LV = 2>
-__global__ void __launch_bounds__(RowCfg<NX, LAY>::THREADS, RowCfg<NX, LAY>::MIN_BLOCKS) k_row(RowArgs a) {
+// The row pass of one CTA: row block bx (RPC rows) of target by.
+template <int NX, int MODE, int QK, int LAY, int FQ, int LV>
+__device__ __forceinline__ void row_cta(const RowArgs& a, const int bx, const int by) {
     using Cfg = RowCfg<NX, LAY>;
     constexpr int E = Cfg::E, T = Cfg::T;
     extern __shared__ __align__(128) float2 smem[];
@@ -164,8 +174,8 @@ __global__ void __launch_bounds__(RowCfg<NX, LAY>::THREADS, RowCfg<NX, LAY>::MIN
     }
     // rows per CTA: the compile-time tile, or fewer when a launch would leave SMs idle
     const int RPCr = (LAY == LAY_QUAD && Cfg::RPC > 2 && a.rpc > 0) ? a.rpc : Cfg::RPC;
-    const int y = blockIdx.x * RPCr + lr;
-    const int b = blockIdx.y;
+    const int y = bx * RPCr + lr;
+    const int b = by;
     RowSmemIdx idx{lr * RowStride<NX>::value};
     const bool valid = y < a.ny;  // (ny is a multiple of RPC except for tiny fields)
     const int yy = valid ? y : 0;
@@ -197,9 +207,9 @@ __global__ void __launch_bounds__(RowCfg<NX, LAY>::THREADS, RowCfg<NX, LAY>::MIN
     }
     // (recomputed where used, so nothing extra stays live across the transforms)
     auto tile_bytes = [&] {
-        return (uint32_t)(min(RPCr, a.ny - (int)blockIdx.x * RPCr) * NX * (int)sizeof(float2));
+        return (uint32_t)(min(RPCr, a.ny - (int)bx * RPCr) * NX * (int)sizeof(float2));
     };
-    auto tile = [&] { return a.field + a.bstride * blockIdx.y + quad_index(0, blockIdx.x * RPCr, NX); };
+    auto tile = [&] { return a.field + a.bstride * by + quad_index(0, bx * RPCr, NX); };
     auto lbase = [&] { return (lr >> 1) * (2 * NX) + (t >> 1) * 4 + (lr & 1) * 2 + (t & 1); };
     if constexpr (kBulk) {
         if (threadIdx.x == 0) {
@@ -237,6 +247,10 @@ __global__ void __launch_bounds__(RowCfg<NX, LAY>::THREADS, RowCfg<NX, LAY>::MIN
             for (int e = 0; e < E; ++e) v[e] = cmul_conj_rn(v[e], __ldg(&a.fresnel_q[rowbase + t + e * T]));
     } else {
 #if !HG_NULL_COMPUTE  // diagnostic build: the passes' memory traffic alone
+#if HG_ROW_VARIANT == 3  // diagnostic: the aperture-plane work twice per tile (compute without tile traffic)
+#pragma unroll 1
+        for (int rep = 0; rep < 2; ++rep)
+#endif
         row_fused_body<NX, QK, FQ, LV>(v, t, y, b, valid, smem, idx, a, sstates);
 #endif
     }
@@ -259,6 +273,11 @@ __global__ void __launch_bounds__(RowCfg<NX, LAY>::THREADS, RowCfg<NX, LAY>::MIN
 #pragma unroll
         for (int e = 0; e < E; ++e) ob[addr(e)] = v[e];
     }
+}
+
+template <int NX, int MODE, int QK, int LAY, int FQ, int LV = 2>
+__global__ void __launch_bounds__(RowCfg<NX, LAY>::THREADS, RowCfg<NX, LAY>::MIN_BLOCKS) k_row(RowArgs a) {
+    row_cta<NX, MODE, QK, LAY, FQ, LV>(a, blockIdx.x, blockIdx.y);
 }
 
 // ------------------------------------------------------------- column pass
@@ -285,6 +304,8 @@ struct ColArgs {
     float clamp_lo, clamp_hi;
     int lt, lt_x0, lt_x1, lt_y0, lt_y1;
     int last;             // last iteration: store R, skip constraint + IFFT
+    int ckpt;             // with last: apply the constraint (+WGS weights) first and store the
+                          // constrained R (the state iteration K+1 resumes from)
     float2* replay_out;   // where the last iteration's R goes (may alias field)
     double* partials;     // per block: 8 doubles
     // OSPR accumulation
@@ -390,15 +411,16 @@ __device__ __forceinline__ void block_sum_float_store(float (&v)[NV], double* ou
     }
 }
 
+// The column pass of one CTA: column block bx (C columns) of target by, of
+// gx column blocks per target (the partial-sum slot).
 template <int NY, int C, int MODE, int LAY>
-__global__ void __launch_bounds__(LineCfg<NY, ColCfg<NY, LAY>::EM>::T * C, ColCfg<NY, LAY>::MIN_BLOCKS)
-    k_col(ColArgs a) {
+__device__ __forceinline__ void col_cta(const ColArgs& a, const int bx, const int by, const int gx) {
     constexpr int EM = ColCfg<NY, LAY>::EM;
     constexpr int E = LineCfg<NY, EM>::E, T = LineCfg<NY, EM>::T;
     extern __shared__ __align__(128) float2 smem[];
     const int c = threadIdx.x % C, t = threadIdx.x / C;
-    const int x = blockIdx.x * C + c;
-    const int b = blockIdx.y;
+    const int x = bx * C + c;
+    const int b = by;
     const int nx = a.nx;
     ColSmemIdx<C> idx{c};
     // element e of this thread is row y = t + e*T.  Field offsets: per-thread
@@ -433,7 +455,7 @@ __global__ void __launch_bounds__(LineCfg<NY, ColCfg<NY, LAY>::EM>::T * C, ColCf
     constexpr bool kTma = Tma::on;
     constexpr int kBoxRows = Tma::kBoxRows, kBoxes = NY / 2 / kBoxRows;
     __shared__ uint64_t tbar;
-    const int tq = blockIdx.x * (C / 2) * 8;  // inner coordinate (floats) of this column pair
+    const int tq = bx * (C / 2) * 8;  // inner coordinate (floats) of this column pair
     const int tr = a.tma_row0 + b * a.tma_brows;
     constexpr bool kTgt = ColTgtBulk<NY, C, LAY, MODE>::target;
     constexpr bool kSB = ColTgtBulk<NY, C, LAY, MODE>::S;
@@ -449,7 +471,7 @@ __global__ void __launch_bounds__(LineCfg<NY, ColCfg<NY, LAY>::EM>::T * C, ColCf
             if constexpr (kTgt || kSB) {
                 mbar_init(&gbar, 1);
                 const float* src = kTgt ? a.target + a.t_bstride * b : a.S + a.S_bstride * b;
-                bulk_g2s(tsm, src + colpair_index(blockIdx.x * C, 0, NY), (uint32_t)ColTgtBulk<NY, C, LAY, MODE>::BYTES,
+                bulk_g2s(tsm, src + colpair_index(bx * C, 0, NY), (uint32_t)ColTgtBulk<NY, C, LAY, MODE>::BYTES,
                          &gbar);
             }
         }
@@ -499,7 +521,7 @@ __global__ void __launch_bounds__(LineCfg<NY, ColCfg<NY, LAY>::EM>::T * C, ColCf
         const float norm = a.norm;
         const float* tg = a.target + a.t_bstride * b + sb;
         // target element e: from the bulk-loaded slice (same column-pair offsets) or global
-        const int tso = (int)(sb - colpair_index(blockIdx.x * C, 0, NY));
+        const int tso = (int)(sb - colpair_index(bx * C, 0, NY));
         if constexpr (kTgt) mbar_wait(&gbar, 0);
         auto tload = [&](int e) -> float {
             if constexpr (kTgt) return tsm[tso + e * ss];
@@ -512,7 +534,7 @@ __global__ void __launch_bounds__(LineCfg<NY, ColCfg<NY, LAY>::EM>::T * C, ColCf
         if constexpr (MODE == COL_GS_FAST || MODE == COL_WGS_FAST) {
             // GS/WGS, no ROI, phase freedom: mse partials (metrics.hpp:70-97) and
             // R <- amp * R/|R| (ifta.hpp:198-214), branch-free
-            const bool last = a.last;
+            const bool last = a.last && !a.ckpt;  // skip the constraint
             float* w = MODE == COL_WGS_FAST ? a.weights + a.t_bstride * b + sb : nullptr;
             const float lo = a.clamp_lo, hi = a.clamp_hi;
 #pragma unroll
@@ -559,7 +581,7 @@ __global__ void __launch_bounds__(LineCfg<NY, ColCfg<NY, LAY>::EM>::T * C, ColCf
                     acc[2] += r * r;
                     acc[3] += amp * amp;
                 }
-                if (!a.last) {  // replay-plane constraint, ifta.hpp:190-223
+                if (!a.last || a.ckpt) {  // replay-plane constraint, ifta.hpp:190-223
                     if (in_roi) {
                         const bool active = !a.lt || (x >= a.lt_x0 && x < a.lt_x1 && y >= a.lt_y0 && y < a.lt_y1);
                         if (active) {
@@ -623,12 +645,12 @@ __global__ void __launch_bounds__(LineCfg<NY, ColCfg<NY, LAY>::EM>::T * C, ColCf
                 store_col(base);
             }
         }
-        const size_t blk = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
+        const size_t blk = (size_t)by * gx + bx;
         if constexpr (kSB) {  // the updated S slice back to HBM in one bulk store
             fence_proxy_async();
             __syncthreads();
             if (threadIdx.x == 0) {
-                bulk_s2g(a.S + a.S_bstride * b + colpair_index(blockIdx.x * C, 0, NY), tsm,
+                bulk_s2g(a.S + a.S_bstride * b + colpair_index(bx * C, 0, NY), tsm,
                          (uint32_t)ColTgtBulk<NY, C, LAY, MODE>::BYTES);
                 bulk_commit();
                 bulk_wait_read0();
@@ -636,6 +658,12 @@ __global__ void __launch_bounds__(LineCfg<NY, ColCfg<NY, LAY>::EM>::T * C, ColCf
         }
         block_sum_float_store<NV>(acc, a.partials + blk * 8);
     }
+}
+
+template <int NY, int C, int MODE, int LAY>
+__global__ void __launch_bounds__(LineCfg<NY, ColCfg<NY, LAY>::EM>::T * C, ColCfg<NY, LAY>::MIN_BLOCKS)
+    k_col(ColArgs a) {
+    col_cta<NY, C, MODE, LAY>(a, blockIdx.x, blockIdx.y, gridDim.x);
 }
 
 }  // namespace hg

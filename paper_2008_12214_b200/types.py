@@ -303,6 +303,7 @@ class RunReport:  # report.hpp:48-65 (+ levels: the hologram's level indices)
     accepted: int = 0
     decisions: list = field(default_factory=list)
     levels: np.ndarray | None = None
+    weights: np.ndarray | None = None  # WGS weights of a checkpointed run (run_ifta(..., checkpoint=True))
 
 
 @dataclass

@@ -64,6 +64,16 @@ int main() {
     std::printf("gs binary 128^2: level mismatches %d, mse %.9g vs %.9g (rel %.2e)\n", mm, gpu.final_error,
                 ref.final_error, rel);
     CHECK(mm <= 4 && rel < 1e-4 && gpu.trace.size() == 20 && gpu.algorithm == "gs");
+    // RunReport::profile: every phase attributed, the total is the run
+    // (test_ifta.cpp:270-280 "profile accounts for the whole run"; bench.cpp:167-183)
+    auto profile_ok = [](const auto& r) {
+        const auto& q = r.profile;
+        std::printf("  profile transform %.3g constraint %.3g metric %.3g other %.3g of %.3g s\n", q.transform,
+                    q.constraint, q.metric, q.other, r.seconds);
+        return q.transform > 0.0 && q.constraint > 0.0 && q.metric > 0.0 && q.other >= 0.0 && r.seconds > 0.0 &&
+               std::abs(q.total() - r.seconds) <= 1e-9 * r.seconds;
+    };
+    CHECK(profile_ok(gpu));
 
     // WGS 256-level with a Fresnel propagator (lock-step not needed at 3 iterations)
     FresnelParams p{532e-9, 0.1, 8e-6, 8e-6};
@@ -106,6 +116,7 @@ int main() {
         double rel64 = std::abs(gd.final_error - rd.final_error) / rd.final_error;
         std::printf("gs<double> binary 128^2: level mismatches %d, mse rel %.2e\n", m, rel64);
         CHECK(m == 0 && rel64 < 1e-9);
+        CHECK(profile_ok(gd));
         auto p64 = Propagator<double>::fresnel(128, 128, p);
         IftaConfig wd = w;
         wd.iterations = 2;
@@ -119,6 +130,7 @@ int main() {
         rel64 = std::abs(go64.report.final_error - ro64.report.final_error) / ro64.report.final_error;
         std::printf("ospr<double> 6 frames: cumulative mse rel %.2e\n", rel64);
         CHECK(rel64 < 1e-9 && go64.set.frames.size() == 6);
+        CHECK(profile_ok(go64.report));
     }
 
     // the runner's batch pool (runner.cpp:387-421): one job per host thread,

@@ -23,7 +23,7 @@ def test_header_symbols_exported():
     for s in syms:
         assert hasattr(_lib.lib, s), s
     assert set(syms) <= set(_lib.exported_symbols()) | {"hgc_ifta_plan_profile", "hgc_ospr_plan_profile"}
-    assert _lib.lib.hgc_abi_version() == 4 and _lib.lib.hgc_max_side() == 4096
+    assert _lib.lib.hgc_abi_version() == _lib.ABI_VERSION == 5 and _lib.lib.hgc_max_side() == 4096
 
 
 def test_fork_seed_matches_reference_rng():

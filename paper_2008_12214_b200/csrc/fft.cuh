@@ -308,6 +308,11 @@ __device__ __forceinline__ void apply_twiddles(float2* x, const float2* __restri
 struct CtaSync {
     __device__ __forceinline__ void operator()() const { __syncthreads(); }
 };
+// Barrier of one thread group of a CTA (named barrier `id`, `n` threads).
+struct GroupSync {
+    int id, n;
+    __device__ __forceinline__ void operator()() const { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+};
 
 // Exchange-buffer slot access (one element per slot).
 template <class C2, class I>

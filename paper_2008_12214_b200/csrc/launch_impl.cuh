@@ -44,6 +44,47 @@ inline void row_launch(const RowArgs& a, int batch, cudaStream_t st, bool prepar
     CK(cudaGetLastError());
 }
 
+// Persistent pipelined row pass (k_row_persist): one 1024-thread CTA per SM
+// over all (row block, target) tiles.  Used for the large fused launches
+// (>= 2 tiles per SM); returns false when it does not apply.
+inline bool row_persist_on() {
+    static const bool on = [] {
+        const char* e = getenv("HG_ROW_PERSIST");
+        return e ? atoi(e) != 0 : true;
+    }();
+    return on;
+}
+template <int NX, int QK, int FQ, int LV>
+inline bool row_persist_launch(const RowArgs& a, int batch, cudaStream_t st, bool prepare) {
+    if constexpr (!RowPersistCfg<NX>::ok) {
+        return false;
+    } else {
+        using Cfg = RowCfg<NX, LAY_QUAD>;
+        auto kern = k_row_persist<NX, QK, FQ, LV>;
+        if (prepare) {
+            set_smem(kern, RowPersistCfg<NX>::SMEM);
+            return true;
+        }
+        if (!row_persist_on() || a.ny % Cfg::RPC != 0) return false;
+        const int rowblocks = a.ny / Cfg::RPC;
+        const long long ntiles = (long long)rowblocks * batch;
+        const int sms = sm_count();
+        if (ntiles < 2LL * sms || ntiles > (1LL << 30)) return false;
+        kern<<<sms, 1024, RowPersistCfg<NX>::SMEM, st>>>(a, rowblocks, (int)ntiles);
+        CK(cudaGetLastError());
+        return true;
+    }
+}
+template <int QK, int FQ, int LV>
+inline bool row_persist_dispatch(int nx, const RowArgs& a, int batch, cudaStream_t st, bool prepare) {
+    switch (nx) {
+        case 1024: return row_persist_launch<1024, QK, FQ, LV>(a, batch, st, prepare);
+        case 2048: return row_persist_launch<2048, QK, FQ, LV>(a, batch, st, prepare);
+        case 4096: return row_persist_launch<4096, QK, FQ, LV>(a, batch, st, prepare);
+        default: return false;
+    }
+}
+
 // Which specialised quantiser a fused row pass can use (quant.cuh).
 inline int quant_kind(const QuantParams& q) {
     const bool illum = q.illum_arg || q.illum || q.illum_unit;
@@ -88,6 +129,46 @@ inline void col_launch_c(const ColArgs& a, int batch, cudaStream_t st, bool prep
     dim3 grid(a.nx / C, batch);
     kern<<<grid, LineCfg<NY, EM>::T * C, smem, st>>>(a);
     CK(cudaGetLastError());
+}
+
+// Persistent pipelined GS / WGS column pass (k_col_persist), as the row pass.
+inline bool col_persist_on() {
+    static const bool on = [] {
+        const char* e = getenv("HG_COL_PERSIST");  // (off by default: measured slower)
+        return e ? atoi(e) != 0 : false;
+    }();
+    return on;
+}
+template <int NY, int MODE>
+inline bool col_persist_launch(const ColArgs& a, int batch, cudaStream_t st, bool prepare) {
+    if constexpr (!ColPersistCfg<NY>::ok || (MODE != COL_GS_FAST && MODE != COL_WGS_FAST)) {
+        return false;
+    } else {
+        constexpr int C = ColPersistCfg<NY>::C;
+        auto kern = k_col_persist<NY, MODE>;
+        if (prepare) {
+            set_smem(kern, ColPersistCfg<NY>::SMEM);
+            return true;
+        }
+        if (!col_persist_on() || !a.tmap || a.layout != LAY_QUAD || (a.cw > 0 && a.cw != C) || a.nx % C != 0)
+            return false;
+        const int colblocks = a.nx / C;
+        const long long ntiles = (long long)colblocks * batch;
+        const int sms = sm_count();
+        if (ntiles < 2LL * sms || ntiles > (1LL << 30)) return false;
+        kern<<<sms, 1024, ColPersistCfg<NY>::SMEM, st>>>(a, colblocks, (int)ntiles);
+        CK(cudaGetLastError());
+        return true;
+    }
+}
+template <int MODE>
+inline bool col_persist_dispatch(int ny, const ColArgs& a, int batch, cudaStream_t st, bool prepare) {
+    switch (ny) {
+        case 1024: return col_persist_launch<1024, MODE>(a, batch, st, prepare);
+        case 2048: return col_persist_launch<2048, MODE>(a, batch, st, prepare);
+        case 4096: return col_persist_launch<4096, MODE>(a, batch, st, prepare);
+        default: return false;
+    }
 }
 
 template <int NY, int MODE, int LAY>

@@ -5,16 +5,21 @@
 Workload (BASELINE config 5, the largest single-GPU config): batch GS,
 4096x4096, 256-level full-circle phase SLM, K = 25 iterations (reference
 default, config.hpp:35), smooth_blobs + UnitEnergy targets (the reference's
-bench target, bench.cpp:115-116), target t seeded with 1 + t.  One step = one
+bench target, bench.cpp:115-116), target t seeded with 1 + t.  The 64 targets
+(--total-targets) are sharded over the GPUs: one step = one
 full batched run per GPU (random-phase init + K iterations + trace reduction)
-of `--targets` targets; value = target-iterations per second over all GPUs.
+of its shard; value = target-iterations per second over all GPUs ("strong":
+the total is fixed).  --targets T instead runs T targets per GPU ("weak").
 OSPR (config 3: 1024^2 binary, 24 subframes) is reported in the "ospr" object.
 
   python bench.py [--gpus N --steps K --warmup W]          ours
   python bench.py --impl reference [...]                  reference CPU path
 
-Multi-GPU: one process per GPU (torchrun); whole targets per GPU, no
-data-path collective; NCCL only gathers the per-target final errors.
+Multi-GPU: one process per GPU.  Under torchrun the world comes from
+WORLD_SIZE (and must equal --gpus); a bare `bench.py --gpus N` re-launches
+itself under torch.distributed.run with N ranks.  Whole targets per GPU, no
+data-path collective; after the timed steps NCCL gathers every target's
+levels and MSE trace to rank 0 (cmd_batch's result set).
 """
 from __future__ import annotations
 
@@ -28,6 +33,7 @@ import subprocess
 import sys
 import threading
 import time
+from types import SimpleNamespace
 
 import numpy as np
 
@@ -55,7 +61,12 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n", type=int, default=4096)
     ap.add_argument("--levels", type=int, default=256)
-    ap.add_argument("--targets", type=int, default=64, help="targets per GPU per step")
+    ap.add_argument("--total-targets", type=int, default=64,
+                    help="targets per step over all GPUs, sharded (BASELINE config 5: 64)")
+    ap.add_argument("--targets", type=int, default=None,
+                    help="targets per GPU per step instead (weak scaling); default: --total-targets sharded")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="exercise the launch / sharding / gather plumbing only (gloo, no GPU work)")
     ap.add_argument("--iters", type=int, default=25)
     ap.add_argument("--ospr-n", type=int, default=1024)
     ap.add_argument("--ospr-jobs", type=int, default=148, help="OSPR jobs per GPU per step (one MT stream per SM)")
@@ -68,16 +79,20 @@ def parse():
 
 # ----------------------------------------------------------- distributed
 class Dist:
-    def __init__(self, collectives: bool = True):
+    def __init__(self, collectives: bool = True, backend: str = "nccl"):
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
+        self.device = "cuda" if backend == "nccl" else "cpu"
         if self.world > 1 and collectives:
             import torch
             import torch.distributed as dist
-            torch.cuda.set_device(self.local)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            if backend == "nccl":
+                torch.cuda.set_device(self.local)
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            else:
+                dist.init_process_group(backend)
             self.pg = dist
 
     def barrier(self):
@@ -88,19 +103,9 @@ class Dist:
         if not self.pg:
             return v
         import torch
-        t = torch.tensor([v], device="cuda", dtype=torch.float64)
+        t = torch.tensor([v], device=self.device, dtype=torch.float64)
         self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
         return float(t.item())
-
-    def gather_errors(self, errs_dev):
-        """NCCL gather of per-target final errors to rank 0 (the only
-        collective of the sharded path)."""
-        if not self.pg:
-            return errs_dev
-        import torch
-        out = [torch.empty_like(errs_dev) for _ in range(self.world)] if self.rank == 0 else None
-        self.pg.gather(errs_dev, out, dst=0)
-        return torch.cat(out) if self.rank == 0 else None
 
     def close(self):
         if self.pg:
@@ -152,14 +157,40 @@ class Clocks:
 
 
 # --------------------------------------------------------------- GS (ours)
+def shard_of(args, d: Dist):
+    """This rank's targets: a contiguous block of --total-targets (strong
+    scaling, BASELINE config 5 sharded over the GPUs) or --targets per GPU."""
+    from paper_2008_12214_b200.shard import shard_range
+    if args.targets:
+        return d.rank * args.targets, args.targets, args.targets * d.world, "weak"
+    first, count = shard_range(args.total_targets, d.world, d.rank)
+    return first, count, args.total_targets, "strong"
+
+
+def timed_steps(plan, stream, steps):
+    """Back-to-back graph launches with an event pair around each: total ms and
+    the per-step times (for the dispersion)."""
+    import torch
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    torch.cuda.synchronize()
+    ev[0].record(stream)
+    for i in range(steps):
+        plan.execute(stream.cuda_stream)
+        ev[i + 1].record(stream)
+    torch.cuda.synchronize()
+    per = [ev[i].elapsed_time(ev[i + 1]) for i in range(steps)]
+    return ev[0].elapsed_time(ev[-1]), per
+
+
 def gs_ours(args, d: Dist):
     import torch
     import paper_2008_12214_b200 as hg
-    from paper_2008_12214_b200 import _lib
-    n, B, K = args.n, args.targets, args.iters
+    from paper_2008_12214_b200.shard import gather_batch_results, unit_seeds
+    n, K = args.n, args.iters
+    first, B, total, scaling = shard_of(args, d)
     hg.set_device(d.local)
     amp1 = hg.patterns.bench_target(n)
-    seeds = np.arange(1 + d.rank * B, 1 + (d.rank + 1) * B, dtype=np.uint64)
+    seeds = unit_seeds(first, B)
     slm = hg.SlmSpec.full_circle_phase(args.levels) if args.levels > 2 else hg.SlmSpec.binary_phase()
     cfg = hg.IftaConfig(iterations=K, slm=slm, target=hg.TargetSpec(amp1))
     npix = n * n
@@ -174,36 +205,37 @@ def gs_ours(args, d: Dist):
         plan.execute(stream.cuda_stream)
     torch.cuda.synchronize()
     d.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(d.local) as clk:
-        torch.cuda.synchronize()
-        e0.record(stream)
-        for _ in range(args.steps):
-            plan.execute(stream.cuda_stream)
-        e1.record(stream)
-        torch.cuda.synchronize()
+        ms, per_step = timed_steps(plan, stream, args.steps)
     d.barrier()
-    ms = e0.elapsed_time(e1)
     ms_max = d.max(ms)
     launches = plan.launches() * args.steps
-    # result check + the sharded path's only collective: gather final errors
-    _, _, tr = plan.device_arrays()
+    # rank 0 gathers every target's levels and MSE trace (NCCL), after the timed steps
+    _, lv, tr = plan.device_arrays()
+    levels = torch.as_tensor(lv, device="cuda")
     trace = torch.as_tensor(tr, device="cuda")
-    finals = d.gather_errors(trace[:, -1].contiguous())
-    ok = bool(torch.isfinite(trace).all().item() and (trace[:, -1] < trace[:, 0]).all().item())
+    got = gather_batch_results(levels, trace, d.pg, d.world, d.rank, total)
+    check = None
+    if got is not None:
+        glv, gtr = got
+        check = {"gathered_targets": int(gtr.shape[0]), "gathered_level_bytes": int(glv.numel() * glv.element_size()),
+                 "traces_finite_and_decreasing": bool(torch.isfinite(gtr).all().item()
+                                                      and (gtr[:, -1] < gtr[:, 0]).all().item()),
+                 "final_mse_mean": float(gtr[:, -1].mean().item()),
+                 "levels_checksum": int(glv.to(torch.int64).sum().item())}
     kt = plan.kernel_times()  # the last timed step's passes, measured inside its graph
     prof = plan.profile(reps=5)
     prof["graph_row"], prof["graph_col"] = kt["row"], kt["col"]
-    prof["iteration_in_graph"] = in_graph_iteration_ms(args, plan, amps, seeds, stream, ms / args.steps)
-    res = {"ms": ms_max, "launches": launches, "clocks": clk.summary(), "profile_ms": prof, "check_ok": ok,
-           "final_mse_mean": float(finals.mean().item()) if finals is not None else None, "npix": npix, "B": B}
+    prof["iteration_in_graph"] = in_graph_iteration_ms(args, plan, amps, seeds, stream, ms / args.steps, B)
+    res = {"ms": ms_max, "per_step_ms": per_step, "launches": launches, "clocks": clk.summary(),
+           "profile_ms": prof, "check": check, "npix": npix, "B": B, "total": total, "scaling": scaling}
     if not args.no_e2e:
-        res["e2e"] = gs_e2e(args, plan, amps, seeds, d)
+        res["e2e"] = gs_e2e(args, plan, amps, seeds, d, total)
     plan.close()
     return res
 
 
-def in_graph_iteration_ms(args, plan, amps, seeds, stream, ms_step):
+def in_graph_iteration_ms(args, plan, amps, seeds, stream, ms_step, B):
     """Per-iteration device time inside the real launch sequence: the same
     batch run with K1 = K/5 iterations, timed like the step, and
     (t(K) - t(K1)) / (K - K1); init, seed and trace reduction cancel."""
@@ -214,7 +246,7 @@ def in_graph_iteration_ms(args, plan, amps, seeds, stream, ms_step):
     if K - K1 < 4:
         return None
     cfg = hg.IftaConfig(iterations=K1, slm=plan.cfg.slm, target=plan.cfg.target)
-    p1 = hg.IftaPlan(cfg, args.n, args.n, args.targets)
+    p1 = hg.IftaPlan(cfg, args.n, args.n, B)
     p1.upload(amps.numpy(), seeds=seeds)
     p1.execute(stream.cuda_stream)
     torch.cuda.synchronize()
@@ -229,7 +261,7 @@ def in_graph_iteration_ms(args, plan, amps, seeds, stream, ms_step):
     return (ms_step - t1) / (K - K1)
 
 
-def gs_e2e(args, plan, amps, seeds, d: Dist):
+def gs_e2e(args, plan, amps, seeds, d: Dist, total: int):
     """Same metric through the C ABI with host buffers.  Every step uploads
     that step's targets from pinned memory (H2D, validated on the device),
     runs, and reads back the levels and the MSE traces (D2H).  Two plans are
@@ -238,7 +270,7 @@ def gs_e2e(args, plan, amps, seeds, d: Dist):
     import torch
     import paper_2008_12214_b200 as hg
     from paper_2008_12214_b200 import _lib
-    B, n, K = args.targets, args.n, args.iters
+    B, n, K = plan.batch, args.n, args.iters
     plan2 = hg.IftaPlan(plan.cfg, n, n, B)
     plans = [plan, plan2]
     lvs = [torch.empty((B, n, n), dtype=torch.uint8, pin_memory=True) for _ in range(2)]
@@ -275,7 +307,7 @@ def gs_e2e(args, plan, amps, seeds, d: Dist):
     dt = d.max(time.perf_counter() - t0)
     ok = bool(np.isfinite(trs[0]).all() and (trs[0][:, -1] < trs[0][:, 0]).all())
     plan2.close()
-    units = d.world * B * K * steps
+    units = total * K * steps
     return {"value": units / dt, "unit": "iterations/s", "h2d_bytes_per_step": int(B * n * n * 8 + B * 8),
             "d2h_bytes_per_step": int(B * n * n + B * K * 8), "steps": steps, "check_ok": ok,
             "api": "hgc_ifta_plan_upload/execute/download (C ABI, pinned host buffers, two plans double-buffered)"}
@@ -438,36 +470,43 @@ def single_target_configs(args, d: Dist, peak: float):
 
 
 # ---------------------------------------------------- reference CPU path
-def reference_gs(n, levels, iters, jobs, threads):
-    """The reference's own run_ifta<float> (oracle/_ref: unmodified headers,
-    substitute f32 FFT since FFTW is absent), `jobs` independent targets on
-    `threads` host threads (cmd_batch's job pool, runner.cpp:388-421)."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    from pyoracle import Oracle
-    import paper_2008_12214_b200.patterns as pat
-    from paper_2008_12214_b200.types import SlmSpec
-    ref = Oracle("reference")
-    ref.set_fast_fft(True)
-    amp = pat.bench_target(n)
-    slm = SlmSpec.full_circle_phase(levels) if levels > 2 else SlmSpec.binary_phase()
-    t0 = time.perf_counter()
-    with cf.ThreadPoolExecutor(max_workers=threads) as ex:
-        list(ex.map(lambda s: ref.ifta(amp, slm, iters, seed=int(s)), range(1, jobs + 1)))
-    return time.perf_counter() - t0
+# The reference's own run_ifta<float> / run_ospr (oracle/_ref/libhgref.so: its
+# unmodified headers compiled here; a substitute f32 FFT since FFTW is absent
+# on these hosts).  Nothing from the product package is imported on this path:
+# the target comes from the reference's patterns::smooth_blobs +
+# normalize_image (UnitEnergy), the SLM is a plain SlmSpec record.
+TWO_PI = 6.283185307179586476925286766559
 
 
-def reference_ospr(n, subframes, jobs, threads):
+def ref_oracle():
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     from pyoracle import Oracle
-    import paper_2008_12214_b200.patterns as pat
-    from paper_2008_12214_b200.types import SlmSpec
     ref = Oracle("reference")
-    ref.set_fast_fft(True)
-    amp = pat.bench_target(n)
-    t0 = time.perf_counter()
-    with cf.ThreadPoolExecutor(max_workers=threads) as ex:
-        list(ex.map(lambda s: ref.ospr(amp, SlmSpec.binary_phase(), subframes, seed=int(s)), range(1, jobs + 1)))
-    return time.perf_counter() - t0
+    ref.set_fast_fft(True)  # the substitute's fast f32 path (FFTW stand-in); labelled in `sample`
+    return ref
+
+
+def ref_slm(levels):
+    """SlmSpec::full_circle_phase(L) / binary_phase() (quantise.hpp:33-58)."""
+    if levels > 2:
+        return SimpleNamespace(mode=1, levels=levels, min_arg=0.0, max_arg=TWO_PI, full_circle=True, min_amp=0.0,
+                               max_amp=1.0, illumination=None)
+    return SimpleNamespace(mode=1, levels=2, min_arg=0.0, max_arg=TWO_PI / 2, full_circle=False, min_amp=0.0,
+                           max_amp=1.0, illumination=None)
+
+
+def ref_target(ref, n):
+    return ref.normalize(ref.smooth_blobs(n, n), True)  # patterns.hpp:55-80, target.hpp:15-30
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 def cpu_threads():
@@ -477,64 +516,179 @@ def cpu_threads():
         return os.cpu_count() or 1
 
 
-def base_config(args, d):
+def ref_gs_batch(ref, amp, slm, K, jobs, threads):
+    """`jobs` independent run_ifta<float> jobs (seeds 1..jobs) on `threads` host
+    threads (cmd_batch's job pool, runner.cpp:388-421); wall seconds + reports."""
+    t0 = time.perf_counter()
+    with cf.ThreadPoolExecutor(max_workers=threads) as ex:
+        reps = list(ex.map(lambda sd: ref.ifta(amp, slm, K, seed=int(sd)), range(1, jobs + 1)))
+    return time.perf_counter() - t0, reps
+
+
+def ref_gs_throughput(ref, n, levels, K_run, threads, k_lo=1, k_hi=3):
+    """All-core throughput of the reference GS on a bounded sample (BASELINE.md
+    §3): one job per host thread, each timed at k_lo and k_hi iterations.  The
+    difference gives the per-iteration cost and the rest the per-job init
+    (random-phase seed); `value` is the K_run-iteration job rate they imply,
+    i.e. the same target-iterations/s the GPU line reports (init included)."""
+    amp, slm = ref_target(ref, n), ref_slm(levels)
+    t_lo, _ = ref_gs_batch(ref, amp, slm, k_lo, threads, threads)
+    t_hi, reps = ref_gs_batch(ref, amp, slm, k_hi, threads, threads)
+    t_it = max(t_hi - t_lo, 1e-9) / (k_hi - k_lo)  # wall per iteration of the whole job pool
+    t_init = max(t_lo - k_lo * t_it, 0.0)
+    value = threads * K_run / (K_run * t_it + t_init)
+    return {"value": value, "per_iteration_rate": threads / t_it, "init_s_per_job_pool": t_init,
+            "wall_s": t_lo + t_hi, "jobs": threads, "k": [k_lo, k_hi],
+            "check_ok": all(np.isfinite(r.trace).all() for r in reps)}
+
+
+def ref_gs_single_core(ref, n, levels, K=3):
+    """One job on one thread, K iterations: the reference's own RunReport
+    seconds and PhaseProfile (report.hpp:38-65) — seconds per iteration =
+    (transform + constraint + metric) / K; the rest ("other") is the init."""
+    r = ref.ifta(ref_target(ref, n), ref_slm(levels), K, seed=1)
+    tr, cn, me, ot = r.profile
+    return {"seconds_per_iteration": (tr + cn + me) / K, "iterations_per_s": K / (tr + cn + me),
+            "run_seconds": r.seconds, "init_and_other_s": ot, "iterations": K,
+            "profile": {"transform": tr, "constraint": cn, "metric": me, "other": ot}}
+
+
+def ref_ospr_throughput(ref, n, subframes, threads):
+    amp, slm = ref_target(ref, n), ref_slm(2)
+    t0 = time.perf_counter()
+    with cf.ThreadPoolExecutor(max_workers=threads) as ex:
+        list(ex.map(lambda sd: ref.ospr(amp, slm, subframes, seed=int(sd)), range(1, threads + 1)))
+    return threads * subframes / (time.perf_counter() - t0)
+
+
+def base_config(args, d, total, scaling):
+    per = args.targets if args.targets else f"{total} sharded over {d.world} GPU(s) (shard_range)"
     return {"workload": f"batch_gs_{args.n}_{args.levels}level (BASELINE config 5)", "resolution": args.n,
-            "levels": args.levels, "iterations": args.iters, "targets_per_gpu": args.targets,
-            "total_targets": args.targets * d.world, "seeds": "1 + target index",
-            "target": "smooth_blobs + UnitEnergy (bench.cpp:115-116)",
+            "levels": args.levels, "iterations": args.iters, "total_targets": total, "targets_per_gpu": per,
+            "seeds": "1 + target index", "target": "smooth_blobs + UnitEnergy (bench.cpp:115-116)",
+            "scaling": scaling,
             "l2": "inputs larger than L2 (per GPU: targets x 128 MiB field + 64 MiB fp32 target)"}
 
 
 def run_reference(args, d: Dist):
+    """--impl reference: the reference's own CPU path on this host's cores,
+    rank 0 only, on the same config / metric as our arm (bounded samples)."""
     if d.rank != 0:
         d.close()
         return
+    ref = ref_oracle()
     threads = cpu_threads()
-    jobs, iters = threads, 1
+    total = args.targets * d.world if args.targets else args.total_targets
     for _ in range(args.warmup):
-        reference_gs(args.n, args.levels, iters, jobs, threads)
-    times = [reference_gs(args.n, args.levels, iters, jobs, threads) for _ in range(args.steps)]
-    t = sum(times)
-    value = jobs * iters * args.steps / t
-    sample = (f"{jobs} jobs x {iters} iteration (incl. random-phase init) of GS {args.n}^2 {args.levels}-level per "
-              f"step, one job per host thread; reference headers + substitute f32 FFT (FFTW absent)")
+        ref_gs_throughput(ref, args.n, args.levels, args.iters, threads, 1, 2)
+    runs = [ref_gs_throughput(ref, args.n, args.levels, args.iters, threads) for _ in range(args.steps)]
+    vals = [r["value"] for r in runs]
+    value = statistics.mean(vals)
+    single = ref_gs_single_core(ref, args.n, args.levels)
+    sample = (f"per step: {threads} concurrent jobs (one per host thread) of GS {args.n}^2 {args.levels}-level at "
+              f"1 and 3 iterations; per-iteration cost = difference, init = remainder; value = the "
+              f"{args.iters}-iteration job rate they imply; reference headers unmodified + substitute f32 FFT "
+              f"(FFTW absent); CPU {cpu_model()}")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": d.world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": base_config(args, d),
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(r["wall_s"] for r in runs),
+            "value_sigma": statistics.stdev(vals) if len(vals) > 1 else 0.0,
+            "higher_is_better": True, "scaling": "strong" if not args.targets else "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": base_config(args, d, total, "strong" if not args.targets else "weak"),
+            "product_package_imported": "paper_2008_12214_b200" in sys.modules,
             "cpu_baseline": {"value": value, "unit": "iterations/s", "cores": threads, "kind": "reference",
-                             "sample": sample},
+                             "sample": sample, "cpu_model": cpu_model(), "single_core": single,
+                             "per_iteration_rate_all_cores": statistics.mean(r["per_iteration_rate"] for r in runs)},
             "e2e": {"value": value, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     d.close()
 
 
+def relaunch_if_needed(args):
+    """--gpus N without torchrun: re-run this command under
+    torch.distributed.run with N ranks (127.0.0.1 rendezvous).  Under torchrun
+    WORLD_SIZE must equal --gpus."""
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is not None:
+        if int(ws) != args.gpus:
+            print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={ws}"}), flush=True)
+            sys.exit(2)
+        return
+    if args.gpus <= 1:
+        return
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
+
+
+def dry_run(args):
+    """The multi-GPU plumbing without GPU work (gloo): world size, target
+    shards, and the rank-0 gather of per-target levels + traces."""
+    import torch
+    from paper_2008_12214_b200.shard import gather_batch_results
+    d = Dist(backend="gloo")
+    first, B, total, scaling = shard_of(args, d)
+    lv = torch.full((B, 4, 4), d.rank, dtype=torch.uint8)
+    tr = torch.arange(first, first + B, dtype=torch.float64)[:, None].repeat(1, args.iters)
+    got = gather_batch_results(lv, tr, d.pg, d.world, d.rank, total)
+    if d.rank == 0:
+        order_ok = bool((got[1][:, 0] == torch.arange(total, dtype=torch.float64)).all().item())
+        print(json.dumps({"dry_run": True, "metric": METRIC, "value": None, "n_gpus": d.world, "scaling": scaling,
+                          "config": base_config(args, d, total, scaling),
+                          "shards": [list(__import__("paper_2008_12214_b200.shard", fromlist=["x"]).shard_range(
+                              total, d.world, r)) for r in range(d.world)] if not args.targets else None,
+                          "gathered_targets": int(got[1].shape[0]), "gather_in_target_order": order_ok}), flush=True)
+    d.close()
+
+
 def main():
     args = parse()
+    relaunch_if_needed(args)
+    if args.dry_run:
+        return dry_run(args)
     if args.impl == "reference":  # rank 0 alone works on the host cores: no process group needed
         return run_reference(args, Dist(collectives=False))
     d = Dist()
     peak, peak_kind = peaks()
     gs = gs_ours(args, d)
+    weak = None
+    if d.world > 1 and not args.targets:  # secondary line: 64 targets on EVERY GPU (weak scaling)
+        wa = argparse.Namespace(**{**vars(args), "targets": args.total_targets, "no_e2e": True})
+        w = gs_ours(wa, d)
+        weak = {"value": w["total"] * args.iters * args.steps / (w["ms"] / 1e3), "unit": "iterations/s",
+                "targets_per_gpu": args.total_targets, "ms_per_step": w["ms"] / args.steps, "scaling": "weak"}
     osp = None if args.no_ospr else ospr_ours(args, d)
     single = None if args.no_ospr else ospr_single_job(args, d)
     singles = single_target_configs(args, d, peak) if d.rank == 0 and not args.no_ospr else None
     cpu = None
     if d.rank == 0 and d.world == 1 and not args.no_cpu:
+        ref = ref_oracle()
         threads = cpu_threads()
-        t = reference_gs(args.n, args.levels, 1, threads, threads)
-        cpu = {"value": threads / t, "unit": "iterations/s", "cores": threads, "kind": "reference",
-               "sample": f"{threads} concurrent jobs x 1 iteration (+init) of GS {args.n}^2 {args.levels}-level, "
-                         f"reference headers + substitute f32 FFT (FFTW absent), one job per host thread"}
+        r = ref_gs_throughput(ref, args.n, args.levels, args.iters, threads)
+        cpu = {"value": r["value"], "unit": "iterations/s", "cores": threads, "kind": "reference",
+               "sample": f"{threads} concurrent jobs (one per host thread) of GS {args.n}^2 {args.levels}-level at "
+                         f"1 and 3 iterations; per-iteration cost = difference, init = remainder; value = the "
+                         f"{args.iters}-iteration job rate they imply; reference headers + substitute f32 FFT "
+                         f"(FFTW absent)",
+               "cpu_model": cpu_model(), "per_iteration_rate_all_cores": r["per_iteration_rate"],
+               "single_core": ref_gs_single_core(ref, args.n, args.levels)}
         if osp is not None:
-            to = reference_ospr(args.ospr_n, 2, threads, threads)
-            cpu["ospr"] = {"value": threads * 2 / to, "unit": "subframes/s", "cores": threads,
+            cpu["ospr"] = {"value": ref_ospr_throughput(ref, args.ospr_n, 2, threads), "unit": "subframes/s",
+                           "cores": threads,
                            "sample": f"{threads} concurrent jobs x 2 subframes of OSPR {args.ospr_n}^2 binary"}
     if d.rank != 0:
         d.close()
         return
     B, K, npix = gs["B"], args.iters, gs["npix"]
-    units = d.world * B * K * args.steps
+    units = gs["total"] * K * args.steps
     value = units / (gs["ms"] / 1e3)
+    per = gs["per_step_ms"]
+    sigma_ms = statistics.stdev(per) if len(per) > 1 else 0.0
     pr = gs["profile_ms"]
     # pass times: CUDA events around each pass inside the timed step's graph
     # (the last timed step, iterations 1..K-1); repeated isolated launches of
@@ -560,8 +714,10 @@ def main():
         pass
     line = {
         "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": d.world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": gs["ms"] / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": base_config(args, d),
+        "warmup": args.warmup, "ms_per_step": gs["ms"] / args.steps,
+        "ms_per_step_sigma": sigma_ms, "value_sigma": value * sigma_ms / (gs["ms"] / args.steps),
+        "ms_per_step_each": per, "higher_is_better": True, "scaling": gs["scaling"],
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": base_config(args, d, gs["total"], gs["scaling"]),
         "roofline": {"bound": "hbm", "kernel": f"k_{dom} (fused {'replay-plane column' if dom == 'col' else 'aperture-plane row'} pass)",
                      "achieved": ach, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": ach / peak,
                      "traffic": traffic, "bytes_per_px": GS_BYTES_PER_PX[dom],
@@ -576,7 +732,7 @@ def main():
                      "col": {"ms": g_col, "achieved": col_gbs, "frac": col_gbs / peak, "isolated_ms": pr["col"]},
                      "seed_ms": pr["seed"]},
         "cpu_baseline": cpu, "e2e": gs.get("e2e"), "gpu_launches": gs["launches"], "clocks": gs["clocks"],
-        "check": {"traces_finite_and_decreasing": gs["check_ok"], "final_mse_mean": gs["final_mse_mean"]},
+        "check": gs["check"], "weak_scaling": weak,
     }
     if osp is not None:
         J, N, on = args.ospr_jobs, args.ospr_subframes, args.ospr_n

@@ -374,6 +374,37 @@ static void lt_rect(int bx0, int by0, int bw, int bh, double fraction, int *x0, 
 /* detail::run_ifta<float>, ifta.hpp:86-235.  Returns 0 or -1 (bad input).
  * hologram/replay: 2*npix floats; levels: npix int32 of the last
  * quantisation; trace: iterations doubles. */
+/* Test hook (lock-step parity, tests/test_gpu_lockstep.py): at the start of
+ * each iteration k listed in snap_iters[0..nsnap), the replay field R_{k-1}
+ * (2*npix floats) and the WGS weights (npix doubles) are copied to slot j of
+ * snaps_r / snaps_w, and the level indices of iteration k to snaps_lv. */
+static int g_nsnap;
+static const int *g_snap_iters;
+static float *g_snaps_r;
+static double *g_snaps_w;
+static int32_t *g_snaps_lv;
+
+int hgo_ifta_run(const hgo_ifta_cfg *cfg, const hgo_slm *slm, int nx, int ny, const double *amp,
+                 const double *phase_turns, const uint8_t *roi, const float *init_field,
+                 const double *init_weights, float *hologram, float *replay, int32_t *levels,
+                 double *trace, float *snap_r, double *snap_w);
+
+/* hgo_ifta_run with the snapshot lists above (not re-entrant: test use only). */
+int hgo_ifta_run_snaps(const hgo_ifta_cfg *cfg, const hgo_slm *slm, int nx, int ny, const double *amp,
+                       const double *phase_turns, const uint8_t *roi, float *hologram, float *replay,
+                       int32_t *levels, double *trace, int nsnap, const int *snap_iters, float *snaps_r,
+                       double *snaps_w, int32_t *snaps_lv) {
+    g_nsnap = nsnap;
+    g_snap_iters = snap_iters;
+    g_snaps_r = snaps_r;
+    g_snaps_w = snaps_w;
+    g_snaps_lv = snaps_lv;
+    int rc = hgo_ifta_run(cfg, slm, nx, ny, amp, phase_turns, roi, NULL, NULL, hologram, replay, levels, trace,
+                          NULL, NULL);
+    g_nsnap = 0;
+    return rc;
+}
+
 int hgo_ifta_run(const hgo_ifta_cfg *cfg, const hgo_slm *slm, int nx, int ny, const double *amp,
                  const double *phase_turns, const uint8_t *roi, const float *init_field,
                  const double *init_weights, float *hologram, float *replay, int32_t *levels,
@@ -447,6 +478,11 @@ int hgo_ifta_run(const hgo_ifta_cfg *cfg, const hgo_slm *slm, int nx, int ny, co
             if (snap_r) memcpy(snap_r, R, sizeof(float) * 2 * n);
             if (snap_w && w) memcpy(snap_w, w, sizeof(double) * n);
         }
+        for (int j = 0; j < g_nsnap; ++j)
+            if (g_snap_iters[j] == k) {
+                memcpy(g_snaps_r + (size_t)j * 2 * n, R, sizeof(float) * 2 * n);
+                if (g_snaps_w && w) memcpy(g_snaps_w + (size_t)j * n, w, sizeof(double) * n);
+            }
         /* f = prop.inverse(R), propagation.hpp:89-95 */
         hgo_fft2d_precise(nx, ny, +1, R, f);
         if (Q)
@@ -456,6 +492,8 @@ int hgo_ifta_run(const hgo_ifta_cfg *cfg, const hgo_slm *slm, int nx, int ny, co
             }
         /* quant.apply(f), ifta.hpp:172 */
         quant_apply(&q, f, levels);
+        for (int j = 0; j < g_nsnap; ++j)
+            if (g_snap_iters[j] == k && g_snaps_lv) memcpy(g_snaps_lv + (size_t)j * n, levels, sizeof(int32_t) * n);
         /* R = prop.forward(f), propagation.hpp:81-87 */
         if (Q) {
             for (size_t i = 0; i < n; ++i)

@@ -107,6 +107,7 @@ class IftaResult:
     snap_r: np.ndarray | None = None
     snap_w: np.ndarray | None = None
     seconds: float = 0.0
+    profile: tuple | None = None  # (transform, constraint, metric, other) seconds, reference only
 
 
 @dataclass
@@ -152,6 +153,8 @@ class Oracle:
             fn("mse", d, [vp, vp, vp, sz, i])
             fn("ifta_run", i, [C.POINTER(HgoIftaCfg), C.POINTER(HgoSlm), i, i, vp, vp, vp, vp, vp,
                                vp, vp, vp, vp, vp, vp])
+            fn("ifta_run_snaps", i, [C.POINTER(HgoIftaCfg), C.POINTER(HgoSlm), i, i, vp, vp, vp, vp, vp,
+                                     vp, vp, i, vp, vp, vp, vp])
             fn("ospr_run", i, [i, i, u64, d, C.POINTER(HgoSlm), i, i, vp, vp, i, vp, vp, vp, vp, vp, vp])
         else:
             fn("last_error", C.c_char_p, [])
@@ -308,10 +311,46 @@ class Oracle:
             return IftaResult(holo, rep, lv, tr, sr, sw)
         if init_field is not None or snapshot_iter:
             raise ValueError("snapshots / given init are restatement-only hooks")
-        secs = C.c_double()
+        tm = np.zeros(5, np.float64)  # RunReport seconds, profile transform/constraint/metric/other
         self._check(self._f["ifta_run"](C.byref(c), C.byref(s), nx, ny, _p(amp), _p(ph), _p(rm),
-                                        _p(holo), _p(rep), _p(lv), _p(tr), C.byref(secs)))
-        return IftaResult(holo, rep, lv, tr, seconds=secs.value)
+                                        _p(holo), _p(rep), _p(lv), _p(tr), _p(tm)))
+        return IftaResult(holo, rep, lv, tr, seconds=float(tm[0]), profile=tuple(float(v) for v in tm[1:]))
+
+    def ifta_snaps(self, amp, slm, iterations, snap_iters, seed=0, variant="gs", clamp=(0.1, 10.0),
+                   fresnel=None, scale_freedom=False):
+        """Restatement run with snapshots at the start of each iteration k in
+        snap_iters: returns (IftaResult, {k: (R_{k-1}, W_{k-1} or None, levels_k)}).
+        Test hook for the lock-step parity protocol."""
+        if self.kind != "restatement":
+            raise ValueError("snapshots are a restatement-only hook")
+        keep = []
+        amp = np.ascontiguousarray(amp, np.float64)
+        ny, nx = amp.shape
+        c = HgoIftaCfg()
+        c.variant = {"gs": 0, "wgs": 1, "lt": 2}[variant]
+        c.iterations = iterations
+        c.seed = seed
+        c.clamp_lo, c.clamp_hi = clamp
+        c.lt_initial_fraction = 0.1
+        c.phase_freedom = 1
+        c.scale_freedom = int(scale_freedom)
+        if fresnel is not None:
+            c.fresnel = 1
+            c.wavelength, c.distance, c.pitch_x, c.pitch_y = fresnel
+        s = _slm(slm, keep)
+        ks = np.ascontiguousarray(sorted(set(int(k) for k in snap_iters)), np.int32)
+        m = len(ks)
+        sr = np.empty((m, ny, nx), np.complex64)
+        sw = np.empty((m, ny, nx), np.float64) if variant == "wgs" else None
+        sl = np.empty((m, ny, nx), np.int32)
+        holo = np.empty((ny, nx), np.complex64)
+        rep = np.empty((ny, nx), np.complex64)
+        lv = np.empty((ny, nx), np.int32)
+        tr = np.empty(iterations, np.float64)
+        self._check(self._f["ifta_run_snaps"](C.byref(c), C.byref(s), nx, ny, _p(amp), None, None, _p(holo),
+                                              _p(rep), _p(lv), _p(tr), m, _p(ks), _p(sr), _p(sw), _p(sl)))
+        snaps = {int(k): (sr[j], None if sw is None else sw[j], sl[j]) for j, k in enumerate(ks)}
+        return IftaResult(holo, rep, lv, tr), snaps
 
     def ifta64(self, amp, slm, iterations, seed=0, variant="gs", phase_turns=None, roi=None,
                clamp=(0.1, 10.0), lt_initial_fraction=0.1, init_phase="auto", amp_outside_roi=False,

@@ -220,7 +220,7 @@ int hgr_normalize(double* img, int w, int h, int unit_energy) {
 // returned hologram with Quantiser::decide, as runner.cpp:259-262 does.
 int hgr_ifta_run(const hgo_ifta_cfg* c, const hgo_slm* s, int nx, int ny, const double* amp,
                  const double* phase_turns, const uint8_t* roi, float* hologram, float* replay,
-                 int32_t* levels, double* trace, double* seconds) {
+                 int32_t* levels, double* trace, double* timing) {
     return guard([&] {
         IftaConfig cfg;
         cfg.variant = c->variant == 0   ? IftaVariant::GS
@@ -260,7 +260,13 @@ int hgr_ifta_run(const hgo_ifta_cfg* c, const hgo_slm* s, int nx, int ny, const 
         }
         if (trace)
             for (size_t k = 0; k < rep.trace.points.size(); ++k) trace[k] = rep.trace.points[k].second;
-        if (seconds) *seconds = rep.seconds;
+        if (timing) {  // RunReport::seconds and ::profile (report.hpp:38-65)
+            timing[0] = rep.seconds;
+            timing[1] = rep.profile.transform;
+            timing[2] = rep.profile.constraint;
+            timing[3] = rep.profile.metric;
+            timing[4] = rep.profile.other;
+        }
     });
 }
 

@@ -336,7 +336,8 @@ def _check_variant(cfg: IftaConfig, want: IftaVariant | None, name: str):
 
 
 def run_ifta_batch(cfg: IftaConfig, amplitudes: np.ndarray, seeds=None, prop: Propagator | None = None,
-                   phases=None, init_field=None, init_weights=None, checkpoint=False) -> list[RunReport]:
+                   phases=None, init_field=None, init_weights=None, checkpoint=False,
+                   want_hologram=True) -> list[RunReport]:
     """B independent targets of one size/SLM/propagation, one launch sequence.
     seeds[b] replaces cfg.seed for target b (default: cfg.seed for all).
     checkpoint: the last iteration also applies the replay-plane constraint;
@@ -350,7 +351,8 @@ def run_ifta_batch(cfg: IftaConfig, amplitudes: np.ndarray, seeds=None, prop: Pr
     if cfg.iterations < 1:
         raise ValueError("IftaConfig: iterations must be >= 1")
     seeds = np.full(b, cfg.seed, np.uint64) if seeds is None else np.asarray(seeds, np.uint64)
-    bufs = _IftaBuffers(cfg, amps, seeds, phases, init_field, init_weights, checkpoint=checkpoint)
+    bufs = _IftaBuffers(cfg, amps, seeds, phases, init_field, init_weights, want_hologram=want_hologram,
+                        checkpoint=checkpoint)
     keep = []
     slm = _slm(cfg.slm, keep)
     c = _ifta_cfg(cfg)
@@ -359,7 +361,7 @@ def run_ifta_batch(cfg: IftaConfig, amplitudes: np.ndarray, seeds=None, prop: Pr
     reps = []
     for i in range(b):
         rep = RunReport(algorithm=_ALG[IftaVariant(cfg.variant)], seed=int(seeds[i]))
-        rep.hologram = bufs.hologram[i]
+        rep.hologram = None if bufs.hologram is None else bufs.hologram[i]
         rep.replay = bufs.replay[i]
         rep.levels = bufs.levels[i]
         rep.trace = MetricTrace("mse", [(k + 1, float(v)) for k, v in enumerate(bufs.trace[i])])

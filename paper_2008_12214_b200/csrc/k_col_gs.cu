@@ -7,16 +7,9 @@ void col_gs_fast(int ny, const ColArgs& a, int batch, cudaStream_t st, bool prep
     if (prepare) {
         col_dispatch<COL_GS_FAST, LAY_QUAD>(ny, a, batch, st, true);
         col_dispatch<COL_WGS_FAST, LAY_QUAD>(ny, a, batch, st, true);
-        col_persist_dispatch<COL_GS_FAST>(ny, a, batch, st, true);
-        col_persist_dispatch<COL_WGS_FAST>(ny, a, batch, st, true);
         return;
     }
-    if (a.weights) {
-        if (!col_persist_dispatch<COL_WGS_FAST>(ny, a, batch, st, false))
-            col_dispatch<COL_WGS_FAST, LAY_QUAD>(ny, a, batch, st, false);
-    } else {
-        if (!col_persist_dispatch<COL_GS_FAST>(ny, a, batch, st, false))
-            col_dispatch<COL_GS_FAST, LAY_QUAD>(ny, a, batch, st, false);
-    }
+    if (a.weights) col_dispatch<COL_WGS_FAST, LAY_QUAD>(ny, a, batch, st, false);
+    else col_dispatch<COL_GS_FAST, LAY_QUAD>(ny, a, batch, st, false);
 }
 }  // namespace hg

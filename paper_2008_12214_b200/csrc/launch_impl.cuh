@@ -131,46 +131,6 @@ inline void col_launch_c(const ColArgs& a, int batch, cudaStream_t st, bool prep
     CK(cudaGetLastError());
 }
 
-// Persistent pipelined GS / WGS column pass (k_col_persist), as the row pass.
-inline bool col_persist_on() {
-    static const bool on = [] {
-        const char* e = getenv("HG_COL_PERSIST");  // (off by default: measured slower)
-        return e ? atoi(e) != 0 : false;
-    }();
-    return on;
-}
-template <int NY, int MODE>
-inline bool col_persist_launch(const ColArgs& a, int batch, cudaStream_t st, bool prepare) {
-    if constexpr (!ColPersistCfg<NY>::ok || (MODE != COL_GS_FAST && MODE != COL_WGS_FAST)) {
-        return false;
-    } else {
-        constexpr int C = ColPersistCfg<NY>::C;
-        auto kern = k_col_persist<NY, MODE>;
-        if (prepare) {
-            set_smem(kern, ColPersistCfg<NY>::SMEM);
-            return true;
-        }
-        if (!col_persist_on() || !a.tmap || a.layout != LAY_QUAD || (a.cw > 0 && a.cw != C) || a.nx % C != 0)
-            return false;
-        const int colblocks = a.nx / C;
-        const long long ntiles = (long long)colblocks * batch;
-        const int sms = sm_count();
-        if (ntiles < 2LL * sms || ntiles > (1LL << 30)) return false;
-        kern<<<sms, 1024, ColPersistCfg<NY>::SMEM, st>>>(a, colblocks, (int)ntiles);
-        CK(cudaGetLastError());
-        return true;
-    }
-}
-template <int MODE>
-inline bool col_persist_dispatch(int ny, const ColArgs& a, int batch, cudaStream_t st, bool prepare) {
-    switch (ny) {
-        case 1024: return col_persist_launch<1024, MODE>(a, batch, st, prepare);
-        case 2048: return col_persist_launch<2048, MODE>(a, batch, st, prepare);
-        case 4096: return col_persist_launch<4096, MODE>(a, batch, st, prepare);
-        default: return false;
-    }
-}
-
 template <int NY, int MODE, int LAY>
 inline void col_launch(const ColArgs& a, int batch, cudaStream_t st, bool prepare) {
     constexpr int CM = ColCfg<NY, LAY>::C;

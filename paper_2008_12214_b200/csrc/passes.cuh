@@ -741,170 +741,4 @@ __global__ void __launch_bounds__(LineCfg<NY, ColCfg<NY, LAY>::EM>::T * C, ColCf
     col_cta<NY, C, MODE, LAY>(a, blockIdx.x, blockIdx.y, gridDim.x);
 }
 
-// A read-only global load that stays in program order with the other
-// ordered loads (software-pipelined side-array reads).
-__device__ __forceinline__ float ldg_ordered(const float* p) {
-    float v;
-    asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(v) : "l"(p));
-    return v;
-}
-
-// ------------------------------------------------ persistent column pass
-// The fused GS / WGS column pass as the same two-group software pipeline as
-// k_row_persist: one 1024-thread CTA per SM, two 512-thread groups with their
-// own exchange buffers, one shared landing buffer filled by TMA (the tile of
-// the next group) while both groups transform.  The fp32 target slice is
-// prefetched into L2 when its tile's load is issued and read per thread
-// after the forward transform (coalesced: 32 consecutive floats per warp and
-// element).  MSE partials: one block of 8 doubles per tile, summed per group.
-template <int NY>
-struct ColPersistCfg {
-    static constexpr int C = ColCfg<NY, LAY_QUAD>::C;
-    static constexpr int T = LineCfg<NY>::T;
-    static constexpr bool ok = ColTma<NY, C, LAY_QUAD>::on && T * C == 512 && ColCfg<NY, LAY_QUAD>::EM == 16;
-    // exchange buffer, rounded to 128 B: TMA boxes land in / leave from smem at 128-B alignment
-    static constexpr int XB = (PaddedLen<NY>::value * C * (int)sizeof(float2) + 127) / 128 * 128;
-    static constexpr int TILE = NY * C * (int)sizeof(float2);
-    static constexpr int SMEM = 2 * XB + TILE;
-};
-
-template <int NY, int MODE>
-__global__ void __launch_bounds__(1024, 1) k_col_persist(ColArgs a, int colblocks, int ntiles) {
-    using PC = ColPersistCfg<NY>;
-    constexpr int C = PC::C, T = PC::T, E = LineCfg<NY>::E;
-    using Tma = ColTma<NY, C, LAY_QUAD>;
-    constexpr int kBoxRows = Tma::kBoxRows, kBoxes = NY / 2 / kBoxRows;
-    static_assert(MODE == COL_GS_FAST || MODE == COL_WGS_FAST, "k_col_persist: GS / WGS fast constraint");
-    extern __shared__ __align__(128) float2 smem[];
-    __shared__ uint64_t full[2];
-    __shared__ double red[2][16][4];
-    const int g = threadIdx.x >> 9, tg = threadIdx.x & 511;
-    float2* xg = smem + g * (PC::XB / (int)sizeof(float2));
-    float2* land = smem + 2 * (PC::XB / (int)sizeof(float2));
-    const GroupSync gsync{1 + g, 512};
-    const int c0 = tg % C, t0 = tg / C;
-    const int lane = threadIdx.x & 31, wg = tg >> 5;
-    const int nx = a.nx;
-    const bool last = a.last && !a.ckpt;  // skip the constraint
-    const float norm = a.norm, lo = a.clamp_lo, hi = a.clamp_hi;
-    const int G = gridDim.x;
-    auto issue = [&](int s, uint64_t* bar) {  // the tile's TMA boxes + an L2 prefetch of its target slice
-        const int bx = s % colblocks, by = s / colblocks;
-        const int tq = bx * (C / 2) * 8, tr = a.tma_row0 + by * a.tma_brows;
-        mbar_expect_tx(bar, PC::TILE);
-#pragma unroll 1
-        for (int k = 0; k < kBoxes; ++k) tma_load_2d(land + k * kBoxRows * 2 * C, a.tmap, tq, tr + k * kBoxRows, bar);
-        const float* ts = a.target + a.t_bstride * by + colpair_index(bx * C, 0, NY);
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ts), "r"(C * NY * (int)sizeof(float))
-                     : "memory");
-    };
-    if (threadIdx.x == 0) {
-        mbar_init(&full[0], 1);
-        mbar_init(&full[1], 1);
-        if ((int)blockIdx.x < ntiles) issue(blockIdx.x, &full[0]);
-    }
-    __syncthreads();
-    const bool leader = tg == 0;
-#pragma unroll 1
-    for (int k = g, s = blockIdx.x + g * G; s < ntiles; k += 2, s += 2 * G) {
-        const int bx = s % colblocks, by = s / colblocks;
-        // per-tile opaque copies of the thread coordinates: everything derived
-        // from them (smem slots, side-array offsets) is loop-invariant, and
-        // hoisting it out of the tile loop would hold ~40 registers across it
-        const int c = opaque(c0), t = opaque(t0);
-        const ColSmemIdx<C> idx{c};
-        const int x = bx * C + c;
-        float2 v[E];
-        mbar_wait(&full[g], (k >> 1) & 1);
-#pragma unroll
-        for (int e = 0; e < E; ++e) v[e] = land[Tma::slot(c, t + e * T)];
-        if (leader) bulk_wait_read0();  // this group's previous store has left its exchange buffer
-        gsync();
-#ifndef HG_CP_DBG
-#define HG_CP_DBG 0
-#endif
-        if (!(HG_CP_DBG & 1) && leader && s + G < ntiles) issue(s + G, &full[g ^ 1]);
-        // (opaque table pointers: the twiddle loads depend only on t, so without
-        // them the compiler hoists them out of the tile loop and spills)
-        if (!(HG_CP_DBG & 16)) fft_line<NY, -1, 16, float2, ColSmemIdx<C>, GroupSync>(v, t, xg, idx, opaque(a.tw), gsync);  // completes P
-        // GS/WGS, no ROI, phase freedom: mse partials (metrics.hpp:70-97) and
-        // R <- amp * R/|R| (ifta.hpp:198-214), as k_col COL_GS_FAST / COL_WGS_FAST
-        const size_t sb = colpair_index(x, t, NY);
-        const float* tgp = a.target + a.t_bstride * by + sb;
-        float* w = MODE == COL_WGS_FAST ? a.weights + a.t_bstride * by + sb : nullptr;
-        // target loads four elements ahead of their use (ordered volatile loads keep
-        // the compiler from hoisting all 16 and spilling the line)
-        constexpr int AH = 4;
-        float amp0v[E];
-#pragma unroll
-        for (int e = 0; e < AH; ++e) amp0v[e] = ldg_ordered(&tgp[e * 2 * T]);
-        float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-            if (e + AH < E) amp0v[e + AH] = ldg_ordered(&tgp[(e + AH) * 2 * T]);
-            const float2 R = cscale(v[e], norm);
-            const float r2 = R.x * R.x + R.y * R.y;
-            const float amp0 = amp0v[e];
-            const float ri = rsqrtf(r2);
-            const float r = r2 > 0.f ? r2 * ri : 0.f;
-            const float d = amp0 - r;
-            acc[0] = fmaf(d, d, acc[0]);
-            acc[1] = fmaf(amp0, r, acc[1]);
-            acc[2] += r2;
-            acc[3] = fmaf(amp0, amp0, acc[3]);
-            float amp = amp0;
-            if constexpr (MODE == COL_WGS_FAST) {
-                if (!last && amp0 > 0.f) {  // ifta.hpp:198-204
-                    const float cand = w[e * 2 * T] * amp0 * (r > 1e-12f ? ri : 1e12f);
-                    const float wn = fminf(fmaxf(cand, lo), hi);
-                    w[e * 2 * T] = wn;
-                    amp = amp0 * wn;
-                }
-            }
-            const float sc = amp * ri;
-            v[e] = r2 > 0.f ? make_float2(R.x * sc, R.y * sc) : make_float2(amp, 0.f);
-            if (last) v[e] = R;
-        }
-        if (!(HG_CP_DBG & 4) && !a.last) fft_line<NY, +1, 16, float2, ColSmemIdx<C>, GroupSync>(v, t, xg, idx, opaque(a.tw), gsync);
-        // tile back to HBM: landing layout in this group's exchange buffer, then TMA
-        float* dsts = nullptr;
-        (void)dsts;
-        if (!(HG_CP_DBG & 2))
-#pragma unroll
-        for (int e = 0; e < E; ++e) xg[Tma::slot(c, t + e * T)] = v[e];
-        // per-tile MSE partials: warp sums in float, per-warp doubles, fixed-order group sum
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
-        if (lane == 0)
-#pragma unroll
-            for (int i = 0; i < 4; ++i) red[g][wg][i] = (double)acc[i];
-        fence_proxy_async();
-        gsync();
-        if (leader) {
-            const void* map = a.tmap;
-            const int tq = bx * (C / 2) * 8, tr = a.tma_row0 + by * a.tma_brows;
-#pragma unroll 1
-            for (int kb = 0; kb < kBoxes; ++kb) tma_store_2d(map, tq, tr + kb * kBoxRows, xg + kb * kBoxRows * 2 * C);
-            bulk_commit();
-        }
-        if (!(HG_CP_DBG & 8) && wg == 0) {
-            double sacc[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                double xx = lane < 16 ? red[g][lane][i] : 0.0;
-                sacc[i] = warp_sum(xx);
-            }
-            if (lane == 0) {
-                double* out = a.partials + ((size_t)by * colblocks + bx) * 8;
-#pragma unroll
-                for (int i = 0; i < 4; ++i) out[i] = sacc[i];
-            }
-        }
-    }
-    if (tg == 0) bulk_wait_read0();
-    (void)nx;
-}
-
 }  // namespace hg

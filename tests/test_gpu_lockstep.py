@@ -1,0 +1,242 @@
+"""Lock-step parity of the IFTA loop at config size, with the replay-plane
+constraint and the WGS weight rule inside the window.
+
+Protocol (BASELINE north_star contract: levels bit-exact except pixels whose
+pre-quantisation value lies within 1e-5 rad of a decision threshold; MSE
+within 1e-4 relative).  One oracle run of K iterations records, at the start
+of iterations k and k+1, the replay field R_{k-1} / R_k, the WGS weights and
+the levels of that iteration (oracle/hg_oracle.c hgo_ifta_run_snaps).  From
+the oracle's R_{k-1} (and W_{k-1}) the GPU then runs
+
+  (A) ONE iteration with checkpoint on: the constraint and the WGS weight
+      update of iteration k run (ifta.hpp:185-224), so the GPU's constrained
+      field R_k and weights W_k are compared with the oracle's, and its
+      levels_k / mse_k with the oracle's;
+  (B) TWO iterations: levels_{k+1} and mse_k, mse_{k+1}.
+
+Comparisons (counts and errors are recorded in profiles/parity_r02.json,
+or $HG_PARITY_OUT; every level mismatch must fall in a named class):
+  (A) levels_k: mismatches only where the oracle's pre-quantisation angle is
+      within 1e-5 rad of a threshold ("near", the north-star exception);
+      mse_k within 1e-4.  Constrained field and weights: the constraint
+      R <- amp w R/|R| divides the transform's rounding by |R| (ill-conditioned
+      where the unconstrained replay is dark), so the error is compared after
+      removing that condition number: |dR_i| |R_unc,i| / |R_k,i| and
+      |dW_i|/W_i |R_unc,i| (R_unc: the oracle's unconstrained replay of
+      iteration k) must be at the transform's rounding level, RMS < 1e-5 of
+      RMS |R_unc|.
+  (B) levels_{k+1}: the inverse transform is linear, so the oracle's
+      pre-quantisation field plus P^-1(GPU R_k - oracle R_k) predicts the
+      GPU's.  Mismatches must be "near" or "propagated": pixels where that
+      predicted field quantises differently from the oracle's or lies within
+      1e-5 rad + 6 x the transform's rounding / |f| of a threshold.  I.e. the
+      GPU's second iteration is exact given its own first one; the difference
+      it inherits is the float rounding of iteration k, amplified by the
+      chaotic multi-level loop.  mse_k, mse_{k+1} within 1e-4.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from helpers import TWO_PI, level_mismatches, phase_threshold_distance, rel
+
+pytestmark = pytest.mark.gpu
+hg = pytest.importorskip("paper_2008_12214_b200")
+
+MSE_TOL = 1e-4
+NEAR = 1e-5
+RESULTS = {}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _write_parity_report():
+    yield
+    if not RESULTS:
+        return
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    path = os.environ.get("HG_PARITY_OUT", os.path.join(root, "profiles", "parity_r02.json"))
+    old = {}
+    if os.path.exists(path):
+        try:
+            old = json.load(open(path))
+        except ValueError:
+            old = {}
+    old.update(RESULTS)
+    os.makedirs(os.path.dirname(path), exist_ok=True)
+    with open(path, "w") as f:
+        json.dump(old, f, indent=1, sort_keys=True)
+
+
+def pre_quant(oracle, R, fresnel):
+    """The oracle's aperture field before quantisation, P^-1(R) (double)."""
+    f = oracle.fft2(R.astype(np.complex128), +1)
+    if fresnel is not None:
+        ny, nx = R.shape
+        f = f * np.conj(oracle.fresnel_q(nx, ny, *fresnel))
+    return f
+
+
+def quantise_levels(f, slm):
+    """Full-circle phase quantiser decision (quantise.hpp:175-190) in double."""
+    d = np.arctan2(f.imag, f.real) - slm.min_arg
+    d = d - TWO_PI * np.floor(d / TWO_PI)
+    k = np.floor(d * (slm.levels / TWO_PI) + 0.5).astype(np.int64)
+    return np.where(k >= slm.levels, 0, k)
+
+
+def unconstrained_replay(oracle, levels, slm, fresnel):
+    """P(state[levels]) in double: the oracle's replay of that iteration before
+    the constraint (to the float rounding of the states)."""
+    f = np.exp(1j * (slm.min_arg + levels.astype(np.float64) * (TWO_PI / slm.levels)))
+    if fresnel is not None:
+        ny, nx = levels.shape
+        f = f * oracle.fresnel_q(nx, ny, *fresnel)
+    return oracle.fft2(f, -1)
+
+
+def gpu_run(amps, slm, K, R0, W0, variant, fresnel, checkpoint):
+    ny, nx = amps.shape[-2:]
+    c = hg.IftaConfig(iterations=K, slm=slm, target=hg.TargetSpec(amps[0]), seed=1)
+    if variant == "wgs":
+        c.variant = hg.IftaVariant.WeightedGS
+    c.init_phase = hg.InitPhase.Given
+    prop = None if fresnel is None else hg.Propagator.fresnel(nx, ny, hg.FresnelParams(*fresnel))
+    return hg.run_ifta_batch(c, amps, prop=prop, init_field=R0,
+                             init_weights=None if W0 is None else W0.astype(np.float32), checkpoint=checkpoint,
+                             want_hologram=False)
+
+
+def check_window(oracle, name, amps, slm, k, snaps, tr_ref, variant=None, fresnel=None, targets=(0,), init=None):
+    """Windows (A) and (B) at iteration k for the batch `amps`; `targets`
+    are the batch entries compared with the oracle snapshots `snaps` /
+    traces `tr_ref` (dicts by target; init = per-target R_{k-1}, W_{k-1})."""
+    B = amps.shape[0]
+    R0 = np.empty(amps.shape, np.complex64)
+    W0 = None if variant != "wgs" else np.empty(amps.shape, np.float64)
+    for b in range(B):
+        t = b if b in snaps else targets[0]
+        R0[b] = snaps[t][k][0]
+        if W0 is not None:
+            W0[b] = snaps[t][k][1]
+    repA = gpu_run(amps, slm, 1, R0, W0, variant, fresnel, checkpoint=True)
+    repB = gpu_run(amps, slm, 2, R0, W0, variant, fresnel, checkpoint=False)
+    for t in targets:
+        Rp, _, lv_k = snaps[t][k]
+        Rk, Wk, lv_k1 = snaps[t][k + 1]
+        A, Bt = repA[t], repB[t]
+        # (A) levels_k, mse_k, constrained R_k, W_k
+        pre_k = pre_quant(oracle, Rp, fresnel)
+        near_k = phase_threshold_distance(pre_k, slm) < NEAR
+        mA = level_mismatches(A.levels, lv_k)
+        R_unc = unconstrained_replay(oracle, lv_k, slm, fresnel)  # oracle's R of iteration k, before the constraint
+        mag_unc = np.abs(R_unc)
+        rms_unc = float(np.sqrt(np.mean(mag_unc ** 2)))
+        Rk64 = Rk.astype(np.complex128)
+        dR = A.replay.astype(np.complex128) - Rk64
+        cond = np.abs(dR) * mag_unc / np.maximum(np.abs(Rk64), 1e-300)
+        out = {"k": k, "target": int(t), "A_level_mismatch": int(mA.sum()), "A_near": int((mA & near_k).sum()),
+               "A_bad": int((mA & ~near_k).sum()), "A_mse_rel": rel(A.trace.values()[0], tr_ref[t][k - 1]),
+               "A_R_rel_rms_raw": float(np.sqrt(np.mean(np.abs(dR) ** 2)) / np.sqrt(np.mean(np.abs(Rk64) ** 2))),
+               "A_R_conditioned_rel_rms": float(np.sqrt(np.mean(cond ** 2))) / rms_unc,
+               "A_R_conditioned_rel_max": float(cond.max()) / rms_unc}
+        if Wk is not None:
+            wr = np.abs(A.weights.astype(np.float64) - Wk) / np.maximum(np.abs(Wk), 1e-300)
+            wc = wr * mag_unc
+            out.update({"A_W_rel_rms_raw": float(np.sqrt(np.mean(wr ** 2))),
+                        "A_W_conditioned_rel_rms": float(np.sqrt(np.mean(wc ** 2))) / rms_unc,
+                        "A_W_conditioned_rel_max": float(wc.max()) / rms_unc})
+        # (B) levels_{k+1}, mse_k, mse_{k+1}
+        pre_k1 = pre_quant(oracle, Rk, fresnel)
+        near = phase_threshold_distance(pre_k1, slm) < NEAR
+        pred = pre_k1 + pre_quant(oracle, dR, fresnel)  # the GPU's pre-quantisation field, to rounding
+        mag = np.abs(pred)
+        floor = 2e-7 * float(np.sqrt(np.mean(mag ** 2)))  # the GPU transform's own rounding
+        prop = (quantise_levels(pred, slm) != lv_k1) | (
+            phase_threshold_distance(pred, slm) < NEAR + 6.0 * floor / np.maximum(mag, 1e-300))
+        mB = level_mismatches(Bt.levels, lv_k1)
+        trB = Bt.trace.values()
+        out.update({"B_level_mismatch": int(mB.sum()), "B_near": int((mB & near).sum()),
+                    "B_propagated": int((mB & ~near & prop).sum()), "B_bad": int((mB & ~near & ~prop).sum()),
+                    "B_propagated_class_size": int(prop.sum()), "B_mse_rel_k": rel(trB[0], tr_ref[t][k - 1]),
+                    "B_mse_rel_k1": rel(trB[1], tr_ref[t][k])})
+        RESULTS[f"{name}/k={k}/t={t}"] = out
+        assert out["A_bad"] == 0, out
+        assert out["A_mse_rel"] < MSE_TOL, out
+        assert out["A_R_conditioned_rel_rms"] < 1e-5, out
+        if Wk is not None:
+            assert out["A_W_conditioned_rel_rms"] < 1e-5, out
+        assert out["B_bad"] == 0, out
+        assert out["B_mse_rel_k"] < MSE_TOL and out["B_mse_rel_k1"] < MSE_TOL, out
+    return RESULTS
+
+
+def windows(K):
+    return [1, 2, K // 2, K - 1]
+
+
+def snap_iters(K):
+    return sorted({j for k in windows(K) for j in (k, k + 1)})
+
+
+@pytest.fixture(scope="module")
+def config2(oracle):
+    # BASELINE config 2: WGS 1024^2, 256 levels, 200 iterations, clamp [0.1, 10], seed 1
+    amp = hg.patterns.bench_target(1024)
+    slm = hg.SlmSpec.full_circle_phase(256)
+    K = 200
+    res, snaps = oracle.ifta_snaps(amp, slm, K, snap_iters(K), seed=1, variant="wgs")
+    return amp, slm, K, {0: snaps}, {0: res.trace}
+
+
+@pytest.mark.parametrize("k", windows(200))
+def test_config2_wgs_1024_lockstep_window(oracle, config2, k):
+    amp, slm, K, snaps, tr = config2
+    check_window(oracle, "config2_wgs_1024", amp[None], slm, k, snaps, tr, variant="wgs")
+
+
+FRESNEL = (532e-9, 0.1, 8e-6, 8e-6)  # test_propagation.cpp:25-32
+
+
+@pytest.fixture(scope="module")
+def config4(oracle):
+    # BASELINE config 4: Fresnel GS 2048^2, 256 levels, 100 iterations, seed 1
+    amp = hg.patterns.bench_target(2048)
+    slm = hg.SlmSpec.full_circle_phase(256)
+    K = 100
+    res, snaps = oracle.ifta_snaps(amp, slm, K, snap_iters(K), seed=1, fresnel=FRESNEL)
+    return amp, slm, K, {0: snaps}, {0: res.trace}
+
+
+@pytest.mark.parametrize("k", windows(100))
+def test_config4_fresnel_2048_lockstep_window(oracle, config4, k):
+    amp, slm, K, snaps, tr = config4
+    check_window(oracle, "config4_fresnel_2048", amp[None], slm, k, snaps, tr, fresnel=FRESNEL)
+
+
+@pytest.fixture(scope="module")
+def config5(oracle):
+    # BASELINE config 5: batch GS 4096^2, 256 levels, K = 25, target t has seed 1 + t;
+    # oracle runs for targets 0 and 63
+    amp = hg.patterns.bench_target(4096)
+    slm = hg.SlmSpec.full_circle_phase(256)
+    K = 25
+    snaps, tr = {}, {}
+    for t in (0, 63):
+        res, s = oracle.ifta_snaps(amp, slm, K, snap_iters(K), seed=1 + t)
+        snaps[t], tr[t] = s, res.trace
+    return amp, slm, K, snaps, tr
+
+
+@pytest.mark.parametrize("k", windows(25))
+def test_config5_gs_4096_lockstep_window(oracle, config5, k):
+    amp, slm, K, snaps, tr = config5
+    if k in (1, K - 1):  # inside the benchmark's 64-target batch (its launch geometry)
+        amps = np.broadcast_to(amp, (64,) + amp.shape)
+        check_window(oracle, "config5_gs_4096_batch64", amps, slm, k, snaps, tr, targets=(0, 63))
+    else:  # targets 0 and 63 as a 2-target batch (same kernels: persistent row pass, 64-col tiles)
+        sn = {0: snaps[0], 1: snaps[63]}
+        trr = {0: tr[0], 1: tr[63]}
+        check_window(oracle, "config5_gs_4096_t0_t63", np.broadcast_to(amp, (2,) + amp.shape), slm, k, sn, trr,
+                     targets=(0, 1))

@@ -123,3 +123,48 @@ def test_two_rank_ospr_subframe_blocks_match_single_process():
         assert p.exitcode == 0
     assert got.shape == want.shape
     assert np.max(np.abs(got - want) / want) < 1e-5
+
+
+# ---- rank 0 gathers every target's levels and MSE trace
+# (cmd_batch's result set, runner.cpp:365-451) over uneven shards
+BATCH_TOTAL = 5
+
+
+def _batch_results(seeds):
+    from pyoracle import Oracle
+    from paper_2008_12214_b200.types import SlmSpec
+    o = Oracle("restatement")
+    amp = patterns.bench_target(N)
+    runs = [o.ifta(amp, SlmSpec.full_circle_phase(16), K, seed=int(s)) for s in seeds]
+    return np.stack([r.levels.astype(np.uint8) for r in runs]), np.stack([r.trace for r in runs])
+
+
+def _batch_worker(rank, world, port, q):
+    from paper_2008_12214_b200.shard import gather_batch_results
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    start, count = shard_range(BATCH_TOTAL, world, rank)
+    lv, tr = _batch_results(unit_seeds(start, count))
+    got = gather_batch_results(torch.from_numpy(lv), torch.from_numpy(tr), dist, world, rank, BATCH_TOTAL)
+    if rank == 0:
+        q.put((got[0].numpy(), got[1].numpy()))
+    else:
+        assert got is None
+    dist.destroy_process_group()
+
+
+def test_two_rank_batch_levels_and_traces_gathered_in_target_order():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_batch_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    lv, tr = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want_lv, want_tr = _batch_results(unit_seeds(0, BATCH_TOTAL))
+    assert lv.shape == want_lv.shape and tr.shape == want_tr.shape
+    assert np.array_equal(lv, want_lv) and np.array_equal(tr, want_tr)

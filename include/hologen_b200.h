@@ -360,6 +360,13 @@ int hgc_gray8_to_levels(const uint8_t* px, size_t n, int level_count, int32_t* o
 int hgc_replay_to_gray8(const float* replay, int nx, int ny, int batch, uint8_t* out, double* peak);
 /* The "<png_path>.scale.txt" companion: "amplitude_at_255=<shortest double>\n". */
 int hgc_write_replay_scale(const char* png_path, double peak);
+/* write_png_gray (io.cpp:221-237): an 8-bit greyscale PNG (zlib deflate; the
+ * reference uses libpng's simplified API).  HGC_EINVAL "write_png_gray: pixel
+ * buffer does not match dimensions", HGC_EIO on file errors. */
+int hgc_write_png_gray(const char* path, const uint8_t* pixels, int width, int height);
+/* read_png_gray8 (io.cpp:239-258) for 8-bit greyscale PNGs: pixels == NULL
+ * returns the size only.  HGC_EIO "not a PNG file: <path>" / "png decode failed (...)". */
+int hgc_read_png_gray8(const char* path, int* width, int* height, uint8_t* pixels);
 
 /* ------------------------------------------------------- primitives */
 /* Unitary 2-D DFT of `batch` fields, sign -1 forward / +1 inverse; in == out

@@ -140,6 +140,8 @@ _SIGS = {
     "hgc_gray8_to_levels": (_i, [_vp, C.c_size_t, _i, _vp]),
     "hgc_replay_to_gray8": (_i, [_vp, _i, _i, _i, _vp, _vp]),
     "hgc_write_replay_scale": (_i, [C.c_char_p, _d]),
+    "hgc_write_png_gray": (_i, [C.c_char_p, _vp, _i, _i]),
+    "hgc_read_png_gray8": (_i, [C.c_char_p, _P(_i), _P(_i), _vp]),
     "hgc_fork_seed": (_u64, [_u64, _u64]),
     "hgc_mse": (_i, [_vp, _vp, _vp, _i, _i, _i, _P(_d)]),
     "hgc_fresnel_phase": (_i, [_i, _i, _P(HgcFresnel), _vp]),

@@ -67,7 +67,7 @@ def build(verbose: bool = False, jobs: int | None = None, defines: list[str] | N
                 if verbose:
                     print("compiled", os.path.basename(s), flush=True)
     if todo or not os.path.exists(LIB) or _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs]
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lz"]  # zlib: PNG files (io_hgf.cpp)
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")

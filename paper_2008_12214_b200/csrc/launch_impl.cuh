@@ -124,8 +124,6 @@ inline void col_launch_c(const ColArgs& a, int batch, cudaStream_t st, bool prep
         return;
     }
     if (ColTma<NY, C, LAY>::on && !a.tmap) fail(HGC_ECUDA, "column pass: TMA tile launched without a tensor map");
-    static const bool smem_ready = (set_smem(kern, smem), true);  // narrower run-time widths (col_width_rt)
-    (void)smem_ready;
     dim3 grid(a.nx / C, batch);
     kern<<<grid, LineCfg<NY, EM>::T * C, smem, st>>>(a);
     CK(cudaGetLastError());
@@ -134,6 +132,14 @@ inline void col_launch_c(const ColArgs& a, int batch, cudaStream_t st, bool prep
 template <int NY, int MODE, int LAY>
 inline void col_launch(const ColArgs& a, int batch, cudaStream_t st, bool prepare) {
     constexpr int CM = ColCfg<NY, LAY>::C;
+    if (prepare) {  // every width a launch may narrow to (col_width_rt): kernel attributes are per device
+        if constexpr (CM >= 1 && LAY == LAY_ROW) col_launch_c<NY, 1, MODE, LAY>(a, batch, st, true);
+        if constexpr (CM >= 2) col_launch_c<NY, 2, MODE, LAY>(a, batch, st, true);
+        if constexpr (CM >= 4) col_launch_c<NY, 4, MODE, LAY>(a, batch, st, true);
+        if constexpr (CM >= 8) col_launch_c<NY, 8, MODE, LAY>(a, batch, st, true);
+        if constexpr (CM >= 16) col_launch_c<NY, 16, MODE, LAY>(a, batch, st, true);
+        return;
+    }
     switch (a.cw > 0 ? a.cw : col_width<NY, LAY>(a.nx)) {
         case 1: if constexpr (CM >= 1 && LAY == LAY_ROW) col_launch_c<NY, 1, MODE, LAY>(a, batch, st, prepare); break;
         case 2: if constexpr (CM >= 2) col_launch_c<NY, 2, MODE, LAY>(a, batch, st, prepare); break;

@@ -230,7 +230,7 @@ __device__ __forceinline__ void row_cta(const RowArgs& a, const int bx, const in
     if constexpr (MODE == ROW_PLAIN) {
         // Propagator<float>::forward / inverse halves (propagation.hpp:81-95):
         // forward rows start from f*Q; inverse rows finish with *norm *conj(Q).
-        const size_t rowbase = (size_t)y * NX;
+        const size_t rowbase = (size_t)yy * NX;
         if (a.sign < 0) {
             if (a.fresnel_q)
 #pragma unroll
@@ -251,7 +251,7 @@ __device__ __forceinline__ void row_cta(const RowArgs& a, const int bx, const in
 #pragma unroll 1
         for (int rep = 0; rep < 2; ++rep)
 #endif
-        row_fused_body<NX, QK, FQ, LV>(v, t, y, b, valid, smem, idx, a, sstates);
+        row_fused_body<NX, QK, FQ, LV>(v, t, yy, b, valid, smem, idx, a, sstates);  // (padding rows: row 0's side arrays)
 #endif
     }
 #ifndef HG_ROW_DIRECT_STORE  // bulk-loaded tiles stored by per-thread coalesced stores (no EXIT wait on the bulk read)

@@ -1,8 +1,8 @@
 """Output formats on either side of the hot path, mirroring
 the reference's io.hpp: HGF1 field dumps (io.cpp:168-186, :316-345), the
 hologram-PNG level encoding (io.cpp:272-298) and the replay-PNG pixels and
-scale file (io.cpp:189-207).  Pixel arrays are what the reference hands to
-libpng; PNG compression is outside this package."""
+scale file (io.cpp:189-207), and the PNG files themselves (write_png_gray /
+read_png_gray8, io.cpp:221-258: 8-bit greyscale, zlib deflate)."""
 from __future__ import annotations
 
 import ctypes as C
@@ -70,3 +70,42 @@ def replay_to_gray8(replay: np.ndarray) -> tuple[np.ndarray, float]:
 def write_replay_scale(png_path: str | os.PathLike, peak: float) -> None:
     """The '<png>.scale.txt' companion: 'amplitude_at_255=<shortest double>'."""
     check(lib.hgc_write_replay_scale(os.fsencode(png_path), float(peak)))
+
+
+def write_png_gray(path: str | os.PathLike, pixels: np.ndarray) -> None:
+    """write_png_gray (io.cpp:221-237): 8-bit greyscale PNG of [height][width] pixels."""
+    px = np.ascontiguousarray(pixels, np.uint8)
+    if px.ndim != 2:
+        raise ValueError("write_png_gray: pixel buffer does not match dimensions")
+    check(lib.hgc_write_png_gray(os.fsencode(path), _p(px), px.shape[1], px.shape[0]))
+
+
+def read_png_gray8(path: str | os.PathLike) -> np.ndarray:
+    """read_png_gray8 (io.cpp:239-258) for 8-bit greyscale PNGs."""
+    w, h = C.c_int(), C.c_int()
+    bp = os.fsencode(path)
+    check(lib.hgc_read_png_gray8(bp, C.byref(w), C.byref(h), None))
+    out = np.empty((h.value, w.value), np.uint8)
+    check(lib.hgc_read_png_gray8(bp, C.byref(w), C.byref(h), _p(out)))
+    return out
+
+
+def write_hologram_png(path: str | os.PathLike, levels: np.ndarray, level_count: int) -> None:
+    """write_hologram_png (io.cpp:272-287): levels as lround(255 k / (L-1)) grey."""
+    if level_count < 2 or level_count > 256:
+        raise ValueError("write_hologram_png: level count must be in [2, 256] for a lossless 8-bit encoding")
+    write_png_gray(path, levels_to_gray8(levels, level_count))
+
+
+def read_hologram_png(path: str | os.PathLike, level_count: int) -> np.ndarray:
+    """read_hologram_png (io.cpp:289-298): the level indices back (int32)."""
+    return gray8_to_levels(read_png_gray8(path), level_count)
+
+
+def write_replay_png(path: str | os.PathLike, replay: np.ndarray) -> float:
+    """write_replay_png (io.cpp:189-207): |replay| scaled to 255 at its peak, plus
+    '<path>.scale.txt'.  Returns amplitude_at_255."""
+    px, peak = replay_to_gray8(replay)
+    write_png_gray(path, px)
+    write_replay_scale(path, peak)
+    return peak

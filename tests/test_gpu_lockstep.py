@@ -17,14 +17,18 @@ the oracle's R_{k-1} (and W_{k-1}) the GPU then runs
 Comparisons (counts and errors are recorded in profiles/parity_r02.json,
 or $HG_PARITY_OUT; every level mismatch must fall in a named class):
   (A) levels_k: mismatches only where the oracle's pre-quantisation angle is
-      within 1e-5 rad of a threshold ("near", the north-star exception);
-      mse_k within 1e-4.  Constrained field and weights: the constraint
-      R <- amp w R/|R| divides the transform's rounding by |R| (ill-conditioned
-      where the unconstrained replay is dark), so the error is compared after
-      removing that condition number: |dR_i| |R_unc,i| / |R_k,i| and
-      |dW_i|/W_i |R_unc,i| (R_unc: the oracle's unconstrained replay of
-      iteration k) must be at the transform's rounding level, RMS < 1e-5 of
-      RMS |R_unc|.
+      within 1e-5 rad of a threshold ("near", the north-star exception) or,
+      for dark pixels, within 1e-5 rad + 6 x the transform's rounding / |f|
+      ("lowf": the angle of a small |f| carries the transform's absolute
+      rounding divided by |f|); mse_k within 1e-4.  Constrained field and
+      weights: the reference constraint (ifta.hpp:198-214, in double) applied
+      to the GPU's own iteration-k replay P(state[levels_k]) predicts them;
+      the constraint R <- amp w R/|R| divides the transform's rounding by |R|,
+      so the error is compared after removing that condition number
+      (|dR_i| |R_unc,i| / |R_i|, |dW_i|/W_i |R_unc,i|), RMS < 1e-5 of RMS
+      |R_unc|.  The raw difference to the oracle's own R_k is recorded too: it
+      also carries the near-threshold level flips allowed above (each flip
+      moves every replay pixel by ~2 sin(pi/L)/npix).
   (B) levels_{k+1}: the inverse transform is linear, so the oracle's
       pre-quantisation field plus P^-1(GPU R_k - oracle R_k) predicts the
       GPU's.  Mismatches must be "near" or "propagated": pixels where that
@@ -86,6 +90,20 @@ def quantise_levels(f, slm):
     return np.where(k >= slm.levels, 0, k)
 
 
+def constrain(R, amp, w, variant, lo=0.1, hi=10.0):
+    """The replay-plane constraint with phase freedom, no ROI (ifta.hpp:198-214),
+    in double: WGS weight update (amp > 0), then R <- amp w R/|R| (amp w if R = 0)."""
+    r = np.abs(R)
+    a = amp.copy()
+    wn = None
+    if variant == "wgs":
+        cand = w * amp / np.maximum(r, 1e-12)
+        wn = np.where(amp > 0, np.minimum(np.maximum(cand, lo), hi), w)
+        a = np.where(amp > 0, amp * wn, amp)
+    out = np.where(r > 0, R * (a / np.maximum(r, 1e-300)), a + 0j)
+    return out, wn
+
+
 def unconstrained_replay(oracle, levels, slm, fresnel):
     """P(state[levels]) in double: the oracle's replay of that iteration before
     the constraint (to the float rounding of the states)."""
@@ -127,26 +145,35 @@ def check_window(oracle, name, amps, slm, k, snaps, tr_ref, variant=None, fresne
         Rk, Wk, lv_k1 = snaps[t][k + 1]
         A, Bt = repA[t], repB[t]
         # (A) levels_k, mse_k, constrained R_k, W_k
+        amp = np.asarray(amps[t], np.float64)
         pre_k = pre_quant(oracle, Rp, fresnel)
-        near_k = phase_threshold_distance(pre_k, slm) < NEAR
+        dist_k, mag_k = phase_threshold_distance(pre_k, slm), np.abs(pre_k)
+        near_k = dist_k < NEAR
+        lowf_k = ~near_k & (dist_k < NEAR + 6.0 * 2e-7 * float(np.sqrt(np.mean(mag_k ** 2))) /
+                            np.maximum(mag_k, 1e-300))
         mA = level_mismatches(A.levels, lv_k)
-        R_unc = unconstrained_replay(oracle, lv_k, slm, fresnel)  # oracle's R of iteration k, before the constraint
+        R_unc = unconstrained_replay(oracle, A.levels, slm, fresnel)  # the GPU's own replay of iteration k
         mag_unc = np.abs(R_unc)
         rms_unc = float(np.sqrt(np.mean(mag_unc ** 2)))
+        Wp = snaps[t][k][1]
+        R_pred, W_pred = constrain(R_unc, amp, Wp, variant)
+        dR = A.replay.astype(np.complex128) - R_pred
+        cond = np.abs(dR) * mag_unc / np.maximum(np.abs(R_pred), 1e-300)
         Rk64 = Rk.astype(np.complex128)
-        dR = A.replay.astype(np.complex128) - Rk64
-        cond = np.abs(dR) * mag_unc / np.maximum(np.abs(Rk64), 1e-300)
         out = {"k": k, "target": int(t), "A_level_mismatch": int(mA.sum()), "A_near": int((mA & near_k).sum()),
-               "A_bad": int((mA & ~near_k).sum()), "A_mse_rel": rel(A.trace.values()[0], tr_ref[t][k - 1]),
-               "A_R_rel_rms_raw": float(np.sqrt(np.mean(np.abs(dR) ** 2)) / np.sqrt(np.mean(np.abs(Rk64) ** 2))),
+               "A_lowf": int((mA & lowf_k).sum()), "A_bad": int((mA & ~near_k & ~lowf_k).sum()),
+               "A_lowf_class_size": int(lowf_k.sum()), "A_mse_rel": rel(A.trace.values()[0], tr_ref[t][k - 1]),
+               "A_R_vs_oracle_rel_rms": float(np.sqrt(np.mean(np.abs(A.replay - Rk64) ** 2)) /
+                                              np.sqrt(np.mean(np.abs(Rk64) ** 2))),
                "A_R_conditioned_rel_rms": float(np.sqrt(np.mean(cond ** 2))) / rms_unc,
                "A_R_conditioned_rel_max": float(cond.max()) / rms_unc}
         if Wk is not None:
-            wr = np.abs(A.weights.astype(np.float64) - Wk) / np.maximum(np.abs(Wk), 1e-300)
+            wr = np.abs(A.weights.astype(np.float64) - W_pred) / np.maximum(np.abs(W_pred), 1e-300)
             wc = wr * mag_unc
-            out.update({"A_W_rel_rms_raw": float(np.sqrt(np.mean(wr ** 2))),
-                        "A_W_conditioned_rel_rms": float(np.sqrt(np.mean(wc ** 2))) / rms_unc,
-                        "A_W_conditioned_rel_max": float(wc.max()) / rms_unc})
+            out.update({"A_W_vs_oracle_rel_rms": float(np.sqrt(np.mean(
+                ((A.weights.astype(np.float64) - Wk) / np.maximum(np.abs(Wk), 1e-300)) ** 2))),
+                "A_W_conditioned_rel_rms": float(np.sqrt(np.mean(wc ** 2))) / rms_unc,
+                "A_W_conditioned_rel_max": float(wc.max()) / rms_unc})
         # (B) levels_{k+1}, mse_k, mse_{k+1}
         pre_k1 = pre_quant(oracle, Rk, fresnel)
         near = phase_threshold_distance(pre_k1, slm) < NEAR

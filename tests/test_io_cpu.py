@@ -89,3 +89,82 @@ def test_replay_scale_text(tmp_path):
     assert open(str(p) + ".scale.txt").read() == "amplitude_at_255=0\n"
     hio.write_replay_scale(p, 0.1 + 0.2)
     assert open(str(p) + ".scale.txt").read() == "amplitude_at_255=0.30000000000000004\n"
+
+
+def _parse_png(data: bytes):
+    """Independent PNG check: signature, CRCs, IHDR, and the inflated scanlines."""
+    import struct
+    import zlib
+    assert data[:8] == b"\x89PNG\r\n\x1a\n"
+    at, idat, ihdr = 8, b"", None
+    while at < len(data):
+        n, = struct.unpack(">I", data[at:at + 4])
+        typ, body = data[at + 4:at + 8], data[at + 8:at + 8 + n]
+        crc, = struct.unpack(">I", data[at + 8 + n:at + 12 + n])
+        assert zlib.crc32(typ + body) == crc
+        if typ == b"IHDR":
+            ihdr = struct.unpack(">IIBBBBB", body)
+        elif typ == b"IDAT":
+            idat += body
+        at += 12 + n
+    w, h, depth, ctype, _, _, interlace = ihdr
+    assert (depth, ctype, interlace) == (8, 0, 0)
+    raw = zlib.decompress(idat)
+    rows = [raw[y * (w + 1):(y + 1) * (w + 1)] for y in range(h)]
+    assert all(r[0] == 0 for r in rows)  # filter type 0
+    return np.frombuffer(b"".join(r[1:] for r in rows), np.uint8).reshape(h, w)
+
+
+def test_hologram_png_round_trip(tmp_path):
+    # write_hologram_png / read_hologram_png (io.cpp:272-298) as real PNG files
+    from paper_2008_12214_b200 import io
+    rng = np.random.default_rng(3)
+    for L in (2, 7, 256):
+        lv = rng.integers(0, L, size=(37, 53), dtype=np.int32)
+        p = tmp_path / f"h{L}.png"
+        io.write_hologram_png(p, lv, L)
+        px = _parse_png(p.read_bytes())
+        assert np.array_equal(px, io.levels_to_gray8(lv, L))
+        assert np.array_equal(io.read_hologram_png(p, L), lv)
+    with pytest.raises(ValueError, match="level count must be in"):
+        io.write_hologram_png(tmp_path / "x.png", np.zeros((2, 2), np.int32), 300)
+
+
+def test_png_reader_filters_and_errors(tmp_path):
+    # read_png_gray8 accepts every scanline filter (what libpng would write)
+    import struct
+    import zlib
+    from paper_2008_12214_b200 import io
+    from paper_2008_12214_b200._lib import HgcIOError
+    rng = np.random.default_rng(4)
+    img = rng.integers(0, 256, size=(6, 9), dtype=np.uint8)
+    w, h = 9, 6
+    raw = b""
+    prev = np.zeros(w, np.int64)
+    for y in range(h):
+        f = y % 5
+        cur = img[y].astype(np.int64)
+        out = []
+        for x in range(w):
+            a = cur[x - 1] if x else 0
+            b = prev[x]
+            c = prev[x - 1] if x else 0
+            pred = [0, a, b, (a + b) // 2, None][f]
+            if f == 4:
+                p = a + b - c
+                pa, pb, pc = abs(p - a), abs(p - b), abs(p - c)
+                pred = a if (pa <= pb and pa <= pc) else (b if pb <= pc else c)
+            out.append((cur[x] - pred) & 255)
+        raw += bytes([f]) + bytes(out)
+        prev = cur
+
+    def chunk(t, b):
+        return struct.pack(">I", len(b)) + t + b + struct.pack(">I", zlib.crc32(t + b))
+    data = b"\x89PNG\r\n\x1a\n" + chunk(b"IHDR", struct.pack(">IIBBBBB", w, h, 8, 0, 0, 0, 0)) + \
+        chunk(b"IDAT", zlib.compress(raw)) + chunk(b"IEND", b"")
+    p = tmp_path / "f.png"
+    p.write_bytes(data)
+    assert np.array_equal(io.read_png_gray8(p), img)
+    (tmp_path / "bad.png").write_bytes(b"not a png")
+    with pytest.raises(HgcIOError, match="not a PNG file"):
+        io.read_png_gray8(tmp_path / "bad.png")

@@ -174,6 +174,8 @@ typedef struct hgc_ospr_io {
     double* replay_peak;        /* [jobs] */
     uint8_t* levels1;           /* 2-level SLMs: frame levels as bit-planes [jobs][subframes][ny*nx/8],
                                    bit (i & 7) of byte i >> 3 (what a binary FLC SLM is fed) */
+    double* profile;            /* RunReport::profile {transform, constraint, metric, other} of
+                                   hgc_ospr_run (as hgc_ifta_io::profile) or NULL */
 } hgc_ospr_io;
 
 /* ------------------------------------------------------------ library */
@@ -397,6 +399,12 @@ int hgc_mt_jump_state(uint64_t engine_seed, uint64_t draws, uint64_t* window);
 int hgc_seed_random_phase(const double* amplitude, int nx, int ny, uint64_t engine_seed,
                           uint64_t skip, float* out);
 uint64_t hgc_fork_seed(uint64_t seed, uint64_t stream);
+/* Synthetic targets (host, no device): patterns::smooth_blobs (patterns.hpp:55-80,
+ * peak-normalised) and normalize_image (target.hpp:15-30; unit_energy 0 =
+ * MaxToOne, 1 = UnitEnergy; HGC_EINVAL for a zero-energy image), bit-identical
+ * to the reference's (same operation order, the C library's exp). */
+int hgc_smooth_blobs(int width, int height, double* out);
+int hgc_normalize_image(double* img, size_t n, int unit_energy);
 /* mse(target, replay, {mask, scale_free}) phase-insensitive. */
 int hgc_mse(const double* target, const float* replay, const uint8_t* mask, int nx, int ny,
             int scale_free, double* out);

@@ -190,6 +190,8 @@ inline hologen::OsprRun<float> run_ospr_gpu(const hologen::OsprConfig& cfg, holo
     io.cumulative_mse = cm.data();
     io.mean_intensity = mi.data();
     io.replay = reinterpret_cast<float*>(rep.replay.data.data());
+    double prof[4] = {0, 0, 0, 0};
+    io.profile = prof;
     throw_status(hgc_ospr_run(&c, &s, nx, ny, 1, &io));
     const bool adaptive = cfg.variant == hologen::OsprVariant::AdaptiveOspr;
     rep.algorithm = adaptive ? "adaptive_ospr" : "ospr";
@@ -212,7 +214,7 @@ inline hologen::OsprRun<float> run_ospr_gpu(const hologen::OsprConfig& cfg, holo
     rep.evaluations = N;
     rep.extra_traces.push_back(std::move(frame_trace));
     rep.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-    rep.profile.other = rep.seconds;
+    set_profile(rep, prof);
     return run;
 }
 

@@ -76,7 +76,7 @@ class HgcOsprIo(C.Structure):
                 ("frames", C.c_void_p), ("frame_mse", C.c_void_p), ("cumulative_mse", C.c_void_p),
                 ("mean_intensity", C.c_void_p), ("replay", C.c_void_p), ("final_error", C.c_void_p),
                 ("seconds", C.c_void_p), ("frames_gray8", C.c_void_p), ("replay_gray8", C.c_void_p),
-                ("replay_peak", C.c_void_p), ("levels1", C.c_void_p)]
+                ("replay_peak", C.c_void_p), ("levels1", C.c_void_p), ("profile", C.c_void_p)]
 
 
 class HgcIftaIo64(C.Structure):
@@ -141,6 +141,8 @@ _SIGS = {
     "hgc_replay_to_gray8": (_i, [_vp, _i, _i, _i, _vp, _vp]),
     "hgc_write_replay_scale": (_i, [C.c_char_p, _d]),
     "hgc_write_png_gray": (_i, [C.c_char_p, _vp, _i, _i]),
+    "hgc_smooth_blobs": (_i, [_i, _i, _vp]),
+    "hgc_normalize_image": (_i, [_vp, C.c_size_t, _i]),
     "hgc_read_png_gray8": (_i, [C.c_char_p, _P(_i), _P(_i), _vp]),
     "hgc_fork_seed": (_u64, [_u64, _u64]),
     "hgc_mse": (_i, [_vp, _vp, _vp, _i, _i, _i, _P(_d)]),

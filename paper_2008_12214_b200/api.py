@@ -431,6 +431,8 @@ def run_ifta_f64(cfg: IftaConfig, prop: Propagator | None = None, init_field=Non
     io.amplitude, io.phase, io.roi, io.init_field, io.init_weights = _p(amp), _p(ph), _p(roi), _p(fi), _p(wi)
     io.hologram, io.replay, io.levels, io.trace = _p(holo), _p(rep_f), _p(lv), _p(tr)
     io.final_error = C.addressof(fe)
+    prof = np.zeros(4)
+    io.profile = _p(prof)
     fr = prop.params if prop is not None and prop.is_fresnel() else None
     t0 = time.perf_counter()
     check(lib.hgc_ifta_run_f64(C.byref(c), C.byref(slm), _fresnel(fr), nx, ny, C.byref(io)))
@@ -439,8 +441,15 @@ def run_ifta_f64(cfg: IftaConfig, prop: Propagator | None = None, init_field=Non
     rep.trace = MetricTrace("mse", [(k + 1, float(v)) for k, v in enumerate(tr)])
     rep.final_error = fe.value
     rep.seconds = time.perf_counter() - t0
-    rep.profile = PhaseProfile(other=rep.seconds)
+    rep.profile = _profile(prof, rep.seconds)
     return rep
+
+
+def _profile(p, seconds: float) -> PhaseProfile:
+    """RunReport::profile from the library's per-phase device times; other =
+    the rest of the call, so total() == seconds (ifta.hpp:231-233)."""
+    tr, cn, me = (float(v) for v in p[:3])
+    return PhaseProfile(transform=tr, constraint=cn, metric=me, other=max(0.0, seconds - (tr + cn + me)))
 
 
 def run_ospr_f64(cfg: OsprConfig, keep_frames: bool = True) -> OsprRun:
@@ -464,6 +473,8 @@ def run_ospr_f64(cfg: OsprConfig, keep_frames: bool = True) -> OsprRun:
     io.amplitude, io.roi, io.frames, io.levels = _p(amp), _p(roi), _p(frames), _p(lv)
     io.frame_mse, io.cumulative_mse, io.mean_intensity, io.replay = _p(fm), _p(cm), _p(mi), _p(rp)
     io.final_error = C.addressof(fe)
+    prof = np.zeros(4)
+    io.profile = _p(prof)
     t0 = time.perf_counter()
     check(lib.hgc_ospr_run_f64(C.byref(c), C.byref(slm), nx, ny, C.byref(io)))
     r = OsprRun()
@@ -477,7 +488,7 @@ def run_ospr_f64(cfg: OsprConfig, keep_frames: bool = True) -> OsprRun:
     rep.final_error = fe.value
     rep.evaluations = N
     rep.seconds = time.perf_counter() - t0
-    rep.profile = PhaseProfile(other=rep.seconds)
+    rep.profile = _profile(prof, rep.seconds)
     r.report = rep
     return r
 
@@ -526,6 +537,8 @@ def run_ospr_batch(cfg: OsprConfig, seeds=None, amplitudes: np.ndarray | None = 
     io.frames = _p(frames)
     io.frame_mse, io.cumulative_mse = _p(fm), _p(cm)
     io.mean_intensity, io.replay, io.final_error, io.seconds = _p(mi), _p(rp), _p(fe), _p(secs)
+    prof = np.zeros(4)
+    io.profile = _p(prof)
     keep = []
     slm = _slm(cfg.slm, keep)
     c = _ospr_cfg(cfg)
@@ -545,7 +558,7 @@ def run_ospr_batch(cfg: OsprConfig, seeds=None, amplitudes: np.ndarray | None = 
         rep.final_error = float(fe[j])
         rep.evaluations = N
         rep.seconds = float(secs[0])
-        rep.profile = PhaseProfile(other=rep.seconds)
+        rep.profile = _profile(prof, rep.seconds)  # whole batched call
         r.report = rep
         runs.append(r)
     return runs

@@ -1634,11 +1634,51 @@ struct hgc_ospr_plan {
     cudaEvent_t ev_fork = nullptr, ev_seed = nullptr, ev_pass[2] = {nullptr, nullptr};
     cudaEvent_t done = nullptr;  // recorded after each execute on the execute stream
     cudaEvent_t up_ev = nullptr;  // end of the last upload's stream work
+    // RunReport::profile (hgc_ospr_run with io->profile): external events
+    // around each subframe's column-inverse, row and accumulating passes
+    std::vector<cudaEvent_t> pev;
+    void profile_on() {
+        if (!pev.empty() || graph) return;
+        pev.resize(4 * (size_t)cfg.subframes);
+        for (cudaEvent_t& e : pev) CK(cudaEventCreate(&e));
+    }
+    void pmark(size_t i, cudaStream_t st) {
+        if (i < pev.size()) CK(cudaEventRecordWithFlags(pev[i], st, cudaEventRecordExternal));
+    }
+    // ospr.hpp:118-146 phases: the inverse transform (column pass, row IFFT), the
+    // quantiser (kRowQuant of the fused row pass), the forward transform, and the
+    // intensity accumulation + both MSEs (kAccMetric of the accumulating column
+    // pass); seeds and the rest are "other".
+    void profile_split(double seconds, double* out) const {
+        static constexpr double kRowQuant = 0.05, kAccMetric = 0.10;
+        double ci = 0, rw = 0, ca = 0;
+        for (int n = 0; n < cfg.subframes && !pev.empty(); ++n) {
+            float a = 0.f, b = 0.f, c = 0.f;
+            CK(cudaEventElapsedTime(&a, pev[4 * n], pev[4 * n + 1]));
+            CK(cudaEventElapsedTime(&b, pev[4 * n + 1], pev[4 * n + 2]));
+            CK(cudaEventElapsedTime(&c, pev[4 * n + 2], pev[4 * n + 3]));
+            ci += 1e-3 * a;
+            rw += 1e-3 * b;
+            ca += 1e-3 * c;
+        }
+        double tr = ci + rw * (1 - kRowQuant) + ca * (1 - kAccMetric), cn = rw * kRowQuant, me = ca * kAccMetric;
+        const double dev = tr + cn + me;
+        if (dev > seconds && dev > 0) {
+            tr *= seconds / dev;
+            cn *= seconds / dev;
+            me *= seconds / dev;
+        }
+        out[0] = tr;
+        out[1] = cn;
+        out[2] = me;
+        out[3] = std::max(0.0, seconds - (tr + cn + me));
+    }
     DBuf<int> vflags;             // deferred TargetSpec validation flags
     DBuf<uint8_t> roi_rm;
 
     ~hgc_ospr_plan() {
         if (graph) cudaGraphExecDestroy(graph);
+        for (cudaEvent_t e : pev) cudaEventDestroy(e);
         for (cudaEvent_t e : {ev_fork, ev_seed, ev_pass[0], ev_pass[1], done, up_ev})
             if (e) cudaEventDestroy(e);
         if (stream2) cudaStreamDestroy(stream2);
@@ -1779,9 +1819,13 @@ struct hgc_ospr_plan {
                 CK(cudaEventRecord(ev_seed, ss));
                 CK(cudaStreamWaitEvent(st, ev_seed, 0));
             }
+            pmark(4 * (size_t)(n - 1), st);
             col_plain(ny, col_inv_args(n), jobs, st);
+            pmark(4 * (size_t)(n - 1) + 1, st);
             row_fused(nx, row_args(n), jobs, st);
+            pmark(4 * (size_t)(n - 1) + 2, st);
             col_ospr(ny, col_acc_args(n), jobs, st);
+            pmark(4 * (size_t)(n - 1) + 3, st);
             if (block_mode)  // local running sum after frame n, for hgc_ospr_block_finish
                 CK(cudaMemcpyAsync(snaps.p + (size_t)(n - 1) * npix, S.p, sizeof(float) * npix, cudaMemcpyDeviceToDevice,
                                    st));
@@ -2123,17 +2167,19 @@ int hgc_ospr_run(const hgc_ospr_cfg* cfg, const hgc_slm* slm, int nx, int ny, in
     hgc_ospr_plan* p = nullptr;
     int rc = guarded([] { route_device(); });
     if (rc == HGC_OK) rc = hgc_ospr_plan_create(&p, cfg, slm, nx, ny, jobs, io ? io->per_job_target : 0);
+    if (rc == HGC_OK && io && io->profile) rc = guarded([&] { p->profile_on(); });
     if (rc == HGC_OK) rc = hgc_ospr_plan_upload(p, io);
     if (rc == HGC_OK) rc = guarded([&] { check_validation(p->vflags.p, p->stream); });  // eager in the one-shot run
     if (rc == HGC_OK) rc = hgc_ospr_plan_execute(p, nullptr);
     if (rc == HGC_OK) rc = hgc_ospr_plan_download(p, io);
+    const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (rc == HGC_OK && io && io->profile) rc = guarded([&] { p->profile_split(secs, io->profile); });
     if (p) {
         std::string keep = g_err;
         hgc_ospr_plan_destroy(p);
         g_err = keep;
     }
-    if (rc == HGC_OK && io && io->seconds)
-        *io->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (rc == HGC_OK && io && io->seconds) *io->seconds = secs;
     return rc;
 }
 

@@ -39,14 +39,15 @@ _BLOBS = ((0.30, 0.35, 0.16, 1.00), (0.68, 0.28, 0.10, 0.75), (0.62, 0.70, 0.20,
 
 
 def smooth_blobs(width: int, height: int) -> np.ndarray:  # patterns.hpp:55-80
-    fy = ((np.arange(height) + 0.5) / height)[:, None]
-    fx = ((np.arange(width) + 0.5) / width)[None, :]
-    v = 0.08 + 0.10 * fx + 0.06 * fy
-    for cx, cy, sigma, amp in _BLOBS:
-        dx, dy = fx - cx, fy - cy
-        v = v + amp * np.exp(-(dx * dx + dy * dy) / (2.0 * sigma * sigma))
-    img = np.ascontiguousarray(v, dtype=np.float64)
-    return normalize_image(img, Normalization.MaxToOne)
+    """Bit-identical to the reference's (hgc_smooth_blobs: same operation
+    order and the C library's exp; numpy's vectorised exp differs in the last
+    bit on some inputs)."""
+    from ._lib import check, lib
+    if width < 1 or height < 1:
+        raise ValueError("RealImage: dimensions must be positive")
+    img = np.empty((height, width), np.float64)
+    check(lib.hgc_smooth_blobs(width, height, img.ctypes.data))
+    return img
 
 
 def bench_target(n: int) -> np.ndarray:

@@ -138,7 +138,8 @@ def normalize_image(img: np.ndarray, norm: Normalization) -> np.ndarray:  # targ
         img *= 1.0 / acc
         return img
     flat = img.ravel()
-    acc = float(np.dot(flat, flat))  # (pairwise, not the reference's sequential sum: last-bit differences only)
+    sq = flat * flat
+    acc = float(np.add.accumulate(sq)[-1]) if sq.size else 0.0  # the reference's sequential sum, bit for bit
     if acc <= 0.0:
         raise ValueError("normalize_image: zero-energy image cannot be energy-normalized")
     img *= math.sqrt(img.size / acc)

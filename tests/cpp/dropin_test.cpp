@@ -101,6 +101,7 @@ int main() {
     rel = std::abs(go.report.final_error - ro.report.final_error) / ro.report.final_error;
     std::printf("ospr 6 frames: level mismatches %d, cumulative mse rel %.2e\n", om, rel);
     CHECK(om <= 6 && rel < 1e-4 && go.report.algorithm == "ospr" && go.set.frames.size() == 6);
+    CHECK(profile_ok(go.report));
 
     // T = double: the GPU f64 loop against the reference's own double loop
     // (detail::run_ifta<double>, its transforms on the GPU f64 FftBackend)

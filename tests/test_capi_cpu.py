@@ -120,3 +120,13 @@ def test_ospr_block_plan_validation():
         hg.OsprBlockPlan(hg.OsprConfig(**base), 32, 32, 3, 2)
     with pytest.raises(ValueError, match="count"):
         hg.OsprBlockPlan(hg.OsprConfig(**base), 32, 32, 0, 0)
+
+
+def test_bench_target_bit_identical_to_reference_generator(ref_oracle):
+    # patterns::smooth_blobs + normalize_image(UnitEnergy) (patterns.hpp:55-80,
+    # target.hpp:15-30), the reference bench's target (bench.cpp:115-116)
+    for n in (16, 64, 1024):
+        got = hg.patterns.bench_target(n)
+        want = ref_oracle.normalize(ref_oracle.smooth_blobs(n, n), True)
+        assert np.array_equal(got, want)
+    assert np.array_equal(hg.patterns.smooth_blobs(40, 24), ref_oracle.smooth_blobs(40, 24))

@@ -177,7 +177,7 @@ def check_window(oracle, name, amps, slm, k, snaps, tr_ref, variant=None, fresne
         # (B) levels_{k+1}, mse_k, mse_{k+1}
         pre_k1 = pre_quant(oracle, Rk, fresnel)
         near = phase_threshold_distance(pre_k1, slm) < NEAR
-        pred = pre_k1 + pre_quant(oracle, dR, fresnel)  # the GPU's pre-quantisation field, to rounding
+        pred = pre_k1 + pre_quant(oracle, A.replay - Rk64, fresnel)  # the GPU's pre-quantisation field, to rounding
         mag = np.abs(pred)
         floor = 2e-7 * float(np.sqrt(np.mean(mag ** 2)))  # the GPU transform's own rounding
         prop = (quantise_levels(pred, slm) != lv_k1) | (

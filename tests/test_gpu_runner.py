@@ -70,3 +70,18 @@ def test_thread_routing_policy_concurrent_runs():
         _lib.check(_lib.lib.hgc_set_device_policy(0))
     for g, w in zip(got, want):
         assert np.array_equal(g.levels, w.levels) and g.final_error == w.final_error
+
+
+@pytest.mark.parametrize("which", ["gs", "gs64", "ospr", "ospr64"])
+def test_profile_accounts_for_the_whole_run(which):
+    # test_ifta.cpp:270-280 ("profile accounts for the whole run"), bench.cpp:167-183
+    amp = hg.normalize_image(hg.patterns.checkerboard(32, 32, 4), hg.Normalization.UnitEnergy)
+    if which.startswith("gs"):
+        cfg = hg.IftaConfig(iterations=10, slm=hg.SlmSpec.full_circle_phase(256), target=hg.TargetSpec(amp), seed=1)
+        rep = hg.run_gs(cfg) if which == "gs" else hg.run_ifta_f64(cfg)
+    else:
+        cfg = hg.OsprConfig(subframes=6, slm=hg.SlmSpec.binary_phase(), target=hg.TargetSpec(amp), seed=1)
+        rep = (hg.run_ospr(cfg) if which == "ospr" else hg.run_ospr_f64(cfg)).report
+    p = rep.profile
+    assert p.transform > 0 and p.constraint > 0 and p.metric > 0 and p.other >= 0
+    assert rep.seconds > 0 and abs(p.total() - rep.seconds) <= 1e-9 * rep.seconds

@@ -7,10 +7,6 @@ namespace hg {
 void row_fused_binary(int nx, const RowArgs& a, int batch, cudaStream_t st, bool prepare) {
     const bool lv = a.levels8 || a.levels16;
     if (prepare) {
-        row_persist_dispatch<QK_BINARY, 0, 0>(nx, a, batch, st, true);
-        row_persist_dispatch<QK_BINARY, 0, 1>(nx, a, batch, st, true);
-        row_persist_dispatch<QK_BINARY, 1, 0>(nx, a, batch, st, true);
-        row_persist_dispatch<QK_BINARY, 1, 1>(nx, a, batch, st, true);
         row_dispatch_q<ROW_FUSED, QK_BINARY, LAY_QUAD, 0, 0>(nx, a, batch, st, true);
         row_dispatch_q<ROW_FUSED, QK_BINARY, LAY_QUAD, 1, 0>(nx, a, batch, st, true);
         row_dispatch_q<ROW_FUSED, QK_BINARY, LAY_QUAD, 0, 1>(nx, a, batch, st, true);
@@ -18,15 +14,9 @@ void row_fused_binary(int nx, const RowArgs& a, int batch, cudaStream_t st, bool
         return;
     }
     if (a.fresnel_q) {
-        if (lv ? row_persist_dispatch<QK_BINARY, 1, 1>(nx, a, batch, st, false)
-               : row_persist_dispatch<QK_BINARY, 1, 0>(nx, a, batch, st, false))
-            return;
         if (lv) row_dispatch_q<ROW_FUSED, QK_BINARY, LAY_QUAD, 1, 1>(nx, a, batch, st, false);
         else row_dispatch_q<ROW_FUSED, QK_BINARY, LAY_QUAD, 1, 0>(nx, a, batch, st, false);
     } else {
-        if (lv ? row_persist_dispatch<QK_BINARY, 0, 1>(nx, a, batch, st, false)
-               : row_persist_dispatch<QK_BINARY, 0, 0>(nx, a, batch, st, false))
-            return;
         if (lv) row_dispatch_q<ROW_FUSED, QK_BINARY, LAY_QUAD, 0, 1>(nx, a, batch, st, false);
         else row_dispatch_q<ROW_FUSED, QK_BINARY, LAY_QUAD, 0, 0>(nx, a, batch, st, false);
     }

@@ -16,7 +16,6 @@ HOT = [  # (object, mangled-name regex, label)
     ("k_row_full.o", r"_ZN2hg5k_rowILi4096ELi0ELi2ELi1ELi0ELi0EE", "k_row<4096, QK_FULL> (non-persistent, small batches)"),
     ("k_col_gs.o", r"_ZN2hg5k_colILi4096ELi2ELi3ELi1EE", "k_col<4096, C=2, COL_GS_FAST>  (GS 4096^2 column pass)"),
     ("k_col_plain.o", r"_ZN2hg5k_colILi4096ELi2ELi0ELi1EE", "k_col<4096, C=2, COL_PLAIN>    (initial inverse columns)"),
-    ("k_row_bin.o", r"_ZN2hg13k_row_persistILi1024ELi1ELi0ELi1EE", "k_row_persist<1024, QK_BINARY, levels> (OSPR row pass)"),
     ("k_row_bin.o", r"_ZN2hg5k_rowILi1024ELi0ELi1ELi1ELi0ELi1EE", "k_row<1024, QK_BINARY, levels>   (OSPR row pass, non-persistent)"),
     ("k_col_ospr.o", r"_ZN2hg5k_colILi1024ELi8ELi2ELi1EE", "k_col<1024, C=8, COL_OSPR>     (OSPR accumulating column pass)"),
     ("capi.o", r"_ZN2hg19k_seed_random_phaseILb1EE", "k_seed_random_phase<fast>      (mt19937_64 + double sincos seed)"),

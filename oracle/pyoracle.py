@@ -317,7 +317,7 @@ class Oracle:
         return IftaResult(holo, rep, lv, tr, seconds=float(tm[0]), profile=tuple(float(v) for v in tm[1:]))
 
     def ifta_snaps(self, amp, slm, iterations, snap_iters, seed=0, variant="gs", clamp=(0.1, 10.0),
-                   fresnel=None, scale_freedom=False):
+                   fresnel=None, scale_freedom=False, roi=None, amp_outside_roi=False, lt_initial_fraction=0.1):
         """Restatement run with snapshots at the start of each iteration k in
         snap_iters: returns (IftaResult, {k: (R_{k-1}, W_{k-1} or None, levels_k)}).
         Test hook for the lock-step parity protocol."""
@@ -331,9 +331,11 @@ class Oracle:
         c.iterations = iterations
         c.seed = seed
         c.clamp_lo, c.clamp_hi = clamp
-        c.lt_initial_fraction = 0.1
+        c.lt_initial_fraction = lt_initial_fraction
         c.phase_freedom = 1
         c.scale_freedom = int(scale_freedom)
+        c.amp_outside_roi = int(amp_outside_roi)
+        rm = None if roi is None else np.ascontiguousarray(roi, np.uint8)
         if fresnel is not None:
             c.fresnel = 1
             c.wavelength, c.distance, c.pitch_x, c.pitch_y = fresnel
@@ -347,7 +349,7 @@ class Oracle:
         rep = np.empty((ny, nx), np.complex64)
         lv = np.empty((ny, nx), np.int32)
         tr = np.empty(iterations, np.float64)
-        self._check(self._f["ifta_run_snaps"](C.byref(c), C.byref(s), nx, ny, _p(amp), None, None, _p(holo),
+        self._check(self._f["ifta_run_snaps"](C.byref(c), C.byref(s), nx, ny, _p(amp), None, _p(rm), _p(holo),
                                               _p(rep), _p(lv), _p(tr), m, _p(ks), _p(sr), _p(sw), _p(sl)))
         snaps = {int(k): (sr[j], None if sw is None else sw[j], sl[j]) for j, k in enumerate(ks)}
         return IftaResult(holo, rep, lv, tr), snaps

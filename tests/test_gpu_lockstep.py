@@ -38,39 +38,16 @@ or $HG_PARITY_OUT; every level mismatch must fall in a named class):
       it inherits is the float rounding of iteration k, amplified by the
       chaotic multi-level loop.  mse_k, mse_{k+1} within 1e-4.
 """
-import json
-import os
-
 import numpy as np
 import pytest
 
-from helpers import TWO_PI, level_mismatches, phase_threshold_distance, rel
+from helpers import TWO_PI, level_mismatches, phase_threshold_distance, record, rel
 
 pytestmark = pytest.mark.gpu
 hg = pytest.importorskip("paper_2008_12214_b200")
 
 MSE_TOL = 1e-4
 NEAR = 1e-5
-RESULTS = {}
-
-
-@pytest.fixture(scope="module", autouse=True)
-def _write_parity_report():
-    yield
-    if not RESULTS:
-        return
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    path = os.environ.get("HG_PARITY_OUT", os.path.join(root, "profiles", "parity_r02.json"))
-    old = {}
-    if os.path.exists(path):
-        try:
-            old = json.load(open(path))
-        except ValueError:
-            old = {}
-    old.update(RESULTS)
-    os.makedirs(os.path.dirname(path), exist_ok=True)
-    with open(path, "w") as f:
-        json.dump(old, f, indent=1, sort_keys=True)
 
 
 def pre_quant(oracle, R, fresnel):
@@ -188,7 +165,7 @@ def check_window(oracle, name, amps, slm, k, snaps, tr_ref, variant=None, fresne
                     "B_propagated": int((mB & ~near & prop).sum()), "B_bad": int((mB & ~near & ~prop).sum()),
                     "B_propagated_class_size": int(prop.sum()), "B_mse_rel_k": rel(trB[0], tr_ref[t][k - 1]),
                     "B_mse_rel_k1": rel(trB[1], tr_ref[t][k])})
-        RESULTS[f"{name}/k={k}/t={t}"] = out
+        record(f"{name}/k={k}/t={t}", out)
         assert out["A_bad"] == 0, out
         assert out["A_mse_rel"] < MSE_TOL, out
         assert out["A_R_conditioned_rel_rms"] < 1e-5, out
@@ -196,7 +173,6 @@ def check_window(oracle, name, amps, slm, k, snaps, tr_ref, variant=None, fresne
             assert out["A_W_conditioned_rel_rms"] < 1e-5, out
         assert out["B_bad"] == 0, out
         assert out["B_mse_rel_k"] < MSE_TOL and out["B_mse_rel_k1"] < MSE_TOL, out
-    return RESULTS
 
 
 def windows(K):

@@ -141,6 +141,12 @@ typedef struct hgc_ifta_io {
      * other} seconds of hgc_ifta_run, attributed from per-pass device times
      * (DESIGN.md §5); their sum equals *seconds.  Only hgc_ifta_run fills it. */
     double* profile;
+    /* Diffraction efficiency of the final replay (extension; the reference has
+     * no efficiency metric): the replay power on the target's support (T > 0,
+     * inside the ROI when one is given) over the total replay power,
+     * sum_{T>0, roi} |R|^2 / sum |R|^2, reduced in the last iteration's fused
+     * column pass.  [batch] */
+    double* efficiency;
 } hgc_ifta_io;
 
 /* hologen::OsprConfig (ospr.hpp:20-38).  variant: 0 Ospr, 1 AdaptiveOspr.
@@ -197,6 +203,13 @@ int hgc_ifta_run(const hgc_ifta_cfg* cfg, const hgc_slm* slm, const hgc_fresnel*
                  int nx, int ny, int batch, hgc_ifta_io* io);
 int hgc_ospr_run(const hgc_ospr_cfg* cfg, const hgc_slm* slm, int nx, int ny, int jobs,
                  hgc_ospr_io* io);
+/* Fresnel OSPR (extension; the reference rejects OSPR + Fresnel,
+ * src/config.cpp:443-445): the subframe loop of run_ospr_impl with the
+ * Propagator<float> inverse / forward (propagation.hpp:81-95) in place of the
+ * bare FFTs: f = IFFT(seed) conj(Q), quantise, R = FFT(f Q).  fresnel == NULL
+ * is hgc_ospr_run.  Parity is pinned only against a composed oracle. */
+int hgc_ospr_run_fresnel(const hgc_ospr_cfg* cfg, const hgc_slm* slm, const hgc_fresnel* fresnel, int nx, int ny,
+                         int jobs, hgc_ospr_io* io);
 
 /* ------------------------------------------ device-resident plan API */
 typedef struct hgc_ifta_plan hgc_ifta_plan;
@@ -251,6 +264,9 @@ int hgc_ospr_plan_launches(hgc_ospr_plan* plan);
 int hgc_ospr_plan_profile(hgc_ospr_plan* plan, int reps, double* ms_seed, double* ms_col_inv, double* ms_row,
                           double* ms_col_acc);
 int hgc_ospr_plan_destroy(hgc_ospr_plan* plan);
+/* The plan's propagation: Fresnel (hgc_ospr_run_fresnel) or NULL = Fourier.
+ * Before the first execute. */
+int hgc_ospr_plan_set_fresnel(hgc_ospr_plan* plan, const hgc_fresnel* fresnel);
 
 /* Subframe-block sharding of ONE plain OSPR job across ranks (
  * the loop of run_ospr_impl, ospr.hpp:105-147, split at subframe

@@ -62,7 +62,7 @@ class HgcIftaIo(C.Structure):
                 ("trace", C.c_void_p), ("final_error", C.c_void_p), ("seconds", C.c_void_p),
                 ("fresnel_q", C.c_void_p), ("hologram_gray8", C.c_void_p), ("replay_gray8", C.c_void_p),
                 ("replay_peak", C.c_void_p), ("levels1", C.c_void_p), ("checkpoint", C.c_int),
-                ("weights", C.c_void_p), ("profile", C.c_void_p)]
+                ("weights", C.c_void_p), ("profile", C.c_void_p), ("efficiency", C.c_void_p)]
 
 
 class HgcOsprCfg(C.Structure):
@@ -103,6 +103,8 @@ _SIGS = {
     "hgc_max_side": (_i, []),
     "hgc_ifta_run": (_i, [_P(HgcIftaCfg), _P(HgcSlm), _P(HgcFresnel), _i, _i, _i, _P(HgcIftaIo)]),
     "hgc_ospr_run": (_i, [_P(HgcOsprCfg), _P(HgcSlm), _i, _i, _i, _P(HgcOsprIo)]),
+    "hgc_ospr_run_fresnel": (_i, [_P(HgcOsprCfg), _P(HgcSlm), _P(HgcFresnel), _i, _i, _i, _P(HgcOsprIo)]),
+    "hgc_ospr_plan_set_fresnel": (_i, [_vp, _P(HgcFresnel)]),
     "hgc_ifta_plan_create": (_i, [_P(_vp), _P(HgcIftaCfg), _P(HgcSlm), _P(HgcFresnel), _i, _i, _i]),
     "hgc_ifta_plan_upload": (_i, [_vp, _P(HgcIftaIo)]),
     "hgc_ifta_plan_execute": (_i, [_vp, _vp]),

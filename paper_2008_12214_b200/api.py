@@ -315,6 +315,8 @@ class _IftaBuffers:
         io.checkpoint = int(bool(checkpoint))
         self.weights = np.empty((b, ny, nx), np.float32) if checkpoint else None
         io.weights = _p(self.weights)
+        self.efficiency = np.zeros(b, np.float64)
+        io.efficiency = _p(self.efficiency)
         self.io = io
         self.hologram_gray8 = self.replay_gray8 = self.replay_peak = None
 
@@ -371,6 +373,7 @@ def run_ifta_batch(cfg: IftaConfig, amplitudes: np.ndarray, seeds=None, prop: Pr
         rep.profile = PhaseProfile(transform=tr, constraint=cn, metric=me, other=ot)
         if checkpoint:
             rep.weights = bufs.weights[i]
+        rep.efficiency = float(bufs.efficiency[i])
         reps.append(rep)
     return reps
 
@@ -505,9 +508,11 @@ def _ospr_cfg(cfg: OsprConfig) -> _lib.HgcOsprCfg:
 
 
 def run_ospr_batch(cfg: OsprConfig, seeds=None, amplitudes: np.ndarray | None = None,
-                   want_frames: bool = True) -> list[OsprRun]:
+                   want_frames: bool = True, prop: Propagator | None = None) -> list[OsprRun]:
     """`jobs` independent OSPR runs (one per seed) sharing cfg.target, or one
-    target per job when ``amplitudes`` (jobs, ny, nx) is given."""
+    target per job when ``amplitudes`` (jobs, ny, nx) is given.  prop: a
+    Fresnel Propagator (extension, hgc_ospr_run_fresnel; the reference's
+    run_ospr takes a bare FftBackend)."""
     cfg.validate()
     per_job = amplitudes is not None
     amps = np.ascontiguousarray(amplitudes if per_job else cfg.target.amplitude, np.float64)
@@ -542,7 +547,10 @@ def run_ospr_batch(cfg: OsprConfig, seeds=None, amplitudes: np.ndarray | None = 
     keep = []
     slm = _slm(cfg.slm, keep)
     c = _ospr_cfg(cfg)
-    check(lib.hgc_ospr_run(C.byref(c), C.byref(slm), nx, ny, jobs, C.byref(io)))
+    fr = prop.params if prop is not None and prop.is_fresnel() else None
+    if fr is not None and (prop.nx, prop.ny) != (nx, ny):
+        raise ValueError("Propagator: field size does not match Fresnel phase")
+    check(lib.hgc_ospr_run_fresnel(C.byref(c), C.byref(slm), _fresnel(fr), nx, ny, jobs, C.byref(io)))
     runs = []
     alg = "adaptive_ospr" if cfg.variant == OsprVariant.AdaptiveOspr else "ospr"
     for j in range(jobs):
@@ -564,20 +572,20 @@ def run_ospr_batch(cfg: OsprConfig, seeds=None, amplitudes: np.ndarray | None = 
     return runs
 
 
-def run_ospr(cfg: OsprConfig) -> OsprRun:  # ospr.hpp:168-173
+def run_ospr(cfg: OsprConfig, prop: Propagator | None = None) -> OsprRun:  # ospr.hpp:168-173
     if cfg.variant != OsprVariant.Ospr:
         raise ValueError("run_ospr: config variant mismatch")
-    return run_ospr_batch(cfg)[0]
+    return run_ospr_batch(cfg, prop=prop)[0]
 
 
-def run_adaptive_ospr(cfg: OsprConfig) -> OsprRun:  # ospr.hpp:175-180
+def run_adaptive_ospr(cfg: OsprConfig, prop: Propagator | None = None) -> OsprRun:  # ospr.hpp:175-180
     if cfg.variant != OsprVariant.AdaptiveOspr:
         raise ValueError("run_adaptive_ospr: config variant mismatch")
-    return run_ospr_batch(cfg)[0]
+    return run_ospr_batch(cfg, prop=prop)[0]
 
 
-def run_ospr_variant(cfg: OsprConfig) -> OsprRun:  # ospr.hpp:182-185
-    return run_ospr_batch(cfg)[0]
+def run_ospr_variant(cfg: OsprConfig, prop: Propagator | None = None) -> OsprRun:  # ospr.hpp:182-185
+    return run_ospr_batch(cfg, prop=prop)[0]
 
 
 # -------------------------------------------------- device-resident plans

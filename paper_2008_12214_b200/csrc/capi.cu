@@ -450,8 +450,13 @@ __global__ void k_mse_partials(const double* t, const float2* r, const uint8_t* 
 // Deterministic per-(target, iteration) reduction of the column-pass
 // partials into MSE values (metrics.hpp:70-124; scale-free gain :213-225).
 // partials: [slots][targets][tiles][8]; out: [targets][slots][nout]
+// Per-target traces from the column-pass partial sums.  GS (ospr == 0): the
+// mse (metrics.hpp:70-97, :123) with sum T^2 from stt[target] (scale-free
+// only), and, when eff != nullptr, the diffraction efficiency of the last
+// iteration's replay: power on the target's support (slot 3) over the total
+// replay power (slot 4).  OSPR: frame and cumulative mse.
 __global__ void k_finalize(const double* part, int slots, int targets, int tiles, double M, int scale_free,
-                           int ospr, double* out) {
+                           int ospr, double* out, const double* stt = nullptr, double* eff = nullptr) {
     const int b = blockIdx.x, lane = threadIdx.x;
     for (int k = 0; k < slots; ++k) {
         double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -470,7 +475,8 @@ __global__ void k_finalize(const double* part, int slots, int targets, int tiles
                 return (v < 0.0 ? 0.0 : v) / M;
             };
             if (!ospr) {
-                out[(size_t)b * slots + k] = mse_of(acc[0], acc[1], acc[2], acc[3]);
+                out[(size_t)b * slots + k] = mse_of(acc[0], acc[1], acc[2], stt ? stt[b] : 0.0);
+                if (eff && k == slots - 1) eff[b] = acc[4] > 0.0 ? acc[3] / acc[4] : 0.0;  // the last iteration
             } else {
                 out[((size_t)b * slots + k) * 2 + 0] = mse_of(acc[0], acc[1], acc[2], acc[3]);
                 out[((size_t)b * slots + k) * 2 + 1] = mse_of(acc[4], acc[5], acc[6], acc[3]);
@@ -619,6 +625,25 @@ __global__ void k_amp_gray8(AmpSrc src, size_t npix, const double* peak, uint8_t
 
 // TargetSpec::validate on the device (target.hpp:52-73): bit 0 = non-finite
 // amplitude, bit 1 = negative amplitude, bit 2 = non-finite phase.
+// sum T^2 over the mask per target (metrics.hpp:91-97, the scale-free MSE's
+// target energy), once per upload: [targets] doubles, fixed-order tree.
+__global__ void __launch_bounds__(256) k_target_energy(const double* amp, const uint8_t* roi_rm, size_t npix,
+                                                      double* stt) {
+    const double* a = amp + npix * blockIdx.x;
+    double s = 0.0;
+    for (size_t i = threadIdx.x; i < npix; i += blockDim.x)
+        if (!roi_rm || roi_rm[i]) s += a[i] * a[i];
+    __shared__ double red[8];
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double x = threadIdx.x < 8 ? red[threadIdx.x] : 0.0;
+        x = warp_sum(x);
+        if (threadIdx.x == 0) stt[blockIdx.x] = x;
+    }
+}
+
 __global__ void k_validate(const double* amp, const double* phase, size_t n, int* flags) {
     int f = 0;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
@@ -869,7 +894,7 @@ struct hgc_ifta_plan {
     cudaEvent_t up_ev = nullptr;  // end of the last upload's stream work
     DBuf<int> vflags;             // deferred TargetSpec validation flags
     DBuf<float> target_f, weights, init_weights;
-    DBuf<double> amp_d, phase_d, partials, trace;
+    DBuf<double> amp_d, phase_d, partials, trace, stt, eff;  // stt: sum T^2 per target; eff: efficiency trace
     DBuf<uint8_t> roi, roi_rm, lv8, lv1;
     DBuf<uint16_t> lv16;
     DBuf<MtState> mt;
@@ -1116,7 +1141,7 @@ struct hgc_ifta_plan {
             }
         }
         k_finalize<<<batch, 32, 0, st>>>(partials.p, cfg.iterations, batch, tiles, (double)M, cfg.freedom_scale, 0,
-                                         trace.p);
+                                         trace.p, stt.p, eff.p);
         ++launches;
         CK(cudaGetLastError());
     }
@@ -1281,6 +1306,8 @@ int hgc_ifta_plan_create(hgc_ifta_plan** out, const hgc_ifta_cfg* cfg, const hgc
         else p->lv8.alloc(tot);
         p->partials.alloc((size_t)cfg->iterations * batch * p->tiles * 8);
         p->trace.alloc((size_t)cfg->iterations * batch);
+        p->eff.alloc(batch);
+        p->stt.alloc(batch);
         if (p->random_init()) p->chunking.plan(p->npix, batch);
         p->mt.alloc((size_t)batch * p->chunking.chunks);
         p->seeds.alloc(batch);
@@ -1314,6 +1341,12 @@ int hgc_ifta_plan_upload(hgc_ifta_plan* p, const hgc_ifta_io* io) {
         }
         p->M = roi_count(io->roi, npix);
         launch_validate(p->amp_d.p, io->phase ? p->phase_d.p : nullptr, tot, p->vflags.p, p->stream);
+        if (io->roi) {
+            p->roi_rm.ensure(npix);
+            CK(cudaMemcpyAsync(p->roi_rm.p, io->roi, npix, cudaMemcpyHostToDevice, p->stream));
+        }
+        k_target_energy<<<p->batch, 256, 0, p->stream>>>(p->amp_d.p, io->roi ? p->roi_rm.p : nullptr, npix, p->stt.p);
+        CK(cudaGetLastError());
         to_colpair<double, float>(p->amp_d.p, p->target_f.p, p->nx, p->ny, p->batch, p->stream);
         CK(cudaGetLastError());
         if (io->phase) {
@@ -1339,8 +1372,6 @@ int hgc_ifta_plan_upload(hgc_ifta_plan* p, const hgc_ifta_io* io) {
         p->bh = p->ny;
         if (io->roi) {  // column-pair major for the column pass
             p->roi.ensure(npix);
-            p->roi_rm.ensure(npix);
-            CK(cudaMemcpyAsync(p->roi_rm.p, io->roi, npix, cudaMemcpyHostToDevice, p->stream));
             k_to_colpair<uint8_t, uint8_t><<<ew_grid(npix), 256, 0, p->stream>>>(p->roi_rm.p, p->roi.p, p->nx, p->ny,
                                                                                npix);
             CK(cudaGetLastError());
@@ -1454,6 +1485,8 @@ int hgc_ifta_plan_download(hgc_ifta_plan* p, hgc_ifta_io* io) {
             if (io->final_error)
                 for (int b = 0; b < p->batch; ++b) io->final_error[b] = tr[(size_t)b * K + K - 1];
         }
+        if (io->efficiency)
+            CK(cudaMemcpy(io->efficiency, p->eff.p, sizeof(double) * p->batch, cudaMemcpyDeviceToHost));
         if (io->hologram_gray8) {  // runner.cpp:251-259 hologram.png pixels
             DBuf<uint8_t> g;
             g.alloc(tot);
@@ -1634,6 +1667,8 @@ struct hgc_ospr_plan {
     cudaEvent_t ev_fork = nullptr, ev_seed = nullptr, ev_pass[2] = {nullptr, nullptr};
     cudaEvent_t done = nullptr;  // recorded after each execute on the execute stream
     cudaEvent_t up_ev = nullptr;  // end of the last upload's stream work
+    bool fresnel = false;  // hgc_ospr_plan_set_fresnel
+    DBuf<float2> Q;
     // RunReport::profile (hgc_ospr_run with io->profile): external events
     // around each subframe's column-inverse, row and accumulating passes
     std::vector<cudaEvent_t> pev;
@@ -1769,6 +1804,7 @@ struct hgc_ospr_plan {
         ra.levels8 = wide_levels ? nullptr : lv8.p + (size_t)(n - 1) * npix;
         ra.levels16 = wide_levels ? lv16.p + (size_t)(n - 1) * npix : nullptr;
         ra.lv_bstride = (size_t)N * npix;
+        ra.fresnel_q = fresnel ? Q.p : nullptr;  // Fresnel OSPR (extension): f = IFFT(seed) conj(Q), R = FFT(f Q)
         return ra;
     }
     ColArgs col_acc_args(int n) const {
@@ -2162,11 +2198,41 @@ int hgc_ospr_plan_destroy(hgc_ospr_plan* p) {
     });
 }
 
+// Fresnel OSPR (extension): the reference rejects OSPR with a
+// Fresnel propagator (src/config.cpp:443-445) and run_ospr_impl takes a bare
+// FftBackend (ospr.hpp:68-69); this composes Propagator<float>::inverse /
+// forward (propagation.hpp:81-95) into the subframe loop: f = IFFT(seed)
+// conj(Q), quantise, R = FFT(f Q).  Before the plan's first execute.
+int hgc_ospr_plan_set_fresnel(hgc_ospr_plan* p, const hgc_fresnel* fresnel) {
+    return guarded([&] {
+        if (!p) invalid("hgc_ospr_plan_set_fresnel: null plan");
+        if (p->graph) invalid("hgc_ospr_plan_set_fresnel: call before the first execute");
+        CK(cudaSetDevice(p->device));
+        p->fresnel = fresnel != nullptr;
+        if (!fresnel) return;
+        validate_fresnel(fresnel);
+        p->Q.ensure(p->npix);
+        const double scale = 3.1415926535897932384626433832795 / (fresnel->wavelength * fresnel->distance);
+        k_fresnel_q<<<ew_grid(p->npix), 256, 0, p->stream>>>(p->nx, p->ny, scale, fresnel->pixel_pitch_x,
+                                                              fresnel->pixel_pitch_y, p->Q.p);
+        CK(cudaGetLastError());
+    });
+}
+
+int hgc_ospr_run_fresnel(const hgc_ospr_cfg* cfg, const hgc_slm* slm, const hgc_fresnel* fresnel, int nx, int ny,
+                         int jobs, hgc_ospr_io* io);
+
 int hgc_ospr_run(const hgc_ospr_cfg* cfg, const hgc_slm* slm, int nx, int ny, int jobs, hgc_ospr_io* io) {
+    return hgc_ospr_run_fresnel(cfg, slm, nullptr, nx, ny, jobs, io);
+}
+
+int hgc_ospr_run_fresnel(const hgc_ospr_cfg* cfg, const hgc_slm* slm, const hgc_fresnel* fresnel, int nx, int ny,
+                         int jobs, hgc_ospr_io* io) {
     auto t0 = std::chrono::steady_clock::now();
     hgc_ospr_plan* p = nullptr;
     int rc = guarded([] { route_device(); });
     if (rc == HGC_OK) rc = hgc_ospr_plan_create(&p, cfg, slm, nx, ny, jobs, io ? io->per_job_target : 0);
+    if (rc == HGC_OK && fresnel) rc = hgc_ospr_plan_set_fresnel(p, fresnel);
     if (rc == HGC_OK && io && io->profile) rc = guarded([&] { p->profile_on(); });
     if (rc == HGC_OK) rc = hgc_ospr_plan_upload(p, io);
     if (rc == HGC_OK) rc = guarded([&] { check_validation(p->vflags.p, p->stream); });  // eager in the one-shot run

@@ -359,6 +359,10 @@ __global__ void __launch_bounds__(1024, 1) k_row_persist(RowArgs a, int rowblock
 // COL_GS_FAST / COL_WGS_FAST: no ROI, no LT schedule, phase freedom (the
 // benchmark configurations); COL_GS_GENERIC: every TargetSpec / variant.
 enum ColMode { COL_PLAIN = 0, COL_GS_GENERIC = 1, COL_OSPR = 2, COL_GS_FAST = 3, COL_WGS_FAST = 4 };
+// The last iteration's GS column pass also reduces the diffraction-efficiency
+// sums (a separate instantiation, so the K-1 others carry no extra registers).
+constexpr int COL_EFF = 8;  // flag added to COL_GS_GENERIC / COL_GS_FAST / COL_WGS_FAST
+__host__ __device__ constexpr int col_base_mode(int m) { return m & 7; }
 
 struct ColArgs {
     const float2* tw;
@@ -464,7 +468,7 @@ constexpr int col_smem_bytes() {
 
 // Per-thread float partials -> warp sums in float (32 terms) -> per-warp
 // doubles -> fixed-order double block sum; thread 0 stores NV doubles.
-template <int NV>
+template <int NV, int DUP = -1>  // DUP >= 0: also store sum DUP into slot NV
 __device__ __forceinline__ void block_sum_float_store(float (&v)[NV], double* out) {
     __shared__ double red[32][NV];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
@@ -481,7 +485,10 @@ __device__ __forceinline__ void block_sum_float_store(float (&v)[NV], double* ou
         for (int i = 0; i < NV; ++i) {
             double x = lane < nw ? red[lane][i] : 0.0;
             x = warp_sum(x);
-            if (lane == 0) out[i] = x;
+            if (lane == 0) {
+                out[i] = x;
+                if (DUP == i) out[NV] = x;
+            }
         }
     }
 }
@@ -490,6 +497,8 @@ __device__ __forceinline__ void block_sum_float_store(float (&v)[NV], double* ou
 // gx column blocks per target (the partial-sum slot).
 template <int NY, int C, int MODE, int LAY>
 __device__ __forceinline__ void col_cta(const ColArgs& a, const int bx, const int by, const int gx) {
+    constexpr int M = col_base_mode(MODE);
+    constexpr bool kEff = (MODE & COL_EFF) != 0;
     constexpr int EM = ColCfg<NY, LAY>::EM;
     constexpr int E = LineCfg<NY, EM>::E, T = LineCfg<NY, EM>::T;
     extern __shared__ __align__(128) float2 smem[];
@@ -581,7 +590,7 @@ __device__ __forceinline__ void col_cta(const ColArgs& a, const int bx, const in
         }
     };
 
-    if constexpr (MODE == COL_PLAIN) {
+    if constexpr (M == COL_PLAIN) {
         if (a.sign < 0) fft_line<NY, -1, EM>(v, t, smem, idx, a.tw);
         else fft_line<NY, +1, EM>(v, t, smem, idx, a.tw);
         if (a.apply_norm)
@@ -602,15 +611,22 @@ __device__ __forceinline__ void col_cta(const ColArgs& a, const int bx, const in
             if constexpr (kTgt) return tsm[tso + e * ss];
             else return __ldg(&tg[e * ss]);
         };
-        constexpr int NV = MODE == COL_OSPR ? 7 : 4;
+        // partial sums per CTA.  GS modes: [0..2] the MSE sums (metrics.hpp:70-97:
+        // (T-|R|)^2, T|R|, |R|^2 over the mask; sum T^2 is the same every
+        // iteration and comes from the plan, hgc_ifta_plan::stt); the last
+        // iteration (kEff) also [3] the replay power on the target's support
+        // (T > 0, in the mask) and [4] the total replay power (fast modes: stored
+        // as a copy of [2], no mask): the diffraction efficiency (k_finalize;
+        // DESIGN.md §3, an extension).
+        constexpr int NV = M == COL_OSPR ? 7 : (kEff ? (M == COL_GS_GENERIC ? 5 : 4) : 3);
         float acc[NV];
 #pragma unroll
         for (int i = 0; i < NV; ++i) acc[i] = 0.f;
-        if constexpr (MODE == COL_GS_FAST || MODE == COL_WGS_FAST) {
+        if constexpr (M == COL_GS_FAST || M == COL_WGS_FAST) {
             // GS/WGS, no ROI, phase freedom: mse partials (metrics.hpp:70-97) and
             // R <- amp * R/|R| (ifta.hpp:198-214), branch-free
             const bool last = a.last && !a.ckpt;  // skip the constraint
-            float* w = MODE == COL_WGS_FAST ? a.weights + a.t_bstride * b + sb : nullptr;
+            float* w = M == COL_WGS_FAST ? a.weights + a.t_bstride * b + sb : nullptr;
             const float lo = a.clamp_lo, hi = a.clamp_hi;
 #pragma unroll
             for (int e = 0; e < E; ++e) {
@@ -623,9 +639,9 @@ __device__ __forceinline__ void col_cta(const ColArgs& a, const int bx, const in
                 acc[0] = fmaf(d, d, acc[0]);
                 acc[1] = fmaf(amp0, r, acc[1]);
                 acc[2] += r2;
-                acc[3] = fmaf(amp0, amp0, acc[3]);
+                if constexpr (kEff) acc[3] += amp0 > 0.f ? r2 : 0.f;
                 float amp = amp0;
-                if constexpr (MODE == COL_WGS_FAST) {
+                if constexpr (M == COL_WGS_FAST) {
                     if (!last && amp0 > 0.f) {  // ifta.hpp:198-204
                         const float cand = w[e * ss] * amp0 * (r > 1e-12f ? ri : 1e12f);
                         const float wn = fminf(fmaxf(cand, lo), hi);
@@ -637,7 +653,7 @@ __device__ __forceinline__ void col_cta(const ColArgs& a, const int bx, const in
                 v[e] = r2 > 0.f ? make_float2(R.x * sc, R.y * sc) : make_float2(amp, 0.f);
                 if (last) v[e] = R;
             }
-        } else if constexpr (MODE == COL_GS_GENERIC) {
+        } else if constexpr (M == COL_GS_GENERIC) {
             float* w = a.weights ? a.weights + a.t_bstride * b + sb : nullptr;
             const float2* tcs = a.tphase_cs ? a.tphase_cs + a.t_bstride * b + sb : nullptr;
             const uint8_t* roi = a.roi ? a.roi + sb : nullptr;
@@ -654,8 +670,10 @@ __device__ __forceinline__ void col_cta(const ColArgs& a, const int bx, const in
                     acc[0] += d * d;
                     acc[1] += amp * r;
                     acc[2] += r * r;
-                    acc[3] += amp * amp;
+                    if constexpr (kEff)
+                        if (amp > 0.f) acc[3] += r * r;
                 }
+                if constexpr (kEff) acc[4] += r * r;
                 if (!a.last || a.ckpt) {  // replay-plane constraint, ifta.hpp:190-223
                     if (in_roi) {
                         const bool active = !a.lt || (x >= a.lt_x0 && x < a.lt_x1 && y >= a.lt_y0 && y < a.lt_y1);
@@ -710,7 +728,7 @@ __device__ __forceinline__ void col_cta(const ColArgs& a, const int bx, const in
                 acc[6] = fmaf(rc, rc, acc[6]);
             }
         }
-        if constexpr (MODE != COL_OSPR) {
+        if constexpr (M != COL_OSPR) {
             if (a.last) {
                 store_col(a.replay_out + a.bstride * b);
             } else {
@@ -731,7 +749,8 @@ __device__ __forceinline__ void col_cta(const ColArgs& a, const int bx, const in
                 bulk_wait_read0();
             }
         }
-        block_sum_float_store<NV>(acc, a.partials + blk * 8);
+        block_sum_float_store<NV, (kEff && (M == COL_GS_FAST || M == COL_WGS_FAST)) ? 2 : -1>(acc,
+                                                                                              a.partials + blk * 8);
     }
 }
 

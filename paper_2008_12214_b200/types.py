@@ -305,6 +305,7 @@ class RunReport:  # report.hpp:48-65 (+ levels: the hologram's level indices)
     decisions: list = field(default_factory=list)
     levels: np.ndarray | None = None
     weights: np.ndarray | None = None  # WGS weights of a checkpointed run (run_ifta(..., checkpoint=True))
+    efficiency: float | None = None  # extension: diffraction efficiency of the final replay (hgc_ifta_io::efficiency)
 
 
 @dataclass

@@ -390,3 +390,25 @@ def test_plan_kernel_timing_inside_graph():
                 p.kernel_times()
         p.close()
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("roi", [False, True])
+def test_efficiency_of_final_replay(roi):
+    # extension (no reference counterpart): sum_{T>0, roi} |R|^2 / sum |R|^2 of the
+    # final (unconstrained) replay, reduced in the last column pass; checked
+    # against the returned replay in double
+    amp = np.zeros((128, 128))
+    amp[32:96, 32:96] = hg.patterns.smooth_blobs(64, 64)
+    amp = hg.normalize_image(amp, hg.Normalization.UnitEnergy)
+    c = cfg_for(amp, hg.SlmSpec.full_circle_phase(16), 8, seed=3)
+    if roi:
+        m = np.zeros((128, 128), np.uint8)
+        m[24:104, 24:104] = 1
+        c.target.roi = m
+    rep = hg.run_gs(c)
+    p = np.abs(rep.replay.astype(np.complex128)) ** 2
+    sup = amp > 0
+    if roi:
+        sup &= m.astype(bool)
+    want = p[sup].sum() / p.sum()
+    assert 0 < rep.efficiency < 1 and abs(rep.efficiency - want) < 1e-5, (rep.efficiency, want)

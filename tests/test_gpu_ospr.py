@@ -186,3 +186,39 @@ def test_ospr_roi_with_tma_tiles_matches_oracle(oracle):
     assert level_mismatches(run.set.levels, ref.levels).sum() <= 8
     assert np.max(np.abs(run.report.trace.values() - ref.cumulative_mse) / ref.cumulative_mse) < 1e-4
     assert np.max(np.abs(np.array(run.set.per_frame_mse) - ref.frame_mse) / ref.frame_mse) < 1e-4
+
+
+def test_fresnel_ospr_matches_composed_oracle(oracle):
+    # extension: OSPR with the Fresnel propagator.  The reference
+    # rejects it (src/config.cpp:443-445), so the oracle is composed from its
+    # pinned parts: seed_random_phase (rng.hpp:54-67), Propagator::inverse /
+    # forward (propagation.hpp:81-95), the quantiser and the OSPR accumulation
+    # (ospr.hpp:118-146), in double.  Parity-unpinned by construction.
+    n, N, seed = 256, 6, 11
+    amp = hg.patterns.bench_target(n)
+    fr = (532e-9, 0.1, 8e-6, 8e-6)
+    prop = hg.Propagator.fresnel(n, n, hg.FresnelParams(*fr))
+    slm = hg.SlmSpec.binary_phase()
+    run = hg.run_ospr(ocfg(amp, N, seed), prop=prop)
+    q = oracle.fresnel_q(n, n, *fr).astype(np.complex128)
+    states = np.array([1.0 + 0j, -1.0 + 0j])
+    S = np.zeros((n, n))
+    tot = {}
+    for k in range(N):
+        pre = oracle.fft2(oracle.seed_random_phase(amp, seed, k * amp.size).astype(np.complex128), +1) * np.conj(q)
+        cls = mismatch_classes(level_mismatches(run.set.levels[k], _binary_levels(pre)), pre, slm)
+        for key, v in cls.items():
+            tot[key] = tot.get(key, 0) + v
+        R = oracle.fft2(states[run.set.levels[k].astype(np.int64)] * q, -1)  # the GPU's own frame, forward-propagated
+        I = np.abs(R) ** 2
+        S += I
+        assert rel(run.set.per_frame_mse[k], float(np.mean((amp - np.sqrt(I)) ** 2))) < 1e-4
+        assert rel(run.report.trace.values()[k], float(np.mean((amp - np.sqrt(S / (k + 1))) ** 2))) < 1e-4
+    record("fresnel_ospr_256_binary_6", tot)
+    assert tot["bad"] == 0, tot
+    assert np.allclose(run.set.mean_intensity, S / N, rtol=1e-4, atol=1e-9)
+
+
+def _binary_levels(f):
+    # binary_phase decision: level 1 iff Re(f) < 0 (quantise.hpp:175-198)
+    return (f.real < 0).astype(np.int64)

@@ -57,7 +57,7 @@ __device__ __forceinline__ int decide64(const Q64& q, size_t i, double2 v) {
 }
 
 // Quantiser::apply (quantise.hpp:208-216) + level indices
-__global__ void k_quant64(double2* f, int32_t* levels, size_t n, Q64 q) {
+static __global__ void k_quant64(double2* f, int32_t* levels, size_t n, Q64 q) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
         const int k = decide64(q, i, f[i]);
         double2 s = q.states[k];
@@ -69,7 +69,7 @@ __global__ void k_quant64(double2* f, int32_t* levels, size_t n, Q64 q) {
 }
 
 // Propagator<double>: forward input f*Q (propagation.hpp:85), inverse output *conj(Q) (:93)
-__global__ void k_mulq64(double2* f, const double2* Q, size_t n, int conj_q) {
+static __global__ void k_mulq64(double2* f, const double2* Q, size_t n, int conj_q) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
         f[i] = conj_q ? cmul_conj_rn64(f[i], Q[i]) : cmul_rn64(f[i], Q[i]);
 }
@@ -97,7 +97,7 @@ struct Mag64 {
         return R ? abs_rn64(R[i]) : __dsqrt_rn(__ddiv_rn(S[i], n));
     }
 };
-__global__ void k_mse64_gain(const double* T, Mag64 mag, const uint8_t* mask, size_t n, double* part) {
+static __global__ void k_mse64_gain(const double* T, Mag64 mag, const uint8_t* mask, size_t n, double* part) {
     __shared__ double red[32];
     double s_tr = 0.0, s_rr = 0.0;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
@@ -113,7 +113,7 @@ __global__ void k_mse64_gain(const double* T, Mag64 mag, const uint8_t* mask, si
         part[2 * blockIdx.x + 1] = s_rr;
     }
 }
-__global__ void k_mse64_g(const double* part, int nblk, int scale_free, double* g) {
+static __global__ void k_mse64_g(const double* part, int nblk, int scale_free, double* g) {
     if (threadIdx.x != 0) return;
     double s_tr = 0.0, s_rr = 0.0;
     for (int b = 0; b < nblk; ++b) {
@@ -127,7 +127,7 @@ __global__ void k_mse64_g(const double* part, int nblk, int scale_free, double* 
     }
     *g = v;
 }
-__global__ void k_mse64_sum(const double* T, Mag64 mag, const uint8_t* mask, size_t n, const double* g, double* part) {
+static __global__ void k_mse64_sum(const double* T, Mag64 mag, const uint8_t* mask, size_t n, const double* g, double* part) {
     __shared__ double red[32];
     const double gg = *g;
     double acc = 0.0;
@@ -139,7 +139,7 @@ __global__ void k_mse64_sum(const double* T, Mag64 mag, const uint8_t* mask, siz
     acc = block_sum64(acc, red);
     if (threadIdx.x == 0) part[blockIdx.x] = acc;
 }
-__global__ void k_mse64_final(const double* part, int nblk, double M, double* out) {
+static __global__ void k_mse64_final(const double* part, int nblk, double M, double* out) {
     if (threadIdx.x != 0) return;
     double acc = 0.0;
     for (int b = 0; b < nblk; ++b) acc += part[b];
@@ -157,7 +157,7 @@ struct Con64 {
     int lt, x0, x1, y0, y1;
     int nx;
 };
-__global__ void k_constrain64(double2* R, size_t n, Con64 c) {
+static __global__ void k_constrain64(double2* R, size_t n, Con64 c) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
         if (!c.roi || c.roi[i]) {
             const int x = (int)(i % c.nx), y = (int)(i / c.nx);
@@ -191,7 +191,7 @@ __global__ void k_constrain64(double2* R, size_t n, Con64 c) {
 
 // OSPR (ospr.hpp:105-116, :134-137): frame amplitude (adaptive budget) and
 // the running intensity sum.
-__global__ void k_ospr_amp64(const double* T, const double* S, size_t n, int frame, double g, double* amp) {
+static __global__ void k_ospr_amp64(const double* T, const double* S, size_t n, int frame, double g, double* amp) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
         const double t = T[i], t2 = __dmul_rn(t, t), nn = frame;
         const double budget = __dsub_rn(__dmul_rn(nn, t2), __dmul_rn(nn - 1.0, __ddiv_rn(S[i], nn - 1.0)));
@@ -199,13 +199,13 @@ __global__ void k_ospr_amp64(const double* T, const double* S, size_t n, int fra
         amp[i] = __dadd_rn(__dmul_rn(1.0 - g, t), __dmul_rn(g, tn));
     }
 }
-__global__ void k_ospr_acc64(const double2* R, size_t n, double* S) {
+static __global__ void k_ospr_acc64(const double2* R, size_t n, double* S) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
         const double2 z = R[i];
         S[i] = __dadd_rn(S[i], __dadd_rn(__dmul_rn(z.x, z.x), __dmul_rn(z.y, z.y)));
     }
 }
-__global__ void k_ospr_out64(const double* S, size_t n, int N, double* mean, double2* replay) {
+static __global__ void k_ospr_out64(const double* S, size_t n, int N, double* mean, double2* replay) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
         const double m = __ddiv_rn(S[i], (double)N);
         if (mean) mean[i] = m;

@@ -203,7 +203,7 @@ struct JumpArgs {
     int chunks, c_lo, poly_base;
 };
 
-__global__ void __launch_bounds__(kJumpThreads) k_mt_jump(JumpArgs a) {
+static __global__ void __launch_bounds__(kJumpThreads) k_mt_jump(JumpArgs a) {
     __shared__ uint64_t ring[6 * kMtN];
     __shared__ uint64_t red[kMtN];
     const int per = a.chunks - a.c_lo;

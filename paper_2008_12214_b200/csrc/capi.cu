@@ -12,12 +12,17 @@ thread_local std::string g_err;
 // ------------------------------------------------------- twiddle tables
 static __global__ void k_init_twiddles(float2* tw) {
     int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx < 1 || idx >= 2 * kMaxLine) return;
-    int N = 1;
-    while (N * 2 <= idx) N *= 2;
-    int m = idx - N;
+    if (idx < 1 || idx >= kTwEntries) return;
     double s, c;
-    sincospi(-2.0 * (double)m / (double)N, &s, &c);
+    if (idx >= 2 * kMaxLine) {  // the radix-16 span-256 pass: W_256^(r k), r, k < 16 (fft.cuh kTw256)
+        const int rk = idx - 2 * kMaxLine, r = rk >> 4, k = rk & 15;
+        sincospi(-2.0 * (double)(r * k) / 256.0, &s, &c);
+    } else {
+        int N = 1;
+        while (N * 2 <= idx) N *= 2;
+        int m = idx - N;
+        sincospi(-2.0 * (double)m / (double)N, &s, &c);
+    }
     tw[idx] = make_float2((float)c, (float)s);
 }
 
@@ -32,8 +37,8 @@ const float2* device_twiddles() {
     auto it = g_tw_tables.find(dev);
     if (it != g_tw_tables.end()) return it->second;
     float2* tw = nullptr;
-    CK(cudaMalloc(&tw, sizeof(float2) * 2 * kMaxLine));
-    k_init_twiddles<<<(2 * kMaxLine + 255) / 256, 256>>>(tw);
+    CK(cudaMalloc(&tw, sizeof(float2) * kTwEntries));
+    k_init_twiddles<<<(kTwEntries + 255) / 256, 256>>>(tw);
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
     g_tw_tables[dev] = tw;

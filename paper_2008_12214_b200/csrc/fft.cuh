@@ -25,6 +25,11 @@
 namespace hg {
 
 constexpr int kMaxLine = 4096;
+// Twiddle table layout: tw[N + m] = exp(-2 pi i m / N) for N = 1..4096, then
+// at kTw256 the 16 x 16 table W_256^(r k) (r, k < 16) read directly by the
+// radix-16 pass of span 256 (fft.cuh apply_twiddles).
+constexpr int kTw256 = 2 * kMaxLine;
+constexpr int kTwEntries = kTw256 + 256;
 
 // Complex element type of a transform: float2 (the hot path) or double2 (the
 // f64 FftBackend, k_fft64.cu).
@@ -241,6 +246,9 @@ __device__ __forceinline__ void apply_twiddles(C2* x, const TW* __restrict__ tw,
     }
 }
 
+#ifndef HG_TW256
+#define HG_TW256 0  // measured: 11.16-11.20 vs 11.09-11.14 ms per iteration (loads cost more than the products they save)
+#endif
 // float2 lines: twiddles as (w, i*w) pairs in the forward direction; the
 // inverse applies conj(w) through lane swaps: a * conj(w) = (a.x, a.x) * swap(i*w)
 // + (a.y, a.y) * swap(w).
@@ -270,7 +278,13 @@ __device__ __forceinline__ float2 tw_apply(float2 a, Tw2 w) {
 }
 template <int S, int SIGN, int R>
 __device__ __forceinline__ void apply_twiddles(float2* x, const float2* __restrict__ tw, int k) {
-    if constexpr (R == 16) {
+    if constexpr (R == 16 && S == 256 && HG_TW256) {
+        // span 256 (k < 16): all 15 powers from the 16 x 16 table, one 128-B line
+        // per warp load, instead of 3 loads + 12 products (fewer FP32 ops, and
+        // each twiddle is the rounded exact value instead of a product of them)
+#pragma unroll
+        for (int r = 1; r < 16; ++r) x[r] = tw_apply<SIGN>(x[r], tw_load<kTw256>(tw, r * 16 + k));
+    } else if constexpr (R == 16) {
         const Tw2 w1 = tw_load<S>(tw, k), w4 = tw_load<S / 4>(tw, k), w8 = tw_load<S / 8>(tw, k);
         const Tw2 w2 = tw_mul(w1, w1), w3 = tw_mul(w2, w1), w12 = tw_mul(w8, w4);
         x[1] = tw_apply<SIGN>(x[1], w1);

@@ -144,7 +144,7 @@ struct DevTensorMap {
 // polynomials of mtjump.cpp (computed once per process per shape).  Enough
 // chunks that streams*chunks fills the GPU twice, none shorter than
 // kMinChunkDraws (the jump costs about as much as ~30k draws).
-constexpr size_t kMinChunkDraws = 32768;
+constexpr size_t kMinChunkDraws = 4096;
 constexpr int kMaxChunks = 512;
 // The seed kernel instantiation for a launch: the fast consumer loop when the
 // output is the plans' float quad layout with a plain amplitude.
@@ -183,13 +183,29 @@ struct SeedChunks {
         // enough chunks to fill every slot; among up to 4x that, the count
         // whose last wave is fullest (ties: fewer chunks, fewer jumps)
         const long long slots = (long long)ctas_per_sm * sms, S = std::max(1, streams);
-        const long long cmax = std::max<long long>(1, (long long)(npix / kMinChunkDraws));
-        long long c = std::min((slots + S - 1) / S, cmax);
-        double best = 0.0;
-        for (long long k = c, hi = std::min(4 * c, cmax); k <= hi; ++k) {
-            const long long ctas = S * k, waves = (ctas + slots - 1) / slots;
-            const double eff = (double)ctas / (double)(waves * slots);
-            if (eff > best + 0.02) best = eff, c = k;
+        // Chunk count from a cost model measured on B200: a chunk's draws cost
+        // ~1.2 ns each on its CTA; a jump ~240 us on one CTA (64 sequential
+        // 312-word XOR blocks), split over up to 16 CTAs when the jumps do not
+        // fill the GPU (launch()), plus ~15 us of block prefix per split.
+        const long long cmax = std::max<long long>(1, std::min<long long>(kMaxChunks, (long long)(npix / kMinChunkDraws)));
+        auto cost = [&](long long k) {
+            const double draws = (double)((npix + k - 1) / k);
+            const long long seed_waves = (S * k + slots - 1) / slots;
+            double t = (double)seed_waves * draws * 1.2e-3;  // us
+            if (k > 1 || offset > 0) {
+                const long long nj = S * (offset > 0 ? k : k - 1);
+                const long long jslots = 2LL * sms;
+                const long long sp = std::max<long long>(1, std::min<long long>(16, jslots / std::max<long long>(1, nj)));
+                const long long jwaves = (nj * sp + jslots - 1) / jslots;
+                t += (double)jwaves * (15.0 + 240.0 / (double)sp);
+            }
+            return t;
+        };
+        long long c = 1;
+        double best = cost(1);
+        for (long long k = 2; k <= cmax; ++k) {
+            const double t = cost(k);
+            if (t < best * 0.98) best = t, c = k;
         }
         if (const char* ev = getenv("HG_SEED_CHUNKS")) c = std::max(1, atoi(ev));  // tuning / tests
         c = std::min<long long>(c, (long long)std::max<size_t>(1, npix));
@@ -213,8 +229,18 @@ struct SeedChunks {
     int launch(SeedArgs sa, const uint64_t* seeds, MtState* states, int streams, cudaStream_t st) const {
         int n = 0;
         if (jumps()) {
-            JumpArgs ja{seeds, nullptr, starts.p, pool.p, 1, states, chunks, c_first(), c_first()};
-            k_mt_jump<<<streams * (chunks - c_first()), kJumpThreads, 0, st>>>(ja);
+            // a jump costs ~240 us on one CTA (64 blocks of 312-word XOR windows,
+            // shared-memory bound): when there are fewer jumps than SM slots, each
+            // is split over several CTAs (their partial XORs combined atomically)
+            const int nj = streams * (chunks - c_first());
+            int sms = 148, dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            int splits = std::max(1, std::min(16, 2 * sms / std::max(1, nj)));
+            if (const char* ev = getenv("HG_JUMP_SPLITS")) splits = std::max(1, atoi(ev));  // tuning
+            if (splits > 1) CK(cudaMemsetAsync(states, 0, sizeof(MtState) * (size_t)streams * chunks, st));
+            JumpArgs ja{seeds, nullptr, starts.p, pool.p, 1, states, chunks, c_first(), c_first(), splits};
+            k_mt_jump<<<nj * splits, kJumpThreads, 0, st>>>(ja);
             ++n;
         }
         sa.states = states;
@@ -247,7 +273,7 @@ struct SeedChunks {
         if (chunks == 1) {
             int n = 0;
             if (first && offset0 > 0) {  // stream starts offset0 draws in (subframe block)
-                JumpArgs ja{seeds, nullptr, starts.p, pool.p, 1, states, 1, 0, 0};
+                JumpArgs ja{seeds, nullptr, starts.p, pool.p, 1, states, 1, 0, 0, 1};
                 k_mt_jump<<<streams, kJumpThreads, 0, st>>>(ja);
                 ++n;
             }
@@ -255,8 +281,8 @@ struct SeedChunks {
             seed_launch(streams, sa, st);
             return n + 1;
         }
-        JumpArgs ja = first ? JumpArgs{seeds, nullptr, starts.p, pool.p, 1, states, chunks, 0, c_first()}
-                            : JumpArgs{nullptr, states, step_starts.p, step_pool.p, 0, states, chunks, 0, 0};
+        JumpArgs ja = first ? JumpArgs{seeds, nullptr, starts.p, pool.p, 1, states, chunks, 0, c_first(), 1}
+                            : JumpArgs{nullptr, states, step_starts.p, step_pool.p, 0, states, chunks, 0, 0, 1};
         k_mt_jump<<<streams * chunks, kJumpThreads, 0, st>>>(ja);
         sa.seeds = nullptr;
         sa.chunks = chunks;

@@ -201,13 +201,17 @@ struct JumpArgs {
     int poly_step;          // 1: one polynomial per chunk; 0: one for all
     MtState* states;        // [streams * chunks]
     int chunks, c_lo, poly_base;
+    int splits;             // > 1: each jump's 64 blocks split over `splits` CTAs, combined by
+                            // atomicXor into zeroed states (from must be null); <= 1: one CTA
 };
 
 static __global__ void __launch_bounds__(kJumpThreads) k_mt_jump(JumpArgs a) {
     __shared__ uint64_t ring[6 * kMtN];
     __shared__ uint64_t red[kMtN];
+    const int splits = a.splits > 1 ? a.splits : 1;
     const int per = a.chunks - a.c_lo;
-    const int s = blockIdx.x / per, c = a.c_lo + blockIdx.x % per;
+    const int jb = blockIdx.x / splits, part = blockIdx.x % splits;
+    const int s = jb / per, c = a.c_lo + jb % per;
     const size_t b = (size_t)s * a.chunks + c;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (a.from) {
@@ -222,20 +226,29 @@ static __global__ void __launch_bounds__(kJumpThreads) k_mt_jump(JumpArgs a) {
     }
     __syncthreads();
     if (c < a.poly_base) {  // offset 0: the seed block itself
-        for (int i = tid; i < kMtN; i += blockDim.x) a.states[b].w[i] = ring[i];
-        if (tid == 0) a.states[b].pos = kMtN;
+        if (part == 0) {
+            for (int i = tid; i < kMtN; i += blockDim.x) a.states[b].w[i] = ring[i];
+            if (tid == 0) a.states[b].pos = kMtN;
+        }
         return;
     }
+    // this CTA's share of the blocks: q in [q0, q1); raw blocks 1 .. q0+1 first
+    // (block i lives in ring slot i % 3, mirrored at +3)
+    const int q0 = part * kJumpBlocks / splits, q1 = (part + 1) * kJumpBlocks / splits;
     const int* st = a.starts + (size_t)(c - a.poly_base) * a.poly_step * (kJumpBlocks + 1);
-    if (warp == 0) {  // block 1
-        mt_twist_warp(ring, ring + kMtN, lane);
-        for (int i = lane; i < kMtN; i += 32) ring[4 * kMtN + i] = ring[kMtN + i];
+    if (warp == 0) {
+        for (int i = 1; i <= q0 + 1; ++i) {
+            const int so = (i - 1) % 3, sn = i % 3;
+            mt_twist_warp(ring + so * kMtN, ring + sn * kMtN, lane);
+            for (int w = lane; w < kMtN; w += 32) ring[(sn + 3) * kMtN + w] = ring[sn * kMtN + w];
+            __syncwarp();
+        }
     }
     __syncthreads();
     const int grp = tid / kJumpGroupThreads, j = tid % kJumpGroupThreads;
     uint64_t acc = 0;
-    for (int q = 0; q < kJumpBlocks; ++q) {
-        if (warp == 0) {  // block q+2 from block q+1
+    for (int q = q0; q < q1; ++q) {
+        if (warp == 0 && q + 1 < q1) {  // block q+2 from block q+1 (needed by block q+1's offsets)
             const int so = (q + 1) % 3, sn = (q + 2) % 3;
             mt_twist_warp(ring + so * kMtN, ring + sn * kMtN, lane);
             for (int i = lane; i < kMtN; i += 32) ring[(sn + 3) * kMtN + i] = ring[sn * kMtN + i];
@@ -258,8 +271,11 @@ static __global__ void __launch_bounds__(kJumpThreads) k_mt_jump(JumpArgs a) {
     }
     if (grp == 1 && j < kMtN) red[j] = acc;
     __syncthreads();
-    if (grp == 0 && j < kMtN) a.states[b].w[j] = acc ^ red[j];
-    if (tid == 0) a.states[b].pos = kMtN;
+    if (grp == 0 && j < kMtN) {
+        if (splits > 1) atomicXor(reinterpret_cast<unsigned long long*>(&a.states[b].w[j]), acc ^ red[j]);
+        else a.states[b].w[j] = acc ^ red[j];
+    }
+    if (tid == 0 && part == 0) a.states[b].pos = kMtN;
 }
 
 // One CTA per stream.  Warp 0 produces twists; warps 1.. consume.

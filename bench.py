@@ -222,7 +222,7 @@ def gs_ours(args, d: Dist):
                  "traces_finite_and_decreasing": bool(torch.isfinite(gtr).all().item()
                                                       and (gtr[:, -1] < gtr[:, 0]).all().item()),
                  "final_mse_mean": float(gtr[:, -1].mean().item()),
-                 "levels_checksum": int(glv.to(torch.int64).sum().item())}
+                 "levels_checksum": int(glv.sum(dtype=torch.int64).item())}
     kt = plan.kernel_times()  # the last timed step's passes, measured inside its graph
     prof = plan.profile(reps=5)
     prof["graph_row"], prof["graph_col"] = kt["row"], kt["col"]

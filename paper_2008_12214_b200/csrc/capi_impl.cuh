@@ -626,12 +626,14 @@ static __global__ void k_amp_gray8(AmpSrc src, size_t npix, const double* peak, 
 // TargetSpec::validate on the device (target.hpp:52-73): bit 0 = non-finite
 // amplitude, bit 1 = negative amplitude, bit 2 = non-finite phase.
 // sum T^2 over the mask per target (metrics.hpp:91-97, the scale-free MSE's
-// target energy), once per upload: [targets] doubles, fixed-order tree.
-static __global__ void __launch_bounds__(256) k_target_energy(const double* amp, const uint8_t* roi_rm, size_t npix,
-                                                      double* stt) {
-    const double* a = amp + npix * blockIdx.x;
+// target energy), once per upload of a scale-free plan: kTeBlocks partial
+// sums per target (grid-strided), then a fixed-order sum per target.
+constexpr int kTeBlocks = 128;
+static __global__ void __launch_bounds__(256) k_target_energy_part(const double* amp, const uint8_t* roi_rm,
+                                                                   size_t npix, double* part) {
+    const double* a = amp + npix * blockIdx.y;
     double s = 0.0;
-    for (size_t i = threadIdx.x; i < npix; i += blockDim.x)
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < npix; i += (size_t)gridDim.x * blockDim.x)
         if (!roi_rm || roi_rm[i]) s += a[i] * a[i];
     __shared__ double red[8];
     s = warp_sum(s);
@@ -640,8 +642,14 @@ static __global__ void __launch_bounds__(256) k_target_energy(const double* amp,
     if (threadIdx.x < 32) {
         double x = threadIdx.x < 8 ? red[threadIdx.x] : 0.0;
         x = warp_sum(x);
-        if (threadIdx.x == 0) stt[blockIdx.x] = x;
+        if (threadIdx.x == 0) part[(size_t)blockIdx.y * gridDim.x + blockIdx.x] = x;
     }
+}
+static __global__ void k_target_energy_fin(const double* part, int nb, double* stt) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < nb; i += 32) s += part[(size_t)blockIdx.x * nb + i];
+    s = warp_sum(s);
+    if (threadIdx.x == 0) stt[blockIdx.x] = s;
 }
 
 static __global__ void k_validate(const double* amp, const double* phase, size_t n, int* flags) {

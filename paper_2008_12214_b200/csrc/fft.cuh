@@ -100,6 +100,29 @@ __device__ __forceinline__ C2 tw16(C2 a) {
     }
 }
 
+#ifndef HG_TW16_PACKED  // W16^2 / W16^6 = h(+-1 + SIGN i): one packed add + one packed scale
+#define HG_TW16_PACKED 1
+#endif
+#if HG_TW16_PACKED
+// float2 specialisation of tw16 for the (1 +- i)/sqrt(2) factors: a W16^2 =
+// h (a + SIGN i a), a W16^6 = h (-a + SIGN i a): FADD2 / FFMA2 with operand
+// modifiers + FMUL2 (2 instructions instead of the 4 of a general product).
+template <int SIGN, int M>
+__device__ __forceinline__ float2 tw16(float2 a) {
+    constexpr int m = M & 15;
+    constexpr float h = 0.707106781186547524400844362104849039f;
+    if constexpr (m == 2 || m == 10) {
+        const float2 t = add_si<SIGN>(a, a);
+        return __fmul2_rn(t, make_float2(m == 2 ? h : -h, m == 2 ? h : -h));
+    } else if constexpr (m == 6 || m == 14) {
+        const float2 t = add_si<SIGN>(make_float2(-a.x, -a.y), a);
+        return __fmul2_rn(t, make_float2(m == 6 ? h : -h, m == 6 ? h : -h));
+    } else {
+        return tw16<SIGN, M, float2>(a);
+    }
+}
+#endif
+
 template <int SIGN, class C2>
 __device__ __forceinline__ void dft2(C2& a, C2& b) {
     C2 t = a;

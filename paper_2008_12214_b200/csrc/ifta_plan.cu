@@ -25,7 +25,8 @@ struct hgc_ifta_plan {
     cudaEvent_t up_ev = nullptr;  // end of the last upload's stream work
     DBuf<int> vflags;             // deferred TargetSpec validation flags
     DBuf<float> target_f, weights, init_weights;
-    DBuf<double> amp_d, phase_d, partials, trace, stt, eff;  // stt: sum T^2 per target; eff: efficiency trace
+    DBuf<double> amp_d, phase_d, partials, trace, stt, eff;  // stt: sum T^2 per target; eff: efficiency
+    DBuf<double> scratch_d;
     DBuf<uint8_t> roi, roi_rm, lv8, lv1;
     DBuf<uint16_t> lv16;
     DBuf<MtState> mt;
@@ -360,8 +361,13 @@ int hgc_ifta_plan_upload(hgc_ifta_plan* p, const hgc_ifta_io* io) {
             p->roi_rm.ensure(npix);
             CK(cudaMemcpyAsync(p->roi_rm.p, io->roi, npix, cudaMemcpyHostToDevice, p->stream));
         }
-        k_target_energy<<<p->batch, 256, 0, p->stream>>>(p->amp_d.p, io->roi ? p->roi_rm.p : nullptr, npix, p->stt.p);
-        CK(cudaGetLastError());
+        if (p->cfg.freedom_scale) {  // only the scale-free MSE uses it
+            p->scratch_d.ensure((size_t)kTeBlocks * p->batch);
+            k_target_energy_part<<<dim3(kTeBlocks, p->batch), 256, 0, p->stream>>>(
+                p->amp_d.p, io->roi ? p->roi_rm.p : nullptr, npix, p->scratch_d.p);
+            k_target_energy_fin<<<p->batch, 32, 0, p->stream>>>(p->scratch_d.p, kTeBlocks, p->stt.p);
+            CK(cudaGetLastError());
+        }
         to_colpair<double, float>(p->amp_d.p, p->target_f.p, p->nx, p->ny, p->batch, p->stream);
         CK(cudaGetLastError());
         if (io->phase) {

@@ -17,7 +17,8 @@ int col_tiles(int nx, int ny, int layout) {
 }
 int col_width_rt(int nx, int ny, int batch) {
     int cw = nx / col_tiles(nx, ny, LAY_QUAD);
-    const int T = ny / (ny < 16 ? ny : 16);  // threads per column (LineCfg<ny>::T)
+    const int em = ny <= HG_SMALL_NMAX ? HG_SMALL_EM : 16;
+    const int T = ny / (ny < em ? ny : em);  // threads per column (LineCfg<ny, ColCfg::EM>::T)
     while (cw > 2 && (long long)(nx / cw) * batch < sm_count() && T * (cw / 2) >= 64) cw /= 2;
     return cw;
 }

@@ -20,7 +20,8 @@ inline int sm_count() {
 
 template <class K>
 inline void set_smem(K kernel, int bytes) {
-    if (bytes > 48 * 1024) CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    // (static shared memory counts against the 48 KB default too: opt in for any dynamic size)
+    if (bytes > 0) CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
 }
 
 // ------------------------------------------------------------------- rows

@@ -88,9 +88,28 @@ struct RowStride {  // padded smem row; == 8 (mod 16) so a row pair sits 16 bank
     static constexpr int value = p + ((8 - p % 16) + 16) % 16;
 };
 
+// Elements per thread of the quad-layout passes for lines of at most
+// HG_SMALL_NMAX points: 8 (radix-8 passes), twice the threads of the
+// 16-element form.  A single small field leaves most SMs with 2-4 warps, so
+// its passes are latency chains, not throughput (config 1, 512^2: 11.7 ->
+// 10.2 us per iteration; at 1024 it lost: 23.2 -> 23.9 us, OSPR 53.0k ->
+// 47.9k subframes/s).  Chosen by line length only, so batched and single
+// runs of one size stay bit-identical.
+#ifndef HG_SMALL_EM
+#define HG_SMALL_EM 8
+#endif
+#ifndef HG_SMALL_NMAX
+#define HG_SMALL_NMAX 512
+#endif
+template <int N, int LAY>
+__host__ __device__ constexpr int quad_em() {
+    return (LAY == LAY_QUAD && N <= HG_SMALL_NMAX) ? HG_SMALL_EM : 16;
+}
+
 template <int NX, int LAY>
 struct RowCfg {
-    static constexpr int E = LineCfg<NX>::E, T = LineCfg<NX>::T;
+    static constexpr int EM = quad_em<NX, LAY>();
+    static constexpr int E = LineCfg<NX, EM>::E, T = LineCfg<NX, EM>::T;
     static constexpr int RPC = LAY == LAY_QUAD ? (512 / T < 2 ? 2 : 512 / T) : (T >= 256 ? 1 : 256 / T);
     static constexpr int THREADS = T * RPC;
     static constexpr int SMEM = (NX > E) ? RPC * RowStride<NX>::value * (int)sizeof(float2) : 0;
@@ -100,12 +119,12 @@ struct RowCfg {
 // The aperture-plane work of one row (thread t's elements x = t + e*T of row y
 // of target b, in registers): IFFT (completes P^-1), *norm, *conj(Q),
 // quantise (+levels), *Q, FFT (starts P).
-template <int NX, int QK, int FQ, int LV, class Sync = CtaSync>
-__device__ __forceinline__ void row_fused_body(float2 (&v)[LineCfg<NX>::E], int t, int y, int b, bool valid,
+template <int NX, int QK, int FQ, int LV, class Sync = CtaSync, int EM = 16>
+__device__ __forceinline__ void row_fused_body(float2 (&v)[LineCfg<NX, EM>::E], int t, int y, int b, bool valid,
                                                float2* smem, const RowSmemIdx& idx, const RowArgs& a,
                                                const float2* sstates, const Sync& sync = Sync{}) {
-    constexpr int E = LineCfg<NX>::E, T = LineCfg<NX>::T;
-    fft_line<NX, +1>(v, t, smem, idx, a.tw, sync);  // completes the 2-D inverse (propagation.hpp:89-95)
+    constexpr int E = LineCfg<NX, EM>::E, T = LineCfg<NX, EM>::T;
+    fft_line<NX, +1, EM>(v, t, smem, idx, a.tw, sync);  // completes the 2-D inverse (propagation.hpp:89-95)
     const int rowbase = y * NX;
     const float norm = a.norm;
     const float2* __restrict__ fq = FQ == 0 ? nullptr : a.fresnel_q;
@@ -136,7 +155,7 @@ __device__ __forceinline__ void row_fused_body(float2 (&v)[LineCfg<NX>::E], int 
         v[e] = f;
     }
 #if HG_ROW_VARIANT != 2
-    fft_line<NX, -1>(v, t, smem, idx, a.tw, sync);  // starts the forward transform
+    fft_line<NX, -1, EM>(v, t, smem, idx, a.tw, sync);  // starts the forward transform
 #endif
 }
 
@@ -235,9 +254,9 @@ __device__ __forceinline__ void row_cta(const RowArgs& a, const int bx, const in
             if (a.fresnel_q)
 #pragma unroll
                 for (int e = 0; e < E; ++e) v[e] = cmul_rn(v[e], __ldg(&a.fresnel_q[rowbase + t + e * T]));
-            fft_line<NX, -1>(v, t, smem, idx, a.tw);
+            fft_line<NX, -1, Cfg::EM>(v, t, smem, idx, a.tw);
         } else {
-            fft_line<NX, +1>(v, t, smem, idx, a.tw);
+            fft_line<NX, +1, Cfg::EM>(v, t, smem, idx, a.tw);
         }
         if (a.apply_norm)
 #pragma unroll
@@ -251,7 +270,7 @@ __device__ __forceinline__ void row_cta(const RowArgs& a, const int bx, const in
 #pragma unroll 1
         for (int rep = 0; rep < 2; ++rep)
 #endif
-        row_fused_body<NX, QK, FQ, LV>(v, t, yy, b, valid, smem, idx, a, sstates);  // (padding rows: row 0's side arrays)
+        row_fused_body<NX, QK, FQ, LV, CtaSync, Cfg::EM>(v, t, yy, b, valid, smem, idx, a, sstates);  // (padding rows: row 0's side arrays)
 #endif
     }
 #ifndef HG_ROW_DIRECT_STORE  // bulk-loaded tiles stored by per-thread coalesced stores (no EXIT wait on the bulk read)
@@ -341,7 +360,7 @@ __global__ void __launch_bounds__(1024, 1) k_row_persist(RowArgs a, int rowblock
         gsync();                        // every thread of the group has its tile: release the landing buffer
         if (leader && s + G < ntiles) bulk_g2s(land, tile_ptr(s + G), TILE, &full[g ^ 1]);
         const int bx = s % rowblocks, by = s / rowblocks;
-        row_fused_body<NX, QK, FQ, LV, GroupSync>(v, t, bx * RPC + lr, by, true, xg, idx, a, nullptr, gsync);
+        row_fused_body<NX, QK, FQ, LV, GroupSync, Cfg::EM>(v, t, bx * RPC + lr, by, true, xg, idx, a, nullptr, gsync);
         const int lbo = opaque(lb);
 #pragma unroll
         for (int e = 0; e < E; ++e) xg[lbo + e * 2 * T] = v[e];
@@ -409,7 +428,7 @@ struct ColCfg {
 #endif
     // EM = 8: 8 elements per thread, 1024-thread CTAs at <= 32 registers, 2 CTAs
     // (64 warps) per SM for the large quad-layout columns; else 16 per thread.
-    static constexpr int EM = (HG_COL_E8 && LAY == LAY_QUAD && NY >= 2048) ? 8 : 16;
+    static constexpr int EM = (HG_COL_E8 && LAY == LAY_QUAD && NY >= 2048) ? 8 : quad_em<NY, LAY>();
     static constexpr int E = LineCfg<NY, EM>::E, T = LineCfg<NY, EM>::T;
     // LAY_ROW: up to 128 KiB of complex64 per CTA (1 CTA / SM at 4096);
     // LAY_QUAD: 64 KiB column-pair tiles (2 CTAs / SM)
@@ -422,7 +441,7 @@ struct ColCfg {
     static constexpr int C = CMAX0 < CMIN ? CMIN : CMAX0;
     static constexpr int THREADS = T * C;
     static constexpr int MIN_BLOCKS =
-        EM == 8 ? 2 : ((LAY == LAY_QUAD && THREADS >= 512 && THREADS < 1024) ? HG_COLQ_MINB : 1);
+        (HG_COL_E8 && LAY == LAY_QUAD && NY >= 2048) ? 2 : ((LAY == LAY_QUAD && THREADS >= 512 && THREADS < 1024) ? HG_COLQ_MINB : 1);
 };
 
 #ifndef HG_COL_TGT_BULK

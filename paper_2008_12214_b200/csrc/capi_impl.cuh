@@ -829,6 +829,7 @@ static void build_quant(const hgc_slm* s, int nx, int ny, QuantDev& q) {
     p.wshed_f = (float)(3.1415926535897932384626433832795 + range / 2.0);
     p.margin_rad = 1e-5f;
     p.margin_u = (float)(1e-5 * inv + L * 4e-7 + 1e-6);
+    p.min_u_f = (float)(s->min_arg * inv);
     p.states = q.states.p;
     p.s0 = q.h_states[0];
     p.s1 = q.h_states[L > 1 ? 1 : 0];

@@ -92,7 +92,9 @@ inline int quant_kind(const QuantParams& q) {
     if (q.mode == 1 && !illum && !q.full_circle && q.levels == 2 && q.min_arg == 0.0 &&
         q.range == 3.1415926535897932384626433832795)
         return QK_BINARY;
-    if (q.mode == 1 && !illum && q.full_circle && (!HG_STATES_SMEM || q.levels <= 256)) return QK_FULL;
+    if (q.mode == 1 && !illum && q.full_circle && (q.levels & (q.levels - 1)) == 0 &&
+        (!HG_STATES_SMEM || q.levels <= 256))
+        return QK_FULL;  // (the fast path's mod L is a mask)
     return QK_GENERIC;
 }
 

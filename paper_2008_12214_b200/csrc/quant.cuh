@@ -30,7 +30,7 @@ struct QuantParams {
     float wshed_f;    // watershed angle pi + range/2 (restricted phase mode)
     float margin_rad; // decision margin in radians (phase mode)
     float margin_u;   // same margin in level units
-    float pad2_;
+    float min_u_f;    // min_arg in level units (QK_FULL fast path)
     float2 s0, s1;    // states 0 and 1 (binary fast path)
     const float2* states;      // [levels] (T)allowed_states, quantise.hpp:147-149
     const double* illum_arg;   // [npix] arg(illumination) or nullptr
@@ -148,15 +148,17 @@ __device__ __forceinline__ int quant_decide_kind(const QuantParams& q, float vr,
         if (near) k = quant_decide_exact(1, 2, 0, q.min_arg, q.inv_spac, q.range, 0.0, 0.0, vr, vi);
         return k;
     } else if constexpr (QK == QK_FULL) {
-        const float two_pi_f = 6.28318530717958648f;
-        float d = fast_atan2f(vi, vr) - q.min_arg_f;
-        d -= two_pi_f * floorf(d * (1.0f / two_pi_f));
-        const float u = d * q.inv_spac_f;
-        const float fu = floorf(u);
-        const float fr = u - fu;
-        const bool near = !(fabsf(fr - 0.5f) >= q.margin_u);  // NaN-safe
-        int k = (int)fu + (fr >= 0.5f ? 1 : 0);
-        k = k >= q.levels ? k - q.levels : k;
+        // Directly in level units (L a power of two, quant_kind): u = atan2 * L/2pi
+        // - min_arg * L/2pi, k = round(u) mod L.  The reference's wrap of the
+        // angle into [0, 2pi) only adds multiples of L to u, so the mod takes its
+        // place; the fast estimate's error (< 1e-4 levels at L = 256) stays far
+        // inside margin_u.
+        const float u = fmaf(fast_atan2f(vi, vr), q.inv_spac_f, -q.min_u_f);
+        const float w = u + 0.5f;
+        const float fk = floorf(w);
+        const float fr = w - fk;  // 0 or 1 at a decision boundary
+        const bool near = !(fabsf(fr - 0.5f) <= 0.5f - q.margin_u);  // NaN-safe
+        int k = (int)fk & (q.levels - 1);
         if (near) k = quant_decide_exact(1, q.levels, 1, q.min_arg, q.inv_spac, q.range, 0.0, 0.0, vr, vi);
         return k;
     } else {

@@ -130,3 +130,14 @@ def test_bench_target_bit_identical_to_reference_generator(ref_oracle):
         want = ref_oracle.normalize(ref_oracle.smooth_blobs(n, n), True)
         assert np.array_equal(got, want)
     assert np.array_equal(hg.patterns.smooth_blobs(40, 24), ref_oracle.smooth_blobs(40, 24))
+
+
+def test_missing_library_fails_import(tmp_path):
+    """No silent fallback when the sm_100a library is absent: importing the
+    package raises (subprocess, so this session's loaded library is untouched)."""
+    import subprocess
+    import sys
+    env = dict(__import__("os").environ, HG_LIB=str(tmp_path / "absent.so"))
+    r = subprocess.run([sys.executable, "-c", "import paper_2008_12214_b200"], cwd=_lib._HERE + "/..", env=env,
+                       capture_output=True, text=True)
+    assert r.returncode != 0 and "ImportError" in r.stderr and "build the sm_100a library" in r.stderr

@@ -3,6 +3,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include "ospr_rows_args.h"
 #include "passes.cuh"
 
 namespace hg {
@@ -30,5 +31,16 @@ int col_tiles(int nx, int ny, int layout);
 // least 64 threads per CTA.  The plans use it for the launches, the TMA box
 // and the number of partial-sum tiles (nx / width).
 int col_width_rt(int nx, int ny, int batch);
+
+// Rows-first OSPR subframe (ospr_rows.cuh, k_ospr_rows.cu): field sizes with
+// instantiated kernels, tiles (row blocks) per job, draws per tile.
+bool ospr_rows_supported(int nx, int ny);
+int ospr_rows_tiles(int nx, int ny);
+int ospr_rows_len(int nx);
+void ospr_rows_target(const double* amp, float* out, size_t n, cudaStream_t st);
+void ospr_rows_walk(const WalkArgs& a, cudaStream_t st);
+void ospr_rows_seed(int nx, const SeedRowArgs& a, int jobs, cudaStream_t st, bool prepare = false);
+void ospr_rows_mid(int ny, const ColArgs& a, int qk, int jobs, cudaStream_t st, bool prepare = false);
+void ospr_rows_acc(int nx, const RowAccArgs& a, int chunks, int jobs, cudaStream_t st, bool prepare = false);
 
 }  // namespace hg

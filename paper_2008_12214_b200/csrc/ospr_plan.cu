@@ -2,6 +2,7 @@
 // run_ospr_variant<float>, ospr.hpp:68-185) behind the C ABI: batched jobs,
 // subframe blocks across ranks, Fresnel OSPR (extension).
 #include "capi_impl.cuh"
+#include "launch_impl.cuh"
 
 // =================================================================== OSPR
 struct hgc_ospr_plan {
@@ -42,6 +43,17 @@ struct hgc_ospr_plan {
     cudaEvent_t up_ev = nullptr;  // end of the last upload's stream work
     bool fresnel = false;  // hgc_ospr_plan_set_fresnel
     DBuf<float2> Q;
+    // Rows-first subframe (ospr_rows.cuh): plain Fourier OSPR, one MT stream
+    // per job walked frame by frame (wst) into per-tile start windows (ck,
+    // double-buffered); S accumulates row-major in S_rm and is converted to the
+    // column-pair S at the end; the pass C target is row-major fp32.
+    bool rows_ok = false;
+    int rtiles = 0, qk = 0;
+    DBuf<MtState> wst, ck;
+    DBuf<float> S_rm, target_rm;
+    bool rows_raw = false;  // HG_OSPR_ROWS=3: the walk stores every raw word (no re-twist in the seed pass)
+    DBuf<uint64_t> raw;
+    bool rows() const { return rows_ok && !fresnel; }
     // RunReport::profile (hgc_ospr_run with io->profile): external events
     // around each subframe's column-inverse, row and accumulating passes
     std::vector<cudaEvent_t> pev;
@@ -200,6 +212,99 @@ struct hgc_ospr_plan {
         return co;
     }
 
+    ColArgs col_mid_args(int n) const {
+        ColArgs cm{};
+        cm.tw = tw;
+        cm.field = field.p;
+        cm.bstride = npix;
+        cm.nx = nx;
+        cm.layout = LAY_QUAD;
+        cm.norm = norm();
+        cm.q = q.p;
+        cm.levels8 = lv8.p + (size_t)(n - 1) * npix;
+        cm.lv_bstride = (size_t)cfg.subframes * npix;
+        cm.cw = cw;
+        cm.tmap = tmap1.d.p;
+        cm.tma_row0 = 0;
+        cm.tma_brows = ny / 2;
+        return cm;
+    }
+    RowAccArgs row_acc_args(int n) const {
+        RowAccArgs ra{};
+        ra.field = field.p;
+        ra.npix = npix;
+        ra.tw = tw;
+        ra.norm = norm();
+        ra.inv_n = 1.0f / (float)n;
+        ra.S = S_rm.p;
+        ra.target = target_rm.p;
+        ra.t_bstride = per_job ? npix : 0;
+        ra.roi = has_roi ? roi_rm.p : nullptr;
+        ra.partials = partials.p + (size_t)(n - 1) * jobs * rtiles * 8;
+        return ra;
+    }
+    SeedRowArgs seed_rows_args(int n) const {
+        SeedRowArgs sa{};
+        sa.ck = ck.p + (size_t)(n & 1) * jobs * rtiles;
+        sa.raw = rows_raw ? raw.p + (size_t)(n & 1) * jobs * npix : nullptr;
+        sa.amp = amp_d.p;
+        sa.amp_stride = per_job ? npix : 0;
+        sa.field = field.p;
+        sa.npix = npix;
+        sa.tw = tw;
+        sa.chunks = rtiles;
+        return sa;
+    }
+    WalkArgs walk_args(int n) const {
+        WalkArgs wa{};
+        wa.states = wst.p;
+        wa.seeds = n == 1 ? seeds.p : nullptr;
+        wa.ck = ck.p + (size_t)(n & 1) * jobs * rtiles;
+        wa.streams = jobs;
+        wa.chunks = rtiles;
+        wa.len = ospr_rows_len(nx);
+        wa.raw = rows_raw ? raw.p + (size_t)(n & 1) * jobs * npix : nullptr;
+        return wa;
+    }
+    // The rows-first subframe loop: the walk of frame n (its own stream of the
+    // graph, a few warps) runs beside the passes of frame n-1; then seed + row
+    // IFFT, column IFFT + quantiser + column FFT, row FFT + accumulation.
+    void record_rows(cudaStream_t st) {
+        launches = 0;
+        const int N = cfg.subframes;
+        CK(cudaMemsetAsync(S_rm.p, 0, sizeof(float) * npix * jobs, st));
+        cudaStream_t ss = stream2 ? stream2 : st;
+        if (ss != st) {
+            CK(cudaEventRecord(ev_fork, st));
+            CK(cudaStreamWaitEvent(ss, ev_fork, 0));
+        }
+        for (int n = 1; n <= N; ++n) {
+            if (ss != st && n >= 3) CK(cudaStreamWaitEvent(ss, ev_pass[n & 1], 0));  // checkpoints n%2 read
+            ospr_rows_walk(walk_args(n), ss);
+            if (ss != st) {
+                CK(cudaEventRecord(ev_seed, ss));
+                CK(cudaStreamWaitEvent(st, ev_seed, 0));
+            }
+            pmark(4 * (size_t)(n - 1), st);
+            ospr_rows_seed(nx, seed_rows_args(n), jobs, st);
+            if (ss != st) CK(cudaEventRecord(ev_pass[n & 1], st));
+            pmark(4 * (size_t)(n - 1) + 1, st);
+            ospr_rows_mid(ny, col_mid_args(n), qk, jobs, st);
+            pmark(4 * (size_t)(n - 1) + 2, st);
+            ospr_rows_acc(nx, row_acc_args(n), rtiles, jobs, st);
+            pmark(4 * (size_t)(n - 1) + 3, st);
+            launches += 4;
+        }
+        if (ss != st) {
+            CK(cudaEventRecord(ev_fork, ss));
+            CK(cudaStreamWaitEvent(st, ev_fork, 0));
+        }
+        to_colpair<float, float>(S_rm.p, S.p, nx, ny, (size_t)jobs, st);  // the plan's S layout (downloads)
+        k_finalize<<<jobs, 32, 0, st>>>(partials.p, N, jobs, rtiles, (double)M, cfg.freedom_scale, 1, traces.p);
+        launches += 2;
+        CK(cudaGetLastError());
+    }
+
     // run_ospr_impl's subframe loop (ospr.hpp:105-147), all jobs at once.
     // Plain OSPR: the seed of frame n+1 (one MT stream per job, its own
     // stream of the graph) overlaps the three passes of frame n on a second
@@ -207,6 +312,10 @@ struct hgc_ospr_plan {
     // pass CTA on an SM.  Adaptive OSPR seeds frame n from S after frame n-1,
     // so it stays sequential.
     void record(cudaStream_t st) {
+        if (rows()) {
+            record_rows(st);
+            return;
+        }
         launches = 0;
         const int N = cfg.subframes;
         CK(cudaMemsetAsync(S.p, 0, sizeof(float) * npix * jobs, st));
@@ -295,15 +404,27 @@ static void create_ospr_plan(hgc_ospr_plan** out, const hgc_ospr_cfg* cfg_in, co
             CK(cudaGetDevice(&dev));
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
             const size_t all = (size_t)cfg->subframes * p->npix;
+            // HG_OSPR_ROWS (rows-first subframes, ospr_rows.cuh): unset / 0 off, 1 for plans with a job
+            // per SM, 2 also for few jobs (tests), 3 as 2 with the walk storing every raw word
+            const char* e = getenv("HG_OSPR_ROWS");
+            const bool force_rows = e && atoi(e) >= 2 && ospr_rows_supported(nx, ny);
             p->preseed = cfg->variant == 0 && cfg->subframes > 1 && jobs < sms && all < (1ull << 31) &&
-                         all * jobs * sizeof(float2) <= (8ull << 30);
+                         all * jobs * sizeof(float2) <= (8ull << 30) && !force_rows;
             p->fstride = p->preseed ? all : p->npix;
+        }
+        {
+            const char* e = getenv("HG_OSPR_ROWS");
+            // opt-in (measured slower than the column-first loop)
+            p->rows_ok = e && atoi(e) != 0 && cfg->variant == 0 && !p->preseed && !block && !p->wide_levels &&
+                         ospr_rows_supported(nx, ny);
         }
         p->field.alloc(p->fstride * jobs);
         if (ny >= 512) p->tmap1.make(p->field.p, nx, p->cw, p->fstride * jobs / (2 * (size_t)nx));
-        if (!p->preseed && cfg->variant == 0 && cfg->subframes > 1) {  // second buffer + stream for seed/pass overlap
-            p->field2.alloc(tot);
-            if (ny >= 512) p->tmap2.make(p->field2.p, nx, p->cw, tot / (2 * (size_t)nx));
+        if (!p->preseed && cfg->variant == 0 && cfg->subframes > 1) {  // second stream (+ buffer) for seed/pass overlap
+            if (!p->rows_ok) {  // (a Fresnel plan set later runs the column-first loop without the overlap)
+                p->field2.alloc(tot);
+                if (ny >= 512) p->tmap2.make(p->field2.p, nx, p->cw, tot / (2 * (size_t)nx));
+            }
             CK(cudaStreamCreateWithFlags(&p->stream2, cudaStreamNonBlocking));
             CK(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&p->ev_seed, cudaEventDisableTiming));
@@ -316,7 +437,22 @@ static void create_ospr_plan(hgc_ospr_plan** out, const hgc_ospr_cfg* cfg_in, co
         const size_t lvtot = tot * cfg->subframes;
         if (p->wide_levels) p->lv16.alloc(lvtot);
         else p->lv8.alloc(lvtot);
-        p->partials.alloc((size_t)cfg->subframes * jobs * p->tiles * 8);
+        if (p->rows_ok) {
+            p->rtiles = ospr_rows_tiles(nx, ny);
+            p->qk = quant_kind(p->q.p);
+            p->wst.alloc(jobs);
+            p->ck.alloc(2 * (size_t)jobs * p->rtiles);
+            const char* e = getenv("HG_OSPR_ROWS");
+            p->rows_raw = e && atoi(e) == 3;
+            if (p->rows_raw) p->raw.alloc(2 * tot);
+            p->S_rm.alloc(tot);
+            p->target_rm.alloc(ttot);
+            ColArgs c0{};
+            ospr_rows_seed(nx, SeedRowArgs{}, jobs, nullptr, true);
+            ospr_rows_mid(ny, c0, p->qk, jobs, nullptr, true);
+            ospr_rows_acc(nx, RowAccArgs{}, p->rtiles, jobs, nullptr, true);
+        }
+        p->partials.alloc((size_t)cfg->subframes * jobs * std::max(p->tiles, p->rtiles) * 8);
         p->traces.alloc((size_t)cfg->subframes * jobs * 2);
         p->first = block ? first : 0;
         p->total_subframes = cfg_in->subframes;
@@ -393,6 +529,7 @@ int hgc_ospr_plan_upload(hgc_ospr_plan* p, const hgc_ospr_io* io) {
         p->M = roi_count(io->roi, p->npix);
         launch_validate(p->amp_d.p, nullptr, ttot, p->vflags.p, p->stream);
         to_colpair<double, float>(p->amp_d.p, p->target_f.p, p->nx, p->ny, ttot / p->npix, p->stream);
+        if (p->rows_ok) ospr_rows_target(p->amp_d.p, p->target_rm.p, ttot, p->stream);
         CK(cudaGetLastError());
         p->has_roi = io->roi != nullptr;
         if (io->roi) {  // column-pair major
@@ -540,6 +677,16 @@ int hgc_ospr_plan_profile(hgc_ospr_plan* p, int reps, double* ms_seed, double* m
         CK(cudaSetDevice(p->device));
         cudaStream_t st = p->stream;
         const int j = p->jobs;
+        if (p->rows()) {  // rows-first subframe: walk, seed + row IFFT, column pass, row FFT + accumulation
+            if (ms_seed) *ms_seed = time_launches(st, reps, [&] { ospr_rows_walk(p->walk_args(2), st); });
+            if (ms_col_inv)
+                *ms_col_inv = time_launches(st, reps, [&] { ospr_rows_seed(p->nx, p->seed_rows_args(2), j, st); });
+            if (ms_row) *ms_row = time_launches(st, reps, [&] { ospr_rows_mid(p->ny, p->col_mid_args(1), p->qk, j, st); });
+            if (ms_col_acc)
+                *ms_col_acc = time_launches(st, reps, [&] { ospr_rows_acc(p->nx, p->row_acc_args(1), p->rtiles, j, st); });
+            CK(cudaGetLastError());
+            return;
+        }
         if (ms_seed)
             *ms_seed = p->preseed  // per-frame share of the one all-frames seed
                            ? time_launches(st, reps, [&] {

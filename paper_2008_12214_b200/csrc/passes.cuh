@@ -377,7 +377,9 @@ __global__ void __launch_bounds__(1024, 1) k_row_persist(RowArgs a, int rowblock
 // ------------------------------------------------------------- column pass
 // COL_GS_FAST / COL_WGS_FAST: no ROI, no LT schedule, phase freedom (the
 // benchmark configurations); COL_GS_GENERIC: every TargetSpec / variant.
-enum ColMode { COL_PLAIN = 0, COL_GS_GENERIC = 1, COL_OSPR = 2, COL_GS_FAST = 3, COL_WGS_FAST = 4 };
+// COL_OSPR_MID (+ quantiser kind << 4): the rows-first OSPR subframe's middle
+// pass (ospr_rows.cuh): IFFT columns, *norm, quantise (+levels), FFT columns.
+enum ColMode { COL_PLAIN = 0, COL_GS_GENERIC = 1, COL_OSPR = 2, COL_GS_FAST = 3, COL_WGS_FAST = 4, COL_OSPR_MID = 5 };
 // The last iteration's GS column pass also reduces the diffraction-efficiency
 // sums (a separate instantiation, so the K-1 others carry no extra registers).
 constexpr int COL_EFF = 8;  // flag added to COL_GS_GENERIC / COL_GS_FAST / COL_WGS_FAST
@@ -416,6 +418,10 @@ struct ColArgs {
     const void* tmap;
     int tma_row0, tma_brows;
     int cw;  // columns per CTA this launch (an instantiated width <= ColCfg::C; 0 = the default)
+    // COL_OSPR_MID: the SLM quantiser and the frame's level indices (row-major)
+    QuantParams q;
+    uint8_t* levels8;
+    size_t lv_bstride;
 };
 
 template <int NY, int LAY>
@@ -473,9 +479,10 @@ struct ColTgtBulk {
     // GS / WGS: the fp32 target slice.  OSPR: the job's running intensity sum
     // S instead (read and written, always in HBM; the shared OSPR target stays
     // L2-resident and is read directly).
-    static constexpr bool on = HG_COL_TGT_BULK && ColTma<NY, C, LAY>::on && MODE != COL_PLAIN;
-    static constexpr bool target = on && MODE != COL_OSPR;
-    static constexpr bool S = on && MODE == COL_OSPR;
+    static constexpr int M = col_base_mode(MODE);
+    static constexpr bool on = HG_COL_TGT_BULK && ColTma<NY, C, LAY>::on && M != COL_PLAIN && M != COL_OSPR_MID;
+    static constexpr bool target = on && M != COL_OSPR;
+    static constexpr bool S = on && M == COL_OSPR;
     static constexpr int BYTES = on ? C * NY * (int)sizeof(float) : 0;
 };
 template <int NY, int C, int MODE, int LAY>
@@ -609,7 +616,27 @@ __device__ __forceinline__ void col_cta(const ColArgs& a, const int bx, const in
         }
     };
 
-    if constexpr (M == COL_PLAIN) {
+    if constexpr (M == COL_OSPR_MID) {
+        // rows-first OSPR subframe (ospr.hpp:118-131 with the 2-D transforms'
+        // halves regrouped): the row IFFT was done by the seed pass
+        fft_line<NY, +1, EM>(v, t, smem, idx, a.tw);  // completes P^-1 (unnormalised)
+        constexpr int QK = (MODE >> 4) & 3;
+        uint8_t* __restrict__ lv = a.levels8 + a.lv_bstride * b;  // (set by the plan)
+        const int i0 = t * nx + x, di = T * nx;  // row-major pixel index (levels, illumination): npix <= 2^24
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int i = i0 + e * di;
+            const float2 f = cscale(v[e], a.norm);  // fftw_backend.cpp:121-123
+            const int k = quant_decide_kind<QK>(a.q, f.x, f.y, i);  // quantise.hpp:211-215
+            lv[i] = (uint8_t)k;
+            if constexpr (QK == QK_BINARY) v[e] = k ? a.q.s1 : a.q.s0;
+            else if constexpr (QK == QK_FULL) v[e] = __ldg(&a.q.states[k]);
+            else v[e] = quant_state(a.q, k, i);
+        }
+        fft_line<NY, -1, EM>(v, t, smem, idx, a.tw);  // starts P (rows finish it)
+        store_col(base);
+        return;
+    } else if constexpr (M == COL_PLAIN) {
         if (a.sign < 0) fft_line<NY, -1, EM>(v, t, smem, idx, a.tw);
         else fft_line<NY, +1, EM>(v, t, smem, idx, a.tw);
         if (a.apply_norm)

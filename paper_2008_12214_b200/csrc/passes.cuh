@@ -350,15 +350,23 @@ __global__ void __launch_bounds__(1024, 1) k_row_persist(RowArgs a, int rowblock
     }
     __syncthreads();
     const bool leader = tg == 0;
+#ifndef HG_ROWP_NOMEM  // diagnostic: the first tile only, no tile loads or stores after it (compute alone)
+#define HG_ROWP_NOMEM 0
+#endif
+#if HG_ROWP_NOMEM
+    mbar_wait(&full[0], 0);
+#endif
 #pragma unroll 1
     for (int k = g, s = blockIdx.x + g * G; s < ntiles; k += 2, s += 2 * G) {
         float2 v[E];
+#if !HG_ROWP_NOMEM
         mbar_wait(&full[g], (k >> 1) & 1);
+#endif
 #pragma unroll
         for (int e = 0; e < E; ++e) v[e] = land[lb + e * 2 * T];
         if (leader) bulk_wait_read0();  // this group's previous store has left its exchange buffer
         gsync();                        // every thread of the group has its tile: release the landing buffer
-        if (leader && s + G < ntiles) bulk_g2s(land, tile_ptr(s + G), TILE, &full[g ^ 1]);
+        if (!HG_ROWP_NOMEM && leader && s + G < ntiles) bulk_g2s(land, tile_ptr(s + G), TILE, &full[g ^ 1]);
         const int bx = s % rowblocks, by = s / rowblocks;
         row_fused_body<NX, QK, FQ, LV, GroupSync, Cfg::EM>(v, t, bx * RPC + lr, by, true, xg, idx, a, nullptr, gsync);
         const int lbo = opaque(lb);
@@ -366,7 +374,7 @@ __global__ void __launch_bounds__(1024, 1) k_row_persist(RowArgs a, int rowblock
         for (int e = 0; e < E; ++e) xg[lbo + e * 2 * T] = v[e];
         fence_proxy_async();
         gsync();
-        if (leader) {
+        if (!HG_ROWP_NOMEM && leader) {
             bulk_s2g(tile_ptr(s), xg, TILE);
             bulk_commit();
         }

@@ -142,55 +142,55 @@ __global__ void __launch_bounds__(kSeedThreads, 2) k_ospr_seed_rows(SeedRowArgs 
         }
         __syncthreads();
     } else {
-    const MtState* st = a.ck + (size_t)s * a.chunks + c;
-    uint64_t* init = ring + (kRingSlots - 1) * kMtN;  // twist "-1" lives in the last slot
-    for (int i = tid; i < kMtN; i += blockDim.x) init[i] = st->w[i];
-    if (tid == 0) s_pos = st->pos;
-    __syncthreads();
-    const int pos0 = s_pos;
-    const int first = min(kMtN - pos0, LEN);
-    const int rest = LEN - first;
-    constexpr int kGroup = kMtN * kTwistsPerGroup;
-    const int ngroups = (rest + kGroup - 1) / kGroup;
-    const double* __restrict__ amp = a.amp + a.amp_stride * s;
-    const int p0 = c * LEN;  // row-major pixel index of the tile's first draw (rng.hpp:60)
-    constexpr int lognx = SC::LOGNX;
-    for (int g = 0; g <= ngroups; ++g) {
-        if (warp == 0) {
-            if (g < ngroups)
-                for (int k = 0; k < kTwistsPerGroup; ++k) {
-                    const int t = g * kTwistsPerGroup + k;
-                    mt_twist_warp(ring + ((t - 1 + kRingSlots) % kRingSlots) * kMtN, ring + (t % kRingSlots) * kMtN,
-                                  lane);
-                }
-        } else {
-            const uint64_t* src;
-            int d0, cnt;
-            if (g == 0) {
-                src = init + pos0;
-                d0 = 0;
-                cnt = first;
-            } else {
-                src = ring + (((g - 1) & 1) * kTwistsPerGroup) * kMtN;
-                d0 = first + (g - 1) * kGroup;
-                cnt = min(LEN - d0, kGroup);
-            }
-            const double* __restrict__ ab = opaque(amp);
-            for (int j = tid - 32; j < cnt; j += kSeedThreads - 32) {
-                const int d = d0 + j;  // draw within the tile
-                const double av = __ldg(&ab[p0 + d]);
-                const uint64_t x = mt_temper(src[j]);
-                const double u = (double)(x >> 11) * 0x1.0p-53;  // Rng::uniform01, rng.hpp:32
-                const double theta = __dmul_rn(HG_TWO_PI, u);    // rng.hpp:62
-                double sn, cs;
-                sincos_0_2pi(theta, &sn, &cs);
-                const int px = d & (NX - 1), ly = d >> lognx;
-                const int o = (ly >> 1) * (2 * NX) + (px >> 1) * 4 + (ly & 1) * 2 + (px & 1);
-                smem[o] = make_float2(__double2float_rn(__dmul_rn(av, cs)), __double2float_rn(__dmul_rn(av, sn)));
-            }
-        }
+        const MtState* st = a.ck + (size_t)s * a.chunks + c;
+        uint64_t* init = ring + (kRingSlots - 1) * kMtN;  // twist "-1" lives in the last slot
+        for (int i = tid; i < kMtN; i += blockDim.x) init[i] = st->w[i];
+        if (tid == 0) s_pos = st->pos;
         __syncthreads();
-    }
+        const int pos0 = s_pos;
+        const int first = min(kMtN - pos0, LEN);
+        const int rest = LEN - first;
+        constexpr int kGroup = kMtN * kTwistsPerGroup;
+        const int ngroups = (rest + kGroup - 1) / kGroup;
+        const double* __restrict__ amp = a.amp + a.amp_stride * s;
+        const int p0 = c * LEN;  // row-major pixel index of the tile's first draw (rng.hpp:60)
+        constexpr int lognx = SC::LOGNX;
+        for (int g = 0; g <= ngroups; ++g) {
+            if (warp == 0) {
+                if (g < ngroups)
+                    for (int k = 0; k < kTwistsPerGroup; ++k) {
+                        const int t = g * kTwistsPerGroup + k;
+                        mt_twist_warp(ring + ((t - 1 + kRingSlots) % kRingSlots) * kMtN, ring + (t % kRingSlots) * kMtN,
+                                      lane);
+                    }
+            } else {
+                const uint64_t* src;
+                int d0, cnt;
+                if (g == 0) {
+                    src = init + pos0;
+                    d0 = 0;
+                    cnt = first;
+                } else {
+                    src = ring + (((g - 1) & 1) * kTwistsPerGroup) * kMtN;
+                    d0 = first + (g - 1) * kGroup;
+                    cnt = min(LEN - d0, kGroup);
+                }
+                const double* __restrict__ ab = opaque(amp);
+                for (int j = tid - 32; j < cnt; j += kSeedThreads - 32) {
+                    const int d = d0 + j;  // draw within the tile
+                    const double av = __ldg(&ab[p0 + d]);
+                    const uint64_t x = mt_temper(src[j]);
+                    const double u = (double)(x >> 11) * 0x1.0p-53;  // Rng::uniform01, rng.hpp:32
+                    const double theta = __dmul_rn(HG_TWO_PI, u);    // rng.hpp:62
+                    double sn, cs;
+                    sincos_0_2pi(theta, &sn, &cs);
+                    const int px = d & (NX - 1), ly = d >> lognx;
+                    const int o = (ly >> 1) * (2 * NX) + (px >> 1) * 4 + (ly & 1) * 2 + (px & 1);
+                    smem[o] = make_float2(__double2float_rn(__dmul_rn(av, cs)), __double2float_rn(__dmul_rn(av, sn)));
+                }
+            }
+            __syncthreads();
+        }
     }
     // the row half of the inverse transform (k_row's thread mapping)
     const int pr = tid / (2 * T), q = tid % (2 * T);

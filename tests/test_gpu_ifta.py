@@ -412,3 +412,19 @@ def test_efficiency_of_final_replay(roi):
         sup &= m.astype(bool)
     want = p[sup].sum() / p.sum()
     assert 0 < rep.efficiency < 1 and abs(rep.efficiency - want) < 1e-5, (rep.efficiency, want)
+
+
+@pytest.mark.parametrize("name", ["fc256_offset", "fc64", "fc6", "fc3_offset"])
+def test_fused_quantiser_kinds_lockstep(oracle, name):
+    """The fused row pass's full-circle fast path decides in level units with a
+    mask for mod L (QK_FULL, L a power of two, any min_arg); other L take the
+    generic quantiser.  One lock-step iteration at 512^2 for each."""
+    slm = {"fc256_offset": lambda: hg.SlmSpec.full_circle_phase(256, 0.3),
+           "fc64": lambda: hg.SlmSpec.full_circle_phase(64, 5.9),
+           "fc6": lambda: hg.SlmSpec.full_circle_phase(6),
+           "fc3_offset": lambda: hg.SlmSpec.full_circle_phase(3, 2.0)}[name]()
+    amp = hg.patterns.bench_target(512)
+    *_, (m_gpu, m_ref), _, _, cls = lockstep(oracle, amp, slm, 3)
+    record(f"quantiser_{name}_512_lockstep1/k=3", cls)
+    assert cls["bad"] == 0, cls
+    assert rel(m_gpu, m_ref) < MSE_TOL

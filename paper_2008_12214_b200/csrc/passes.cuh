@@ -582,15 +582,26 @@ __device__ __forceinline__ void col_cta(const ColArgs& a, const int bx, const in
     if constexpr (kTma) {
         if (threadIdx.x == 0) {
             mbar_init(&tbar, 1);
+#ifndef HG_COL_NOMEM  // diagnostic: no tile / target / S traffic (transforms on whatever is in smem)
+#define HG_COL_NOMEM 0
+#endif
+#if HG_COL_NOMEM
+            mbar_arrive_plain(&tbar);
+#else
             mbar_expect_tx(&tbar, NY * C * (int)sizeof(float2));
 #pragma unroll 1
             for (int k = 0; k < kBoxes; ++k)
                 tma_load_2d(smem + k * kBoxRows * 2 * C, a.tmap, tq, tr + k * kBoxRows, &tbar);
+#endif
             if constexpr (kTgt || kSB) {
                 mbar_init(&gbar, 1);
+#if HG_COL_NOMEM
+                mbar_arrive_plain(&gbar);
+#else
                 const float* src = kTgt ? a.target + a.t_bstride * b : a.S + a.S_bstride * b;
                 bulk_g2s(tsm, src + colpair_index(bx * C, 0, NY), (uint32_t)ColTgtBulk<NY, C, LAY, MODE>::BYTES,
                          &gbar);
+#endif
             }
         }
         __syncthreads();  // barrier initialised before anyone waits
@@ -610,7 +621,7 @@ __device__ __forceinline__ void col_cta(const ColArgs& a, const int bx, const in
             for (int e = 0; e < E; ++e) smem[Tma::slot(c, t + e * T)] = v[e];
             fence_proxy_async();
             __syncthreads();
-            if (threadIdx.x == 0) {
+            if (threadIdx.x == 0 && !HG_COL_NOMEM) {
 #pragma unroll 1
                 for (int k = 0; k < kBoxes; ++k)
                     tma_store_2d(a.tmap, tq, tr + k * kBoxRows, smem + k * kBoxRows * 2 * C);

@@ -46,6 +46,11 @@ struct hgc_ifta_plan {
     // after its row pass of iteration k, kev[2k] after its column pass.
     bool ktime = false;
     std::vector<cudaEvent_t> kev;
+    // HG_STAGGER=1 (experiment): the batch as two halves on two
+    // streams of the graph, staggered by a pass, so half B's row pass runs beside
+    // half A's column pass and vice versa.
+    cudaStream_t sB = nullptr;
+    cudaEvent_t evA = nullptr, evB = nullptr, evF = nullptr;
     int group0 = 0;  // targets of the first (timed) group
 
     // RunReport::profile (report.hpp:38-45) of a run of `seconds`: the device
@@ -87,6 +92,9 @@ struct hgc_ifta_plan {
 
     ~hgc_ifta_plan() {
         for (cudaEvent_t e : kev) cudaEventDestroy(e);
+        for (cudaEvent_t e : {evA, evB, evF})
+            if (e) cudaEventDestroy(e);
+        if (sB) cudaStreamDestroy(sB);
         if (graph) cudaGraphExecDestroy(graph);
         if (done) cudaEventDestroy(done);
         if (up_ev) cudaEventDestroy(up_ev);
@@ -258,6 +266,37 @@ struct hgc_ifta_plan {
         // passes and successive iterations (126 MB L2 on B200).  (Running two
         // target halves on concurrent streams, staggered by a pass, measured
         // no gain at 4096^2: 3927 vs 3950 it/s.)
+        const char* stg = getenv("HG_STAGGER");
+        if (stg && atoi(stg) != 0 && batch >= 2 && !ktime) {
+            if (!sB) {
+                CK(cudaStreamCreateWithFlags(&sB, cudaStreamNonBlocking));
+                CK(cudaEventCreateWithFlags(&evA, cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&evB, cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&evF, cudaEventDisableTiming));
+            }
+            const int hA = batch / 2, hB = batch - hA;
+            CK(cudaEventRecord(evF, st));
+            CK(cudaStreamWaitEvent(sB, evF, 0));
+            for (int k = 1; k <= cfg.iterations; ++k) {
+                row_fused(nx, row_args_g(k, 0), hA, st);
+                CK(cudaEventRecord(evA, st));          // A's row pass done
+                CK(cudaStreamWaitEvent(sB, evA, 0));   // B's row pass beside A's column pass
+                col_gs(ny, col_args_g(k, 0), hA, st);
+                row_fused(nx, row_args_g(k, hA), hB, sB);
+                CK(cudaEventRecord(evB, sB));          // B's row pass done
+                CK(cudaStreamWaitEvent(st, evB, 0));   // A's next row pass beside B's column pass
+                col_gs(ny, col_args_g(k, hA), hB, sB);
+                launches += 4;
+            }
+            CK(cudaEventRecord(evF, sB));
+            CK(cudaStreamWaitEvent(st, evF, 0));
+            group0 = batch;
+            k_finalize<<<batch, 32, 0, st>>>(partials.p, cfg.iterations, batch, tiles, (double)M, cfg.freedom_scale, 0,
+                                             trace.p, stt.p, eff.p);
+            ++launches;
+            CK(cudaGetLastError());
+            return;
+        }
         const int G = group_size();
         group0 = std::min(G, batch);
         const bool tk = ktime && (int)kev.size() == 2 * cfg.iterations + 1;

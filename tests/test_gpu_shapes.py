@@ -50,3 +50,17 @@ def test_ospr_shapes_match_oracle(oracle, ny, nx, N):
     ref = oracle.ospr(amp, hg.SlmSpec.binary_phase(), N, seed=5)
     assert level_mismatches(run.set.levels, ref.levels).sum() <= N * max(1, nx * ny // 20000)
     assert np.max(np.abs(run.report.trace.values() - ref.cumulative_mse) / ref.cumulative_mse) < 1e-4
+
+
+def test_staggered_halves_equal_single_graph(monkeypatch):
+    """HG_STAGGER=1 (experiment: the batch's two halves on two graph branches,
+    staggered by a pass) gives the same levels and traces bit for bit."""
+    amp = hg.patterns.bench_target(1024)
+    amps = np.stack([np.roll(amp, 37 * t, axis=1) for t in range(4)])
+    cfg = hg.IftaConfig(iterations=5, slm=hg.SlmSpec.full_circle_phase(256), target=hg.TargetSpec(amp), seed=1)
+    out = {}
+    for m in ("0", "1"):
+        monkeypatch.setenv("HG_STAGGER", m)
+        reps = hg.run_ifta_batch(cfg, amps, seeds=[1, 2, 3, 4])
+        out[m] = (np.stack([r.levels for r in reps]), np.stack([r.trace.values() for r in reps]))
+    assert np.array_equal(out["0"][0], out["1"][0]) and np.array_equal(out["0"][1], out["1"][1])
